@@ -1,0 +1,12 @@
+#!/usr/bin/env bash
+# Regenerates the golden fixtures under tests/golden/ from the UNMODIFIED
+# reference (compiled in place by oracle/Makefile into oracle/_ref/).
+# Requires /root/reference (this container only).
+set -euo pipefail
+here="$(cd "$(dirname "$0")" && pwd)"
+repo="$(cd "$here/../.." && pwd)"
+make -C "$repo/oracle" ref
+for d in rng pack gate feedback update_clause epoch_par_w1 epoch_seq inference; do
+  rm -rf "$here/$d"
+done
+"$repo/oracle/_ref/ref_driver" golden "$here"
