@@ -1,0 +1,333 @@
+#!/usr/bin/env python3
+"""Benchmark of the asynchronous clause-parallel Tsetlin Machine on B200.
+
+Workload (BASELINE.json configs[1]): MNIST-shaped synthetic data, 784 bits x
+10 classes, 2000 clauses per class per GPU, T=50, s=10, 8-bit automata
+(N=128), q=60,000 training examples (synthetic, generated in-process).
+
+One step = one asynchronous training epoch (Algorithm 1) of a FRESH machine
+(reset to counters=N, tallies and previous outputs 0, epoch index 0) over all
+q examples — the most expensive epoch, and identical work every step.
+
+  value : clause-literal evals/s = m * n_total * q * 2o / step time, inputs
+          resident in HBM, CUDA events on the engine's stream, max over ranks
+  e2e   : the same through the C ABI with HOST buffers: per step the pinned
+          host bits/labels are copied in (tmg_pool_create), the machine is
+          reset, the epoch runs, the per-class feedback-event report is read
+          back.
+Multi-GPU (torchrun): weak scaling in clauses — every rank owns 2000 clauses
+per class (global n = 2000 * world), tally deltas are all-reduced with NCCL
+every window (paper_2009_04861_b200/distributed.py).
+
+--impl reference times the UNMODIFIED reference (oracle/_ref/ref_driver, the
+reference sources compiled with their own Release flags) on the host cores:
+train_epoch_parallel with all hardware threads, fresh epoch 0 per step, on a
+bounded q-prefix sample of the same data.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+O_FEAT, M_CLS, N_CLAUSES, MARGIN, SPEC, STATE_N = 784, 10, 2000, 50, 10.0, 128
+Q_TRAIN, Q_TEST = 60000, 10000
+DATA_SEED, TM_SEED = 2009, 42
+REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+METRIC = "clause-literal evals/s (async training epoch, MNIST-shaped 784b x 10c x 2000 clauses)"
+UNIT = "clause-literal evals/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(
+        os.environ.get("LOCAL_RANK", 0))
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.samples, self.proc = device, [], None
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(
+            ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+             "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([f.strip() for f in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if len(s) >= 7 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 7 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples if len(s) >= 7 for k in range(4)
+                          if s[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------- reference arm ---
+def ref_driver_run(q_use: int, steps: int, workers: int) -> list:
+    args = [REF_DRIVER, "train", "--data", "mnist", "--q", str(q_use), "--qtest", "0", "--clauses",
+            str(N_CLAUSES), "--T", str(MARGIN), "--s", str(SPEC), "--N", str(STATE_N), "--epochs",
+            str(steps), "--workers", str(workers), "--seed", str(TM_SEED), "--data-seed", str(DATA_SEED),
+            "--eval", "0", "--fresh", "1"]
+    out = subprocess.run(args, check=True, capture_output=True, text=True).stdout
+    return [json.loads(l) for l in out.splitlines() if l.strip()]
+
+
+def cpu_sample_size(cores: int, budget_s: float) -> int:
+    # ~17 examples/s per core at this shape on epoch 0; calibrate.
+    probe_q = 200
+    rows = ref_driver_run(probe_q, 1, cores)
+    per_ex = rows[0]["seconds"] / probe_q
+    return int(max(200, min(Q_TRAIN, budget_s / max(per_ex, 1e-6))))
+
+
+def evals(q: int, n_total: int) -> float:
+    return float(M_CLS) * n_total * q * 2 * O_FEAT
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    if not os.path.exists(REF_DRIVER):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_driver not built"}))
+        return 0
+    cores = os.cpu_count() or 1
+    per_step_budget = max(3.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    q_use = cpu_sample_size(cores, per_step_budget)
+    rows = ref_driver_run(q_use, args.warmup + args.steps, cores)[args.warmup:]
+    secs = [r["seconds"] for r in rows]
+    t = max(statistics.mean(secs), 1e-9)
+    value = evals(q_use, N_CLAUSES) / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "mnist-784b-10c-2000cl fresh epoch 0", "q_sample": q_use, "q_full": Q_TRAIN,
+                   "clauses_per_class": N_CLAUSES, "T": MARGIN, "s": SPEC, "state_bits": 8},
+        "examples_per_s": q_use / t,
+        "feedback_events_per_step": statistics.mean(r["feedback_events"] for r in rows),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"fresh-model epoch 0 on the first {q_use} of {Q_TRAIN} training rows, "
+                                   f"train_epoch_parallel(workers={cores})"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ----------------------------------------------------------------- ours ---
+def algorithmic_ops(steps_per_epoch: int, events: int, type1: int) -> float:
+    """SURVEY.md §8(d) cost model (fixed up front): gate = 1 draw (~15 int ops)
+    + 3; per event 2*ceil(2o/32) LOP3 of evaluation; Type I = 2o TA updates of
+    (1 draw + 3); Type II = 2o TA updates of 3."""
+    L = 2 * O_FEAT
+    w32 = (L + 31) // 32
+    return 18.0 * steps_per_epoch + events * 2.0 * w32 + type1 * L * 18.0 + (events - type1) * L * 3.0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2009_04861_b200 as T
+    from paper_2009_04861_b200 import distributed as D
+    from paper_2009_04861_b200 import synth
+    from paper_2009_04861_b200.tsetlin import int_peak, kernel_launches, machine_stream
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    d = synth.make("mnist", Q_TRAIN, Q_TEST, DATA_SEED)
+    n_total = N_CLAUSES * world
+    jb, je = D.shard_range(n_total, rank, world)
+    cfg = T.TMConfig(clauses=n_total, margin=MARGIN, specificity=SPEC, state_depth=STATE_N, seed=TM_SEED)
+    tm = T.MultiClassTM(cfg, O_FEAT, M_CLS, device=local, clause_range=(jb, je) if world > 1 else None)
+    # Resident inputs: bits/labels already in HBM (torch allocations), packed on device.
+    d_bits = torch.from_numpy(d.train_x).to(f"cuda:{local}")
+    d_lab = torch.from_numpy(d.train_y).to(f"cuda:{local}")
+    pool = T.ExamplePool.from_device(O_FEAT, d_bits.data_ptr(), d_lab.data_ptr(), Q_TRAIN, M_CLS, device=local,
+                                     labels_host=d.train_y)
+    stream = torch.cuda.ExternalStream(machine_stream(tm), device=f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")  # > 126 MB L2
+    allreduce = D.nccl_allreduce(local) if world > 1 else None
+    windows = args.windows
+
+    def one_epoch(p):
+        tm.reset()
+        p.reset_tallies()
+        if world == 1:
+            rep = T.train_epoch_parallel(tm, p, 1, 0)
+            return rep.feedback_events, rep.type_i_events, rep.device_seconds
+        ev = D.train_epoch_windows(tm, p, 0, windows, allreduce)
+        return ev, None, None
+
+    # ---- integer-pipe peak (roofline denominator), measured on this GPU
+    lop3_peak, mixed_peak = int_peak(local)
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        one_epoch(pool)
+    torch.cuda.synchronize()
+
+    # ---- timed: inputs resident
+    clocks = ClockSampler(local) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    step_ms, kern_s, events, type1 = [], [], [], []
+    launches0 = kernel_launches()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ev, t1, ks = one_epoch(pool)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        step_ms.append(max_over_ranks(e0.elapsed_time(e1)))
+        events.append(sum(ev))
+        if t1 is not None:
+            type1.append(sum(t1))
+            kern_s.append(ks)
+    launches = kernel_launches() - launches0
+    clk = clocks.stop() if clocks else None
+
+    # ---- e2e: host buffers through the C ABI, copies inside the timed region
+    host_bits = torch.from_numpy(d.train_x).pin_memory().numpy()
+    host_lab = torch.from_numpy(d.train_y).pin_memory().numpy()
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        p2 = T.ExamplePool(O_FEAT, host_bits, host_lab, M_CLS, device=local)
+        ev, _, _ = one_epoch(p2)
+        _ = [int(v) for v in ev]  # per-class report read back to the host
+        del p2
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms.append(max_over_ranks((time.perf_counter() - t0) * 1e3))
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    ms = statistics.mean(step_ms)
+    value = evals(Q_TRAIN, n_total) / (ms * 1e-3)
+    e2e_val = evals(Q_TRAIN, n_total) / (statistics.mean(e2e_ms) * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": "mnist-784b-10c-2000cl fresh epoch 0", "q": Q_TRAIN,
+                   "clauses_per_class_per_gpu": N_CLAUSES, "clauses_per_class_total": n_total,
+                   "T": MARGIN, "s": SPEC, "state_bits": 8, "parallelism": f"clause-shard{world}",
+                   "windows": windows if world > 1 else 1,
+                   "l2": "flushed (256 MB write) between timed steps; working set (prev bits 150 MB) > L2"},
+        "examples_per_s": Q_TRAIN / (ms * 1e-3),
+        "feedback_events_per_step": statistics.mean(events),
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    # ---- roofline of the dominant kernel (train_async), INT issue bound
+    if kern_s:
+        ops = algorithmic_ops(M_CLS * N_CLAUSES * Q_TRAIN, int(statistics.mean(events)),
+                              int(statistics.mean(type1)))
+        k = statistics.mean(kern_s)
+        traffic = None
+        tpath = os.path.join(REPO, "profiles", "train_async_dram_bytes.json")
+        if os.path.exists(tpath):
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        line["roofline"] = {"bound": "int-alu", "achieved": ops / k / 1e12, "peak": mixed_peak / 1e12,
+                            "unit": "Tops/s", "frac": ops / k / mixed_peak, "traffic": traffic,
+                            "kernel": "train_async_kernel<1,8>", "kernel_ms": k * 1e3,
+                            "kernel_share_of_step": k * 1e3 / ms,
+                            "peak_source": "measured on this GPU by tmg_bench_int_peak (LOP3+IMAD issue); "
+                                           f"LOP3-only {lop3_peak / 1e12:.2f} Tops/s",
+                            "ops_model": "SURVEY.md 8(d): gate 18, eval 2*ceil(2o/32), TypeI 2o*18, TypeII 2o*3"}
+    line["e2e"] = {"value": e2e_val, "unit": UNIT, "ms_per_step": statistics.mean(e2e_ms),
+                   "h2d_bytes_per_step": int(host_bits.nbytes + host_lab.nbytes + 4 * Q_TRAIN),
+                   "d2h_bytes_per_step": int(8 * M_CLS * 2)}
+    # ---- CPU reference beside it (rank 0, N=1 only)
+    if world == 1 and not args.no_cpu and os.path.exists(REF_DRIVER):
+        cores = os.cpu_count() or 1
+        q_use = cpu_sample_size(cores, 15.0)
+        rows = ref_driver_run(q_use, 1, cores)
+        t = rows[0]["seconds"]
+        line["cpu_baseline"] = {"value": evals(q_use, N_CLAUSES) / t, "unit": UNIT, "cores": cores,
+                                "kind": "reference", "examples_per_s": q_use / t,
+                                "sample": f"fresh-model epoch 0 on the first {q_use} of {Q_TRAIN} rows, "
+                                          f"reference train_epoch_parallel(workers={cores}), "
+                                          f"{rows[0]['feedback_events']} feedback events"}
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--windows", type=int, default=64, help="tally all-reduce windows per epoch (N>1)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -435,7 +435,7 @@ void golden_inference(const std::string& dir) {
 struct Args {
   std::string data = "mnist", mode = "par";
   std::int64_t q = 60000, qt = 10000, q_use = -1, qt_use = -1;
-  int n = 2000, margin = 50, N = 128, boost = 0, epochs = 1, workers = 0, eval = 1;
+  int n = 2000, margin = 50, N = 128, boost = 0, epochs = 1, workers = 0, eval = 1, fresh = 0;
   double s = 10.0, noise = 0.0;
   std::uint64_t seed = 42, data_seed = 2009;
 };
@@ -465,6 +465,7 @@ Args parse(int argc, char** argv, int start) {
     else if (key == "--data-seed") a.data_seed = std::stoull(val());
     else if (key == "--noise") a.noise = std::stod(val());
     else if (key == "--eval") a.eval = std::stoi(val());
+    else if (key == "--fresh") a.fresh = std::stoi(val());
     else throw std::invalid_argument("unknown flag " + key);
   }
   return a;
@@ -496,7 +497,14 @@ int cmd_train(const Args& a) {
   ExamplePool pool(d.features, tx, ty, d.classes);
   ExamplePool test(d.features, vx, vy, d.classes);
   for (int e = 0; e < a.epochs; ++e) {
-    EpochReport rep = a.mode == "seq" ? train_epoch_sequential(tm, pool, e) : train_epoch_parallel(tm, pool, W, e);
+    int epoch = e;
+    if (a.fresh) {  // every step = epoch 0 of a fresh machine and pool
+      tm = MultiClassTM(cfg, d.features, d.classes);
+      pool.reset_tallies();
+      epoch = 0;
+    }
+    EpochReport rep = a.mode == "seq" ? train_epoch_sequential(tm, pool, epoch)
+                                      : train_epoch_parallel(tm, pool, W, epoch);
     double acc = -1.0, pred_s = 0.0;
     if (a.eval && qtu > 0) {
       const auto t0 = std::chrono::steady_clock::now();

@@ -1,0 +1,1102 @@
+// engine.cu — host runtime of the B200 Tsetlin engine and the C ABI
+// (include/tmgpu.h). Owns device memory, one CUDA stream per machine/pool,
+// the epoch orchestration (permutation, Philox keys, thresholds) and the
+// conversions between the reference's host layouts and the device layouts.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "tmgpu.h"
+#include "tmgpu_rng.h"
+
+#define TMG_API extern "C" __attribute__((visibility("default")))
+
+namespace tmg {
+unsigned long long g_launches = 0;
+}
+
+namespace {
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+thread_local std::string g_last_error;
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(TMG_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TMG_OK;
+  } catch (const Error& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "out of host memory";
+    return TMG_ERUNTIME;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TMG_ERUNTIME;
+  }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) CK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  void alloc(size_t n) {
+    release();
+    if (n) CK(cudaMalloc(&ptr, n * sizeof(T)));
+    count = n;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  size_t bytes() const { return count * sizeof(T); }
+};
+
+// Supported words-per-lane instantiations of the training kernels.
+int round_nw(int nw) {
+  static const int kNW[] = {1, 2, 3, 4, 8, 10};
+  for (int v : kNW)
+    if (nw <= v) return v;
+  fail(TMG_EINVAL, "feature count too large for the register-resident clause kernels (max 10240)");
+}
+
+int planes_for(int N) {
+  // 2^(B-1) >= N so Include is the top plane; instantiated B in {4, 8, 15}.
+  if (N <= 8) return 4;
+  if (N <= 128) return 8;
+  return 15;
+}
+
+uint32_t prob_threshold(double p) {  // P(u < p) as 32-bit fixed point
+  if (!(p > 0.0)) return 0u;
+  const double v = std::ldexp(p, 32);
+  if (v >= 4294967295.0) return 0xFFFFFFFFu;
+  return static_cast<uint32_t>(std::llround(v));
+}
+
+}  // namespace
+
+struct tmg_pool {
+  int device = 0;
+  int o = 0, m = 0, Wp = 0;
+  int64_t q = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf<uint32_t> xplane, nplane;
+  DevBuf<int32_t> labels, tallies, delta, order;
+  std::vector<int32_t> host_labels;
+};
+
+struct tmg_machine {
+  tmg_config cfg{};
+  int o = 0, m = 0, n = 0, j_begin = 0, j_end = 0, n_loc = 0;
+  int N = 0, B = 0, NW = 0, Wx = 0, Wp = 0, Wq = 0;
+  int device = 0;
+  int64_t q_bound = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DevBuf<uint32_t> state, prev;
+  DevBuf<int32_t> inc_count, nentries, sums;
+  DevBuf<tmg::EvalEntry> entries;
+  DevBuf<unsigned long long> events;
+  DevBuf<uint16_t> scratch16;
+  bool entries_dirty = true;
+  // current async epoch
+  int32_t cur_epoch = -1;
+  uint32_t key0 = 0, key1 = 0;
+  int clauses() const { return m * n_loc; }
+};
+
+namespace {
+
+void validate_config(const tmg_config& c) {  // core.cpp:48-74
+  if (c.clauses < 2 || c.clauses % 2 != 0)
+    fail(TMG_EINVAL, "clauses must be even and >= 2, got " + std::to_string(c.clauses));
+  if (c.margin < 1) fail(TMG_EINVAL, "margin must be >= 1, got " + std::to_string(c.margin));
+  if (!(c.specificity >= 1.0)) fail(TMG_EINVAL, "specificity must be >= 1, got " + std::to_string(c.specificity));
+  if (c.state_depth < 1) fail(TMG_EINVAL, "state depth must be >= 1, got " + std::to_string(c.state_depth));
+  if (c.state_depth > 16383) fail(TMG_EINVAL, "state depth too large for 16-bit counters");
+  if (c.epochs < 0) fail(TMG_EINVAL, "epochs must be >= 0");
+  if (c.workers < 0) fail(TMG_EINVAL, "workers must be >= 0 (0 = auto)");
+}
+
+int words_x(int o) { return (o + 31) / 32; }
+int wp_for(int o) { return 32 * round_nw((words_x(o) + 31) / 32); }
+
+void check_compatible(const tmg_machine* tm, const tmg_pool* pool) {  // trainer.cpp:46-53
+  if (!tm || !pool) fail(TMG_EINVAL, "null handle");
+  if (tm->o != pool->o) fail(TMG_EINVAL, "model/pool feature count mismatch");
+  if (tm->m != pool->m) fail(TMG_EINVAL, "model/pool class count mismatch");
+  if (tm->device != pool->device) fail(TMG_EINVAL, "model and pool live on different devices");
+}
+
+void bind(tmg_machine* tm, int64_t q) {  // core.cpp:117-126
+  if (q < 0) fail(TMG_EINVAL, "example count must be >= 0");
+  if (q > (int64_t(1) << 31) - 64) fail(TMG_EINVAL, "example count too large");
+  tm->q_bound = q;
+  tm->Wq = static_cast<int>(2 * ((q + 63) / 64));
+  tm->prev.alloc(static_cast<size_t>(tm->clauses()) * tm->Wq);
+  if (tm->prev.bytes()) CK(cudaMemsetAsync(tm->prev.ptr, 0, tm->prev.bytes(), tm->stream));
+  CK(cudaStreamSynchronize(tm->stream));
+}
+
+void rebuild_entries(tmg_machine* tm) {
+  if (!tm->entries_dirty) return;
+  tmg::build_entries_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx, tm->entries.ptr,
+                            tm->nentries.ptr, tm->inc_count.ptr, tm->stream);
+  CK(cudaGetLastError());
+  tm->entries_dirty = false;
+}
+
+void reset_state(tmg_machine* tm) {  // ClassBank ctor: counters = N (core.cpp:96-100)
+  tmg::init_state_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->stream);
+  CK(cudaGetLastError());
+  if (tm->prev.bytes()) CK(cudaMemsetAsync(tm->prev.ptr, 0, tm->prev.bytes(), tm->stream));
+  CK(cudaMemsetAsync(tm->inc_count.ptr, 0, tm->inc_count.bytes(), tm->stream));
+  tm->entries_dirty = true;
+  CK(cudaStreamSynchronize(tm->stream));
+}
+
+tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int jb, int je) {
+  if (!cfg) fail(TMG_EINVAL, "null config");
+  validate_config(*cfg);
+  if (m < 1) fail(TMG_EINVAL, "class count must be >= 1");
+  if (o < 1) fail(TMG_EINVAL, "feature count must be >= 1");
+  if (jb < 0 || je > cfg->clauses || jb >= je || (jb % 2) || (je % 2))
+    fail(TMG_EINVAL, "clause shard must be a non-empty even-aligned sub-range of [0, clauses)");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) fail(TMG_EINVAL, "no such CUDA device " + std::to_string(device));
+  DeviceGuard dg(device);
+  auto tm = new tmg_machine();
+  try {
+    tm->cfg = *cfg;
+    tm->o = o;
+    tm->m = m;
+    tm->n = cfg->clauses;
+    tm->j_begin = jb;
+    tm->j_end = je;
+    tm->n_loc = je - jb;
+    tm->N = cfg->state_depth;
+    tm->B = planes_for(tm->N);
+    tm->Wx = words_x(o);
+    tm->Wp = wp_for(o);
+    tm->NW = tm->Wp / 32;
+    tm->device = device;
+    CK(cudaStreamCreateWithFlags(&tm->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&tm->ev0));
+    CK(cudaEventCreate(&tm->ev1));
+    const size_t cl = static_cast<size_t>(tm->clauses());
+    tm->state.alloc(cl * tm->B * 2 * tm->Wp);
+    tm->inc_count.alloc(cl);
+    tm->nentries.alloc(cl);
+    tm->entries.alloc(cl * tm->Wx);
+    tm->events.alloc(2 * static_cast<size_t>(m));  // all events, then Type I events
+    bind(tm, 0);
+    reset_state(tm);
+  } catch (...) {
+    tmg_machine_destroy(tm);
+    throw;
+  }
+  return tm;
+}
+
+void upload_order(tmg_machine* tm, tmg_pool* pool, int32_t epoch) {
+  // The epoch permutation of train_epoch_parallel (trainer.cpp:196-198).
+  tmg_rng r;
+  tmg_rng_seed(&r, tm->cfg.seed, tmg_mix_stream(TMG_STREAM_PERMUTATION, static_cast<uint64_t>(epoch), 0));
+  std::vector<int32_t> order(static_cast<size_t>(pool->q));
+  tmg_shuffled_indices(static_cast<int32_t>(pool->q), &r, order.data());
+  CK(cudaMemcpyAsync(pool->order.ptr, order.data(), order.size() * 4, cudaMemcpyHostToDevice, tm->stream));
+  CK(cudaStreamSynchronize(tm->stream));
+}
+
+tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
+  tmg::TrainParams p{};
+  p.state = tm->state.ptr;
+  p.inc_count = tm->inc_count.ptr;
+  p.prev = tm->prev.ptr;
+  p.n = tm->n;
+  p.n_loc = tm->n_loc;
+  p.j_begin = tm->j_begin;
+  p.m = tm->m;
+  p.o = tm->o;
+  p.Wp = tm->Wp;
+  p.Wq = tm->Wq;
+  p.lo = (1u << (tm->B - 1)) - static_cast<uint32_t>(tm->N);
+  p.hi = (1u << (tm->B - 1)) + static_cast<uint32_t>(tm->N) - 1u;
+  p.xplane = pool->xplane.ptr;
+  p.nplane = pool->nplane.ptr;
+  p.labels = pool->labels.ptr;
+  p.tallies = pool->tallies.ptr;
+  p.tally_delta = nullptr;
+  p.q = pool->q;
+  p.order = pool->order.ptr;
+  p.margin = tm->cfg.margin;
+  p.boost = tm->cfg.boost_true_positive ? 1 : 0;
+  const double s = tm->cfg.specificity;
+  p.thr_high = prob_threshold((s - 1.0) / s);
+  p.thr_low = prob_threshold(1.0 / s);
+  p.key0 = tm->key0;
+  p.key1 = tm->key1;
+  p.t_begin = 0;
+  p.t_end = pool->q;
+  p.events = tm->events.ptr;
+  return p;
+}
+
+void epoch_keys(tmg_machine* tm, int32_t epoch) {
+  // Philox key per (seed, epoch); stream kind 4 is disjoint from the
+  // reference's kinds 1-3 (trainer.cpp:29-31).
+  const uint64_t k = tmg_mix_stream(4, static_cast<uint64_t>(epoch), tm->cfg.seed);
+  tm->key0 = static_cast<uint32_t>(k);
+  tm->key1 = static_cast<uint32_t>(k >> 32);
+  tm->cur_epoch = epoch;
+}
+
+void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, bool with_delta) {
+  tmg::TrainParams p = make_params(tm, pool);
+  p.t_begin = t0;
+  p.t_end = t1;
+  if (with_delta) p.tally_delta = pool->delta.ptr;
+  int blocks = 0;
+  if (!tmg::train_async_launch(p, tm->B, tm->NW, tm->stream, &blocks))
+    fail(TMG_ERUNTIME, "no async kernel instantiation for this shape");
+  CK(cudaGetLastError());
+  tm->entries_dirty = true;
+}
+
+std::vector<int32_t> class_sums_device(tmg_machine* tm, const uint32_t* xplane, const uint32_t* nplane,
+                                       int64_t q, bool train_mode, int32_t* d_out, uint32_t* prev) {
+  rebuild_entries(tm);
+  tmg::EvalParams e{};
+  e.entries = tm->entries.ptr;
+  e.nentries = tm->nentries.ptr;
+  e.inc_count = tm->inc_count.ptr;
+  e.prev = prev;
+  e.n_loc = tm->n_loc;
+  e.j_begin = tm->j_begin;
+  e.m = tm->m;
+  e.Wx = tm->Wx;
+  e.Wp = tm->Wp;
+  e.Wq = tm->Wq;
+  e.xplane = xplane;
+  e.nplane = nplane;
+  e.q = q;
+  e.sums = d_out;
+  // Enough CTAs for several waves over 148 SMs.
+  const int64_t tiles = (q + 127) / 128;
+  int chunks = static_cast<int>(std::max<int64_t>(1, (148 * 8 + tiles * tm->m - 1) / (tiles * tm->m)));
+  chunks = std::min(chunks, std::max(1, tm->n_loc / 8));
+  e.chunk = (tm->n_loc + chunks - 1) / chunks;
+  CK(cudaMemsetAsync(d_out, 0, static_cast<size_t>(q) * tm->m * 4, tm->stream));
+  tmg::eval_sums_launch(e, train_mode, tm->stream);
+  CK(cudaGetLastError());
+  return {};
+}
+
+void ensure_sums(tmg_machine* tm, int64_t q) {
+  if (tm->sums.count < static_cast<size_t>(q) * tm->m) tm->sums.alloc(static_cast<size_t>(q) * tm->m);
+}
+
+tmg_pool* create_pool_common(int device, int o, int64_t q, int m) {
+  if (o < 1) fail(TMG_EINVAL, "feature count must be >= 1");
+  if (m < 1) fail(TMG_EINVAL, "class count must be >= 1");
+  if (q <= 0) fail(TMG_EINVAL, "example pool must not be empty");
+  if (q > (int64_t(1) << 31) - 64) fail(TMG_EINVAL, "example pool too large");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) fail(TMG_EINVAL, "no such CUDA device " + std::to_string(device));
+  auto pool = new tmg_pool();
+  pool->device = device;
+  pool->o = o;
+  pool->m = m;
+  pool->q = q;
+  pool->Wp = wp_for(o);
+  return pool;
+}
+
+void finish_pool(tmg_pool* pool, const uint8_t* d_bits, const int32_t* d_labels) {
+  const size_t rows = static_cast<size_t>(pool->q);
+  pool->xplane.alloc(rows * pool->Wp);
+  pool->nplane.alloc(rows * pool->Wp);
+  pool->labels.alloc(rows);
+  pool->tallies.alloc(rows * pool->m);
+  pool->delta.alloc(rows * pool->m);
+  pool->order.alloc(rows);
+  tmg::pack_planes_launch(d_bits, pool->xplane.ptr, pool->nplane.ptr, pool->q, pool->o, pool->Wp, pool->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(pool->labels.ptr, d_labels, rows * 4, cudaMemcpyDeviceToDevice, pool->stream));
+  CK(cudaMemsetAsync(pool->tallies.ptr, 0, pool->tallies.bytes(), pool->stream));  // pool.cpp:71
+  CK(cudaMemsetAsync(pool->delta.ptr, 0, pool->delta.bytes(), pool->stream));
+  CK(cudaStreamSynchronize(pool->stream));
+}
+
+void validate_inputs_host(const uint8_t* bits, const int32_t* labels, int64_t q, int o, int m) {
+  // ExamplePool ctor checks (pool.cpp:40-55).
+  const size_t total = static_cast<size_t>(q) * static_cast<size_t>(o);
+  for (size_t k = 0; k < total; ++k)
+    if (bits[k] > 1) fail(TMG_EINVAL, "inputs must be 0/1");
+  if (m > 1)
+    for (int64_t i = 0; i < q; ++i)
+      if (labels[i] < 0 || labels[i] >= m)
+        fail(TMG_EINVAL, "label " + std::to_string(labels[i]) + " outside [0, " + std::to_string(m) + ")");
+}
+
+tmg_machine* M(tmg_machine* tm) {
+  if (!tm) fail(TMG_EINVAL, "null machine handle");
+  return tm;
+}
+const tmg_machine* M(const tmg_machine* tm) {
+  if (!tm) fail(TMG_EINVAL, "null machine handle");
+  return tm;
+}
+
+void check_bank(const tmg_machine* tm, int32_t bank) {
+  if (bank < 0 || bank >= tm->m) fail(TMG_ERANGE, "bank index out of range");
+}
+
+}  // namespace
+
+// ===================================================================== ABI ===
+
+TMG_API int tmg_abi_version(void) { return TMG_ABI_VERSION; }
+TMG_API const char* tmg_last_error(void) { return g_last_error.c_str(); }
+
+TMG_API int tmg_device_count(int32_t* count) {
+  return guarded([&] {
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    *count = n;
+  });
+}
+
+TMG_API void tmg_config_default(tmg_config* cfg) {
+  cfg->clauses = 100;
+  cfg->margin = 15;
+  cfg->specificity = 3.0;
+  cfg->state_depth = 128;
+  cfg->boost_true_positive = 0;
+  cfg->epochs = 100;
+  cfg->workers = 0;
+  cfg->seed = 42;
+}
+
+TMG_API int tmg_config_validate(const tmg_config* cfg) {
+  return guarded([&] {
+    if (!cfg) fail(TMG_EINVAL, "null config");
+    validate_config(*cfg);
+  });
+}
+
+TMG_API int32_t tmg_effective_workers(const tmg_config* cfg) {
+  if (cfg->workers > 0) return cfg->workers;
+  return 1;  // the GPU engine's parallelism is the device, not host threads
+}
+
+TMG_API int tmg_machine_create(const tmg_config* cfg, int32_t o, int32_t m, int32_t device, tmg_machine** out) {
+  return guarded([&] { *out = create_machine(cfg, o, m, device, 0, cfg ? cfg->clauses : 0); });
+}
+
+TMG_API int tmg_machine_create_shard(const tmg_config* cfg, int32_t o, int32_t m, int32_t device, int32_t jb,
+                                     int32_t je, tmg_machine** out) {
+  return guarded([&] { *out = create_machine(cfg, o, m, device, jb, je); });
+}
+
+TMG_API int tmg_machine_destroy(tmg_machine* tm) {
+  if (!tm) return TMG_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(tm->device);
+  if (tm->stream) cudaStreamSynchronize(tm->stream);
+  tm->state.release();
+  tm->prev.release();
+  tm->inc_count.release();
+  tm->nentries.release();
+  tm->sums.release();
+  tm->entries.release();
+  tm->events.release();
+  tm->scratch16.release();
+  if (tm->ev0) cudaEventDestroy(tm->ev0);
+  if (tm->ev1) cudaEventDestroy(tm->ev1);
+  if (tm->stream) cudaStreamDestroy(tm->stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete tm;
+  return TMG_OK;
+}
+
+TMG_API int tmg_machine_info_get(const tmg_machine* tm, tmg_machine_info* info) {
+  return guarded([&] {
+    M(tm);
+    info->feature_count = tm->o;
+    info->num_classes = tm->m;
+    info->clauses = tm->n;
+    info->state_depth = tm->N;
+    info->clause_begin = tm->j_begin;
+    info->clause_end = tm->j_end;
+    info->planes = tm->B;
+    info->words_per_lane = tm->NW;
+    info->bound_examples = static_cast<int32_t>(tm->q_bound);
+    info->device = tm->device;
+    info->device_bytes = tm->state.bytes() + tm->prev.bytes() + tm->inc_count.bytes() + tm->entries.bytes() +
+                         tm->nentries.bytes() + tm->sums.bytes();
+  });
+}
+
+TMG_API int tmg_machine_config(const tmg_machine* tm, tmg_config* cfg) {
+  return guarded([&] { *cfg = M(tm)->cfg; });
+}
+
+TMG_API int tmg_machine_reset(tmg_machine* tm) {
+  return guarded([&] {
+    DeviceGuard dg(M(tm)->device);
+    reset_state(tm);
+  });
+}
+
+TMG_API int tmg_get_counters(const tmg_machine* ctm, int32_t bank, uint16_t* out) {
+  return guarded([&] {
+    auto tm = const_cast<tmg_machine*>(M(ctm));
+    check_bank(tm, bank);
+    DeviceGuard dg(tm->device);
+    const size_t count = static_cast<size_t>(tm->n_loc) * 2 * tm->o;
+    if (tm->scratch16.count < count) tm->scratch16.alloc(count);
+    tmg::planes_to_counters_launch(tm->state.ptr + static_cast<size_t>(bank) * tm->n_loc * tm->B * 2 * tm->Wp,
+                                   tm->scratch16.ptr, tm->n_loc, tm->o, tm->B, tm->Wp, tm->N, tm->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tm->scratch16.ptr, count * 2, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_set_counters(tmg_machine* tm, int32_t bank, const uint16_t* in) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    DeviceGuard dg(tm->device);
+    const size_t count = static_cast<size_t>(tm->n_loc) * 2 * tm->o;
+    for (size_t k = 0; k < count; ++k)
+      if (in[k] < 1 || in[k] > 2 * tm->N)
+        fail(TMG_EINVAL, "automaton counter outside [1, 2N]");
+    if (tm->scratch16.count < count) tm->scratch16.alloc(count);
+    CK(cudaMemcpyAsync(tm->scratch16.ptr, in, count * 2, cudaMemcpyHostToDevice, tm->stream));
+    tmg::counters_to_planes_launch(tm->scratch16.ptr,
+                                   tm->state.ptr + static_cast<size_t>(bank) * tm->n_loc * tm->B * 2 * tm->Wp,
+                                   tm->n_loc, tm->o, tm->B, tm->Wp, tm->N, tm->stream);
+    CK(cudaGetLastError());
+    tm->entries_dirty = true;
+    rebuild_entries(tm);  // refreshes include counts too
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+namespace {
+std::vector<uint32_t> top_planes(tmg_machine* tm, int32_t bank) {
+  // [n_loc][2][Wp] include bits of one bank.
+  std::vector<uint32_t> out(static_cast<size_t>(tm->n_loc) * 2 * tm->Wp);
+  const size_t stride = static_cast<size_t>(tm->B) * 2 * tm->Wp;
+  for (int jl = 0; jl < tm->n_loc; ++jl) {
+    const uint32_t* src = tm->state.ptr + (static_cast<size_t>(bank) * tm->n_loc + jl) * stride +
+                          static_cast<size_t>(tm->B - 1) * 2 * tm->Wp;
+    CK(cudaMemcpyAsync(out.data() + static_cast<size_t>(jl) * 2 * tm->Wp, src, 2 * tm->Wp * 4,
+                       cudaMemcpyDeviceToHost, tm->stream));
+  }
+  CK(cudaStreamSynchronize(tm->stream));
+  return out;
+}
+}  // namespace
+
+TMG_API int tmg_get_include_masks(const tmg_machine* ctm, int32_t bank, uint64_t* out) {
+  return guarded([&] {
+    auto tm = const_cast<tmg_machine*>(M(ctm));
+    check_bank(tm, bank);
+    DeviceGuard dg(tm->device);
+    const auto top = top_planes(tm, bank);
+    const int W64 = (2 * tm->o + 63) / 64;
+    for (int jl = 0; jl < tm->n_loc; ++jl) {
+      uint64_t* row = out + static_cast<size_t>(jl) * W64;
+      std::fill(row, row + W64, 0);
+      const uint32_t* t = top.data() + static_cast<size_t>(jl) * 2 * tm->Wp;
+      for (int part = 0; part < 2; ++part)
+        for (int f = 0; f < tm->o; ++f)
+          if ((t[part * tm->Wp + (f >> 5)] >> (f & 31)) & 1u) {
+            const int k = part * tm->o + f;
+            row[k >> 6] |= 1ULL << (k & 63);
+          }
+    }
+  });
+}
+
+TMG_API int tmg_get_include_counts(const tmg_machine* ctm, int32_t bank, int32_t* out) {
+  return guarded([&] {
+    auto tm = const_cast<tmg_machine*>(M(ctm));
+    check_bank(tm, bank);
+    DeviceGuard dg(tm->device);
+    rebuild_entries(tm);
+    CK(cudaMemcpyAsync(out, tm->inc_count.ptr + static_cast<size_t>(bank) * tm->n_loc, tm->n_loc * 4,
+                       cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_bind_examples(tmg_machine* tm, int64_t q) {
+  return guarded([&] {
+    DeviceGuard dg(M(tm)->device);
+    bind(tm, q);
+  });
+}
+
+TMG_API int tmg_get_prev_outputs(const tmg_machine* ctm, int32_t bank, uint64_t* out) {
+  return guarded([&] {
+    auto tm = const_cast<tmg_machine*>(M(ctm));
+    check_bank(tm, bank);
+    DeviceGuard dg(tm->device);
+    const size_t words = static_cast<size_t>(tm->n_loc) * tm->Wq;
+    if (words)
+      CK(cudaMemcpyAsync(out, tm->prev.ptr + static_cast<size_t>(bank) * words, words * 4, cudaMemcpyDeviceToHost,
+                         tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_set_prev_outputs(tmg_machine* tm, int32_t bank, const uint64_t* in) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    DeviceGuard dg(tm->device);
+    const size_t words = static_cast<size_t>(tm->n_loc) * tm->Wq;
+    if (words)
+      CK(cudaMemcpyAsync(tm->prev.ptr + static_cast<size_t>(bank) * words, in, words * 4, cudaMemcpyHostToDevice,
+                         tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+// ------------------------------------------------------------------ pool ---
+
+TMG_API int tmg_pool_create(int32_t device, int32_t o, const uint8_t* bits, const int32_t* labels, int64_t q,
+                            int32_t m, tmg_pool** out) {
+  return guarded([&] {
+    tmg_pool* pool = create_pool_common(device, o, q, m);
+    try {
+      validate_inputs_host(bits, labels, q, o, m);
+      DeviceGuard dg(device);
+      CK(cudaStreamCreateWithFlags(&pool->stream, cudaStreamNonBlocking));
+      DevBuf<uint8_t> dbits;
+      DevBuf<int32_t> dlab;
+      dbits.alloc(static_cast<size_t>(q) * o);
+      dlab.alloc(static_cast<size_t>(q));
+      CK(cudaMemcpyAsync(dbits.ptr, bits, dbits.bytes(), cudaMemcpyHostToDevice, pool->stream));
+      CK(cudaMemcpyAsync(dlab.ptr, labels, dlab.bytes(), cudaMemcpyHostToDevice, pool->stream));
+      finish_pool(pool, dbits.ptr, dlab.ptr);
+      dbits.release();
+      dlab.release();
+      pool->host_labels.assign(labels, labels + q);
+    } catch (...) {
+      tmg_pool_destroy(pool);
+      throw;
+    }
+    *out = pool;
+  });
+}
+
+TMG_API int tmg_pool_create_device(int32_t device, int32_t o, const uint8_t* d_bits, const int32_t* d_labels,
+                                   int64_t q, int32_t m, tmg_pool** out) {
+  return guarded([&] {
+    tmg_pool* pool = create_pool_common(device, o, q, m);
+    try {
+      DeviceGuard dg(device);
+      CK(cudaStreamCreateWithFlags(&pool->stream, cudaStreamNonBlocking));
+      finish_pool(pool, d_bits, d_labels);
+    } catch (...) {
+      tmg_pool_destroy(pool);
+      throw;
+    }
+    *out = pool;
+  });
+}
+
+TMG_API int tmg_pool_destroy(tmg_pool* pool) {
+  if (!pool) return TMG_OK;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(pool->device);
+  if (pool->stream) cudaStreamSynchronize(pool->stream);
+  pool->xplane.release();
+  pool->nplane.release();
+  pool->labels.release();
+  pool->tallies.release();
+  pool->delta.release();
+  pool->order.release();
+  if (pool->stream) cudaStreamDestroy(pool->stream);
+  if (prev >= 0) cudaSetDevice(prev);
+  delete pool;
+  return TMG_OK;
+}
+
+TMG_API int tmg_pool_size(const tmg_pool* pool, int64_t* q) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    *q = pool->q;
+  });
+}
+
+TMG_API int tmg_pool_get_literals(const tmg_pool* pool, uint64_t* out) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    DeviceGuard dg(pool->device);
+    const size_t rows = static_cast<size_t>(pool->q);
+    std::vector<uint32_t> xs(rows * pool->Wp), ns(rows * pool->Wp);
+    CK(cudaMemcpyAsync(xs.data(), pool->xplane.ptr, xs.size() * 4, cudaMemcpyDeviceToHost, pool->stream));
+    CK(cudaMemcpyAsync(ns.data(), pool->nplane.ptr, ns.size() * 4, cudaMemcpyDeviceToHost, pool->stream));
+    CK(cudaStreamSynchronize(pool->stream));
+    const int o = pool->o, W64 = (2 * o + 63) / 64;
+    for (size_t i = 0; i < rows; ++i) {
+      uint64_t* row = out + i * W64;
+      std::fill(row, row + W64, 0);
+      for (int f = 0; f < o; ++f) {
+        if ((xs[i * pool->Wp + (f >> 5)] >> (f & 31)) & 1u) row[f >> 6] |= 1ULL << (f & 63);
+        if ((ns[i * pool->Wp + (f >> 5)] >> (f & 31)) & 1u) row[(o + f) >> 6] |= 1ULL << ((o + f) & 63);
+      }
+    }
+  });
+}
+
+TMG_API int tmg_pool_get_tallies(const tmg_pool* pool, int32_t* out) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    DeviceGuard dg(pool->device);
+    CK(cudaMemcpyAsync(out, pool->tallies.ptr, pool->tallies.bytes(), cudaMemcpyDeviceToHost, pool->stream));
+    CK(cudaStreamSynchronize(pool->stream));
+  });
+}
+
+TMG_API int tmg_pool_set_tallies(tmg_pool* pool, const int32_t* in) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    DeviceGuard dg(pool->device);
+    CK(cudaMemcpyAsync(pool->tallies.ptr, in, pool->tallies.bytes(), cudaMemcpyHostToDevice, pool->stream));
+    CK(cudaStreamSynchronize(pool->stream));
+  });
+}
+
+TMG_API int tmg_pool_reset_tallies(tmg_pool* pool) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    DeviceGuard dg(pool->device);
+    CK(cudaMemsetAsync(pool->tallies.ptr, 0, pool->tallies.bytes(), pool->stream));
+    CK(cudaMemsetAsync(pool->delta.ptr, 0, pool->delta.bytes(), pool->stream));
+    CK(cudaStreamSynchronize(pool->stream));
+  });
+}
+
+TMG_API int tmg_pool_tally_device_ptr(tmg_pool* pool, void** ptr) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    *ptr = pool->tallies.ptr;
+  });
+}
+
+TMG_API int tmg_pool_delta_device_ptr(tmg_pool* pool, void** ptr) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    *ptr = pool->delta.ptr;
+  });
+}
+
+TMG_API int tmg_pool_apply_reduced(tmg_pool* pool, const void* d_reduced) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    DeviceGuard dg(pool->device);
+    tmg::apply_remote_delta_launch(pool->tallies.ptr, static_cast<const int32_t*>(d_reduced), pool->delta.ptr,
+                                   pool->q * pool->m, pool->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(pool->stream));
+  });
+}
+
+// -------------------------------------------------------------- training ---
+
+TMG_API int tmg_epoch_begin(tmg_machine* tm, tmg_pool* pool, int32_t epoch) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    DeviceGuard dg(tm->device);
+    if (tm->q_bound != pool->q) bind(tm, pool->q);
+    upload_order(tm, pool, epoch);
+    epoch_keys(tm, epoch);
+  });
+}
+
+TMG_API int tmg_train_window(tmg_machine* tm, tmg_pool* pool, int32_t epoch, int64_t t0, int64_t t1,
+                             uint64_t* feedback_events) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    if (tm->cur_epoch != epoch || tm->q_bound != pool->q) fail(TMG_EINVAL, "call tmg_epoch_begin first");
+    if (t0 < 0 || t1 > pool->q || t0 > t1) fail(TMG_ERANGE, "window outside [0, q]");
+    DeviceGuard dg(tm->device);
+    CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
+    run_async_window(tm, pool, t0, t1, true);
+    std::vector<unsigned long long> ev(2 * static_cast<size_t>(tm->m));
+    CK(cudaMemcpyAsync(ev.data(), tm->events.ptr, tm->events.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    if (feedback_events)
+      for (int c = 0; c < tm->m; ++c) feedback_events[c] = ev[static_cast<size_t>(c)];
+  });
+}
+
+TMG_API int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
+                            tmg_epoch_report* report) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    if (workers < 1) fail(TMG_EINVAL, "workers must be >= 1");  // trainer.cpp:184
+    DeviceGuard dg(tm->device);
+    const auto wall0 = std::chrono::steady_clock::now();
+    if (tm->q_bound != pool->q) bind(tm, pool->q);  // trainer.cpp:192-194
+    upload_order(tm, pool, epoch);
+    CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
+    CK(cudaEventRecord(tm->ev0, tm->stream));
+    if (mode == TMG_MODE_ASYNC) {
+      epoch_keys(tm, epoch);
+      run_async_window(tm, pool, 0, pool->q, false);
+    } else if (mode == TMG_MODE_SYNC_MIRROR) {
+      if (tm->n_loc != tm->n) fail(TMG_EINVAL, "sync mirror mode needs the full (unsharded) machine");
+      // Worker w owns g = w, w+W, ... (trainer.cpp:214-227), run one after another.
+      std::vector<tmg::MirrorJob> jobs;
+      const int64_t total = static_cast<int64_t>(tm->m) * tm->n;
+      jobs.reserve(static_cast<size_t>(total));
+      std::vector<uint64_t> rng(static_cast<size_t>(workers) * 4);
+      for (int w = 0; w < workers; ++w) {
+        tmg_rng r;
+        tmg_rng_seed(&r, tm->cfg.seed,
+                     tmg_mix_stream(TMG_STREAM_WORKER, static_cast<uint64_t>(epoch), static_cast<uint64_t>(w)));
+        std::memcpy(&rng[static_cast<size_t>(w) * 4], r.s, 32);
+        for (int64_t g = w; g < total; g += workers) {
+          tmg::MirrorJob jb{};
+          jb.c = static_cast<int32_t>(g / tm->n);
+          jb.j = static_cast<int32_t>(g % tm->n);
+          jb.worker = w;
+          jb.offset = static_cast<int64_t>(tmg_clause_offset(static_cast<uint64_t>(g), pool->q));
+          jb.batch = pool->q;
+          jobs.push_back(jb);
+        }
+      }
+      DevBuf<tmg::MirrorJob> djobs;
+      DevBuf<uint64_t> drng;
+      djobs.alloc(jobs.size());
+      drng.alloc(rng.size());
+      CK(cudaMemcpyAsync(djobs.ptr, jobs.data(), djobs.bytes(), cudaMemcpyHostToDevice, tm->stream));
+      CK(cudaMemcpyAsync(drng.ptr, rng.data(), drng.bytes(), cudaMemcpyHostToDevice, tm->stream));
+      tmg::TrainParams p = make_params(tm, pool);
+      tmg::MirrorParams mp{};
+      mp.jobs = djobs.ptr;
+      mp.njobs = static_cast<int32_t>(jobs.size());
+      mp.rng = drng.ptr;
+      mp.p_high = (tm->cfg.specificity - 1.0) / tm->cfg.specificity;
+      mp.p_low = 1.0 / tm->cfg.specificity;
+      if (!tmg::train_mirror_launch(p, mp, tm->B, tm->NW, tm->stream))
+        fail(TMG_ERUNTIME, "no mirror kernel instantiation for this shape");
+      CK(cudaGetLastError());
+      CK(cudaStreamSynchronize(tm->stream));
+      tm->entries_dirty = true;
+    } else {
+      fail(TMG_EINVAL, "unknown training mode");
+    }
+    CK(cudaEventRecord(tm->ev1, tm->stream));
+    std::vector<unsigned long long> ev(2 * static_cast<size_t>(tm->m));
+    CK(cudaMemcpyAsync(ev.data(), tm->events.ptr, tm->events.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, tm->ev0, tm->ev1));
+    if (report) {
+      report->epoch = epoch;
+      report->device_seconds = ms * 1e-3;
+      double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+      report->seconds = secs > 0 ? secs : 1e-9;
+      if (report->feedback_events)
+        for (int c = 0; c < tm->m; ++c) report->feedback_events[c] = ev[static_cast<size_t>(c)];
+      if (report->type_i_events)
+        for (int c = 0; c < tm->m; ++c)
+          report->type_i_events[c] = mode == TMG_MODE_ASYNC ? ev[static_cast<size_t>(tm->m + c)] : 0;
+    }
+  });
+}
+
+TMG_API unsigned long long tmg_kernel_launches(void) {
+  return __atomic_load_n(&tmg::g_launches, __ATOMIC_RELAXED);
+}
+
+TMG_API int tmg_machine_stream(tmg_machine* tm, void** stream) {
+  return guarded([&] { *stream = M(tm)->stream; });
+}
+
+TMG_API int tmg_bench_int_peak(int32_t device, double* lop3_ops_per_s, double* mixed_ops_per_s) {
+  return guarded([&] {
+    DeviceGuard dg(device);
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (!tmg::int_peak_launch(prop.multiProcessorCount, lop3_ops_per_s, mixed_ops_per_s))
+      fail(TMG_ERUNTIME, "integer peak probe failed");
+  });
+}
+
+TMG_API int tmg_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t c, int32_t j, const int32_t* order,
+                              int64_t order_len, int64_t offset, int64_t batch, int32_t margin, double s,
+                              int32_t boost, uint64_t* rng_state, uint64_t* events) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    if (batch < 1) fail(TMG_EINVAL, "batch must be >= 1");  // trainer.cpp:106
+    if (order && order_len != 0 && order_len != pool->q)
+      fail(TMG_EINVAL, "example order length must equal pool size");  // trainer.cpp:109-111
+    if (c < 0 || c >= tm->m) fail(TMG_ERANGE, "class index out of range");
+    if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
+    if (offset < 0) fail(TMG_EINVAL, "offset must be >= 0");
+    DeviceGuard dg(tm->device);
+    if (tm->q_bound != pool->q) bind(tm, pool->q);
+    const bool use_order = order && order_len == pool->q;
+    if (use_order)
+      CK(cudaMemcpyAsync(pool->order.ptr, order, pool->q * 4, cudaMemcpyHostToDevice, tm->stream));
+    tmg::MirrorJob jb{};
+    jb.c = c;
+    jb.j = j;
+    jb.worker = 0;
+    jb.offset = offset % pool->q;
+    jb.batch = batch;
+    DevBuf<tmg::MirrorJob> djobs;
+    DevBuf<uint64_t> drng;
+    djobs.alloc(1);
+    drng.alloc(4);
+    CK(cudaMemcpyAsync(djobs.ptr, &jb, sizeof jb, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemcpyAsync(drng.ptr, rng_state, 32, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
+    tmg::TrainParams p = make_params(tm, pool);
+    p.order = use_order ? pool->order.ptr : nullptr;
+    p.margin = margin;
+    p.boost = boost ? 1 : 0;
+    tmg::MirrorParams mp{};
+    mp.jobs = djobs.ptr;
+    mp.njobs = 1;
+    mp.rng = drng.ptr;
+    mp.p_high = (s - 1.0) / s;
+    mp.p_low = 1.0 / s;
+    if (!tmg::train_mirror_launch(p, mp, tm->B, tm->NW, tm->stream))
+      fail(TMG_ERUNTIME, "no mirror kernel instantiation for this shape");
+    CK(cudaGetLastError());
+    std::vector<unsigned long long> ev(2 * static_cast<size_t>(tm->m));
+    CK(cudaMemcpyAsync(ev.data(), tm->events.ptr, tm->events.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaMemcpyAsync(rng_state, drng.ptr, 32, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    tm->entries_dirty = true;
+    if (events) *events = ev[static_cast<size_t>(c)];
+  });
+}
+
+TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals, int32_t type,
+                         double s, int32_t boost, uint64_t* rng_state) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
+    if (type != 1 && type != 2) fail(TMG_EINVAL, "feedback type must be 1 (Type I) or 2 (Type II)");
+    DeviceGuard dg(tm->device);
+    const int W64 = (2 * tm->o + 63) / 64;
+    DevBuf<uint64_t> dl;
+    DevBuf<uint32_t> xs, ns;
+    dl.alloc(W64);
+    xs.alloc(tm->Wp);
+    ns.alloc(tm->Wp);
+    CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    tmg::MirrorJob jb{};
+    jb.c = bank;
+    jb.j = j;
+    jb.forced = type;
+    jb.batch = 1;
+    DevBuf<tmg::MirrorJob> djobs;
+    DevBuf<uint64_t> drng;
+    djobs.alloc(1);
+    drng.alloc(4);
+    CK(cudaMemcpyAsync(djobs.ptr, &jb, sizeof jb, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemcpyAsync(drng.ptr, rng_state, 32, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
+    tmg::TrainParams p{};
+    p.state = tm->state.ptr;
+    p.inc_count = tm->inc_count.ptr;
+    p.prev = tm->prev.ptr;
+    p.n = tm->n;
+    p.n_loc = tm->n_loc;
+    p.j_begin = tm->j_begin;
+    p.m = tm->m;
+    p.o = tm->o;
+    p.Wp = tm->Wp;
+    p.Wq = tm->Wq;
+    p.lo = (1u << (tm->B - 1)) - static_cast<uint32_t>(tm->N);
+    p.hi = (1u << (tm->B - 1)) + static_cast<uint32_t>(tm->N) - 1u;
+    p.xplane = xs.ptr;
+    p.nplane = ns.ptr;
+    p.q = 1;
+    p.margin = 1;
+    p.boost = boost ? 1 : 0;
+    p.events = tm->events.ptr;
+    tmg::MirrorParams mp{};
+    mp.jobs = djobs.ptr;
+    mp.njobs = 1;
+    mp.rng = drng.ptr;
+    mp.p_high = (s - 1.0) / s;
+    mp.p_low = 1.0 / s;
+    if (!tmg::train_mirror_launch(p, mp, tm->B, tm->NW, tm->stream))
+      fail(TMG_ERUNTIME, "no mirror kernel instantiation for this shape");
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(rng_state, drng.ptr, 32, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    tm->entries_dirty = true;
+  });
+}
+
+// ------------------------------------------------------------- inference ---
+
+TMG_API int tmg_refresh_tallies(tmg_machine* tm, tmg_pool* pool) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    DeviceGuard dg(tm->device);
+    if (tm->q_bound != pool->q) bind(tm, pool->q);  // pool.cpp:113
+    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, true, pool->tallies.ptr, tm->prev.ptr);
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_class_sums_device(tmg_machine* tm, const tmg_pool* pool, int32_t mode, int32_t* d_sums) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    DeviceGuard dg(tm->device);
+    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, mode == TMG_EVAL_TRAIN, d_sums, nullptr);
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_class_sums(tmg_machine* tm, const tmg_pool* pool, int32_t mode, int32_t* out) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    DeviceGuard dg(tm->device);
+    ensure_sums(tm, pool->q);
+    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, mode == TMG_EVAL_TRAIN, tm->sums.ptr,
+                      nullptr);
+    CK(cudaMemcpyAsync(out, tm->sums.ptr, static_cast<size_t>(pool->q) * tm->m * 4, cudaMemcpyDeviceToHost,
+                       tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    DeviceGuard dg(tm->device);
+    if (tm->n_loc != tm->n) fail(TMG_EINVAL, "predict on a clause shard: reduce class sums across shards first");
+    ensure_sums(tm, pool->q + (pool->q + tm->m - 1) / tm->m + 1);
+    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, false, tm->sums.ptr, nullptr);
+    int32_t* pred = tm->sums.ptr + static_cast<size_t>(pool->q) * tm->m;
+    tmg::argmax_launch(tm->sums.ptr, pred, pool->q, tm->m, tm->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, pred, static_cast<size_t>(pool->q) * 4, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+namespace {
+void literals_to_planes(tmg_machine* tm, const uint64_t* lits, int64_t q, DevBuf<uint32_t>& xs,
+                        DevBuf<uint32_t>& ns) {
+  const int W64 = (2 * tm->o + 63) / 64;
+  DevBuf<uint64_t> dl;
+  dl.alloc(static_cast<size_t>(q) * W64);
+  xs.alloc(static_cast<size_t>(q) * tm->Wp);
+  ns.alloc(static_cast<size_t>(q) * tm->Wp);
+  CK(cudaMemcpyAsync(dl.ptr, lits, dl.bytes(), cudaMemcpyHostToDevice, tm->stream));
+  tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, q, tm->o, tm->Wp, tm->stream);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(tm->stream));
+}
+}  // namespace
+
+TMG_API int tmg_class_sums_literals(tmg_machine* tm, const uint64_t* lits, int64_t q, int32_t mode, int32_t* out) {
+  return guarded([&] {
+    M(tm);
+    if (q <= 0) return;
+    DeviceGuard dg(tm->device);
+    DevBuf<uint32_t> xs, ns;
+    literals_to_planes(tm, lits, q, xs, ns);
+    ensure_sums(tm, q);
+    class_sums_device(tm, xs.ptr, ns.ptr, q, mode == TMG_EVAL_TRAIN, tm->sums.ptr, nullptr);
+    CK(cudaMemcpyAsync(out, tm->sums.ptr, static_cast<size_t>(q) * tm->m * 4, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_predict_literals(tmg_machine* tm, const uint64_t* lits, int64_t q, int32_t* out) {
+  return guarded([&] {
+    M(tm);
+    if (q <= 0) return;
+    if (tm->n_loc != tm->n) fail(TMG_EINVAL, "predict on a clause shard: reduce class sums across shards first");
+    DeviceGuard dg(tm->device);
+    DevBuf<uint32_t> xs, ns;
+    literals_to_planes(tm, lits, q, xs, ns);
+    ensure_sums(tm, q + (q + tm->m - 1) / tm->m + 1);
+    class_sums_device(tm, xs.ptr, ns.ptr, q, false, tm->sums.ptr, nullptr);
+    int32_t* pred = tm->sums.ptr + static_cast<size_t>(q) * tm->m;
+    tmg::argmax_launch(tm->sums.ptr, pred, q, tm->m, tm->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, pred, static_cast<size_t>(q) * 4, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API void tmg_rng_state_init(uint64_t seed, uint64_t stream, uint64_t* state) {
+  tmg_rng r;
+  tmg_rng_seed(&r, seed, stream);
+  std::memcpy(state, r.s, 32);
+}
+
+TMG_API uint64_t tmg_rng_state_next(uint64_t* state) {
+  tmg_rng r;
+  std::memcpy(r.s, state, 32);
+  const uint64_t v = tmg_rng_next(&r);
+  std::memcpy(state, r.s, 32);
+  return v;
+}
+
+TMG_API int tmg_epoch_order(uint64_t seed, int32_t epoch, int32_t q, int32_t* order) {
+  return guarded([&] {
+    if (q < 1) fail(TMG_EINVAL, "q must be >= 1");
+    tmg_rng r;
+    tmg_rng_seed(&r, seed, tmg_mix_stream(TMG_STREAM_PERMUTATION, static_cast<uint64_t>(epoch), 0));
+    tmg_shuffled_indices(q, &r, order);
+  });
+}

@@ -1,0 +1,91 @@
+// kernels.h — launch interface between the host engine and the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace tmg {
+
+// Number of kernels this library has launched (evidence for bench.py's gpu_launches).
+extern unsigned long long g_launches;
+inline void count_launch() { __atomic_fetch_add(&g_launches, 1ULL, __ATOMIC_RELAXED); }
+
+// Device view of one machine shard + pool, shared by all training kernels.
+struct TrainParams {
+  // Machine shard: every class keeps clauses [j_begin, j_begin + n_loc).
+  uint32_t* state;     // [m*n_loc][B][2][Wp] bit-sliced automaton planes
+  int32_t* inc_count;  // [m*n_loc] include count (refreshed at kernel end)
+  uint32_t* prev;      // [m*n_loc][Wq] previous clause output per example
+  int32_t n, n_loc, j_begin, m, o, Wp, Wq;
+  uint32_t lo, hi;  // plane value range of counters [1, 2N]
+  // Pool.
+  const uint32_t* xplane;  // [q][Wp] literals k < o
+  const uint32_t* nplane;  // [q][Wp] literals k >= o
+  const int32_t* labels;   // [q]
+  int32_t* tallies;        // [q][m]
+  int32_t* tally_delta;    // [q][m] or null: deltas also published here (multi-GPU)
+  int64_t q;
+  // Epoch.
+  const int32_t* order;  // [q] epoch permutation, or null = natural order
+  int32_t margin;
+  int32_t boost;
+  uint32_t thr_high, thr_low;  // async: P(u < p) thresholds as 32-bit fixed point
+  uint32_t key0, key1;         // async: Philox key for (seed, epoch)
+  int64_t t_begin, t_end;      // async: window of each clause's pass
+  unsigned long long* events;  // [2m]: feedback events per class, then Type I events per class
+};
+
+struct MirrorJob {
+  int32_t c, j;  // class, global clause index
+  int32_t worker;
+  int32_t forced;  // 0: gated update_clause steps; 1/2: one forced Type I/II
+                   // feedback on literal row 0 (type_i/ii_feedback, feedback.cpp:87-99)
+  int64_t offset, batch;
+};
+
+struct MirrorParams {
+  const MirrorJob* jobs;
+  int32_t njobs;
+  uint64_t* rng;  // [workers][4] xoshiro states, in/out
+  double p_high, p_low;
+};
+
+struct EvalEntry {  // one nonzero include word of a clause
+  uint32_t w, inc_x, inc_n, pad;
+};
+
+struct EvalParams {
+  const EvalEntry* entries;  // [m*n_loc][Wx]
+  const int32_t* nentries;   // [m*n_loc]
+  const int32_t* inc_count;  // [m*n_loc]
+  uint32_t* prev;            // refresh mode: [m*n_loc][Wq]
+  int32_t n_loc, j_begin, m, Wx, Wp, Wq, chunk;
+  const uint32_t* xplane;
+  const uint32_t* nplane;
+  int64_t q;
+  int32_t* sums;  // [q][m], accumulated with atomics
+};
+
+// B (plane count) and NW (words per lane per part) instantiations.
+bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks);
+bool train_mirror_launch(const TrainParams& p, const MirrorParams& mp, int B, int NW, cudaStream_t s);
+void build_entries_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, EvalEntry* e,
+                          int32_t* ne, int32_t* inc_count, cudaStream_t s);
+void eval_sums_launch(const EvalParams& p, bool train_mode, cudaStream_t s);
+void counters_to_planes_launch(const uint16_t* counters, uint32_t* state, int clauses, int o, int B,
+                               int Wp, int N, cudaStream_t s);
+void planes_to_counters_launch(const uint32_t* state, uint16_t* counters, int clauses, int o, int B,
+                               int Wp, int N, cudaStream_t s);
+void pack_planes_launch(const uint8_t* bits, uint32_t* xplane, uint32_t* nplane, int64_t q, int o,
+                        int Wp, cudaStream_t s);
+void unpack_ref_literals_launch(const uint64_t* lits, uint32_t* xplane, uint32_t* nplane, int64_t q,
+                                int o, int Wp, cudaStream_t s);
+void argmax_launch(const int32_t* sums, int32_t* pred, int64_t q, int m, cudaStream_t s);
+void init_state_launch(uint32_t* state, int clauses, int B, int Wp, cudaStream_t s);
+void apply_remote_delta_launch(int32_t* tallies, const int32_t* reduced, int32_t* own, int64_t count,
+                               cudaStream_t s);
+// Integer-pipe peak micro-benchmark: returns thread-ops/s for LOP3-only and LOP3+IMAD streams.
+bool int_peak_launch(int sms, double* lop3_ops, double* mixed_ops);
+
+}  // namespace tmg

@@ -1,0 +1,151 @@
+// tm_device.cuh — device building blocks of the B200 Tsetlin engine.
+//
+// Data layout:
+//   * literal rows: two bit planes per example, u32 words, row stride Wp
+//       xplane[i][w] bit b  = literal k = 32w+b      (feature x_f,   k <  o)
+//       nplane[i][w] bit b  = literal k = o+32w+b    (negation !x_f, k >= o)
+//     i.e. the reference's 2o-bit row (core.cpp:34-46) split at k = o so that
+//     feature f and its negation sit at the same (word, bit) position.
+//   * automaton states: bit-sliced, B planes x 2 parts (x / !x) x Wp words per
+//     clause. Plane value v = counter + (2^(B-1) - N - 1), so counter in [1,2N]
+//     maps to v in [lo, hi] = [2^(B-1)-N, 2^(B-1)+N-1] and Include
+//     (counter > N, core.hpp:42-44) is exactly the top plane.
+//   * one warp owns one clause; lane l holds words l, l+32, ... (NW passes).
+#pragma once
+
+#include <cstdint>
+
+namespace tmg {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------- Philox ---
+// Counter-based Philox4x32-10 (Salmon et al., SC'11). Keyed per (seed, epoch);
+// counters carry (clause, example, literal word, draw block).
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// ------------------------------------------------------------ xoshiro256++ ---
+// Device copy of the reference stream (rng.hpp:44-54) for the sync mirror.
+struct Xoshiro {
+  uint64_t s0, s1, s2, s3;
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t sum = s0 + s3;
+    const uint64_t out = ((sum << 23) | (sum >> 41)) + s0;
+    const uint64_t t = s1 << 17;
+    s2 ^= s0;
+    s3 ^= s1;
+    s1 ^= s2;
+    s0 ^= s3;
+    s2 ^= t;
+    s3 = (s3 << 45) | (s3 >> 19);
+    return out;
+  }
+  // rng.hpp:63 — exact: (next >> 11) * 2^-53.
+  __device__ __forceinline__ double uniform() {
+    return static_cast<double>(next() >> 11) * 0x1.0p-53;
+  }
+};
+
+// ---------------------------------------------------------- bit-sliced ops ---
+// Per-lane view of one clause part (x or !x) word: B planes.
+template <int B>
+struct Planes {
+  uint32_t p[B];
+};
+
+// Lanes (literals) whose value equals the constant `val`.
+template <int B>
+__device__ __forceinline__ uint32_t eq_const(const Planes<B>& s, uint32_t val) {
+  uint32_t acc = kFull;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const uint32_t cb = ((val >> b) & 1u) ? kFull : 0u;
+    acc &= ~(s.p[b] ^ cb);
+  }
+  return acc;
+}
+
+// +1 on lanes in `mask` (caller guarantees no lane is at hi).
+template <int B>
+__device__ __forceinline__ void add_one(Planes<B>& s, uint32_t mask) {
+  uint32_t carry = mask;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const uint32_t t = s.p[b] & carry;
+    s.p[b] ^= carry;
+    carry = t;
+  }
+}
+
+// -1 on lanes in `mask` (caller guarantees no lane is at lo).
+template <int B>
+__device__ __forceinline__ void sub_one(Planes<B>& s, uint32_t mask) {
+  uint32_t borrow = mask;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const uint32_t t = ~s.p[b] & borrow;
+    s.p[b] ^= borrow;
+    borrow = t;
+  }
+}
+
+// Saturating +-1 (apply_transition's clamp to [1, 2N], core.hpp:62-63).
+template <int B>
+__device__ __forceinline__ void step(Planes<B>& s, uint32_t inc, uint32_t dec, uint32_t lo,
+                                     uint32_t hi) {
+  if (inc) inc &= ~eq_const<B>(s, hi);
+  if (dec) dec &= ~eq_const<B>(s, lo);
+  if (inc) add_one<B>(s, inc);
+  if (dec) sub_one<B>(s, dec);
+}
+
+// Bit-serial lazy Bernoulli: returns the lanes (bits) whose fresh uniform u
+// satisfies u < P_k / 2^32, where P_k = thr_hi if bit k of `sel` else thr_lo.
+// Random bits are consumed most-significant first, four 32-bit words (one
+// Philox block) at a time, only until every bit of `need` is decided: the
+// expected number of words is ~log2(popc(need)) + 2 instead of one draw per
+// literal, and the result is an exact Bernoulli(P/2^32) per literal.
+// `block(b)` returns the b-th Philox block of this (clause, example, word)
+// stream.
+__device__ __forceinline__ void bern_bit(uint32_t rb, int bit, uint32_t sel, uint32_t thr_hi,
+                                         uint32_t thr_lo, uint32_t& less, uint32_t& undecided) {
+  const uint32_t ph = ((thr_hi >> bit) & 1u) ? kFull : 0u;
+  const uint32_t pl = ((thr_lo >> bit) & 1u) ? kFull : 0u;
+  const uint32_t pk = (sel & ph) | (~sel & pl);
+  less |= undecided & ~rb & pk;
+  undecided &= ~(rb ^ pk);
+}
+
+template <typename Block>
+__device__ __forceinline__ uint32_t lazy_bernoulli(uint32_t need, uint32_t sel, uint32_t thr_hi,
+                                                   uint32_t thr_lo, Block&& block) {
+  uint32_t less = 0;
+  uint32_t undecided = need;
+  for (int blk = 0; blk < 8 && undecided; ++blk) {
+    const U4 r = block(blk);
+    const int top = 31 - 4 * blk;
+    bern_bit(r.x, top, sel, thr_hi, thr_lo, less, undecided);
+    bern_bit(r.y, top - 1, sel, thr_hi, thr_lo, less, undecided);
+    bern_bit(r.z, top - 2, sel, thr_hi, thr_lo, less, undecided);
+    bern_bit(r.w, top - 3, sel, thr_hi, thr_lo, less, undecided);
+  }
+  return less;
+}
+
+}  // namespace tmg

@@ -1,0 +1,413 @@
+// train.cu — Algorithm 1 (decentralized clause updating) on sm_100a.
+//
+// One warp owns one clause for a whole pass over the example order and keeps
+// its automaton states in registers as bit planes. Per step it reads the
+// (deliberately stale) class tally, gates, applies Type I / Type II feedback,
+// re-evaluates and publishes the output change to the tally with an atomic
+// add — the reference's update_clause (proj/src/trainer.cpp:102-136) with
+// record_output_and_tally (proj/src/pool.cpp:93-106).
+//
+//   train_async  : all clauses concurrently (the paper's GPU architecture),
+//                  counter-based Philox keyed by (seed^epoch, clause, example,
+//                  literal word). Gates of 32 consecutive steps are drawn in
+//                  parallel, one per lane, then only the gated steps run.
+//   train_mirror : one warp replays the reference's W-worker schedule with the
+//                  reference xoshiro streams, bit-exact (sync mirror mode).
+#include <cstdio>
+
+#include "kernels.h"
+#include "tm_device.cuh"
+
+namespace tmg {
+
+namespace {
+
+template <int NW, int B>
+struct Clause {
+  Planes<B> s[2][NW];  // [part][pass]
+  uint32_t valid[NW];  // literal bits that exist (f < o)
+
+  __device__ __forceinline__ void load(const uint32_t* base, int Wp, int lane, int o) {
+#pragma unroll
+    for (int p = 0; p < NW; ++p) {
+      const int wi = p * 32 + lane;
+      const int first = wi * 32;
+      valid[p] = first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
+#pragma unroll
+      for (int part = 0; part < 2; ++part)
+#pragma unroll
+        for (int b = 0; b < B; ++b) s[part][p].p[b] = base[(b * 2 + part) * Wp + wi];
+    }
+  }
+
+  __device__ __forceinline__ void store(uint32_t* base, int Wp, int lane) const {
+#pragma unroll
+    for (int p = 0; p < NW; ++p)
+#pragma unroll
+      for (int part = 0; part < 2; ++part)
+#pragma unroll
+        for (int b = 0; b < B; ++b) base[(b * 2 + part) * Wp + p * 32 + lane] = s[part][p].p[b];
+  }
+
+  // Train-mode evaluation (core.hpp:208-219): empty clause -> 1.
+  __device__ __forceinline__ int eval_train(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) const {
+    uint32_t viol = 0, any = 0;
+#pragma unroll
+    for (int p = 0; p < NW; ++p) {
+      const uint32_t ix = s[0][p].p[B - 1], in = s[1][p].p[B - 1];
+      viol |= (ix & ~x[p]) | (in & ~n[p]);
+      any |= ix | in;
+    }
+    const unsigned vb = __ballot_sync(kFull, viol != 0);
+    const unsigned ab = __ballot_sync(kFull, any != 0);
+    return ab == 0 ? 1 : (vb == 0 ? 1 : 0);
+  }
+
+  __device__ __forceinline__ int include_count() const {
+    int cnt = 0;
+#pragma unroll
+    for (int p = 0; p < NW; ++p) cnt += __popc(s[0][p].p[B - 1]) + __popc(s[1][p].p[B - 1]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+    return cnt;
+  }
+
+  // Type II (feedback.cpp:72-83): with output 1, every excluded automaton of
+  // a false literal takes a Penalty (+1). Excluded states sit below the top
+  // plane, so no saturation is possible. Returns whether anything moved.
+  __device__ __forceinline__ bool type_ii(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) {
+    uint32_t moved = 0;
+#pragma unroll
+    for (int p = 0; p < NW; ++p) {
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const uint32_t lit = part ? n[p] : x[p];
+        const uint32_t inc = ~lit & ~s[part][p].p[B - 1] & valid[p];
+        if (inc) add_one<B>(s[part][p], inc);
+        moved |= inc;
+      }
+    }
+    return __any_sync(kFull, moved != 0);
+  }
+
+  // Type I (feedback.cpp:32-70) given per-word Bernoulli masks:
+  //   out=1, lit=1 : +1 w.p. (s-1)/s  (always if boost and included)
+  //   out=1, lit=0 : -1 w.p. 1/s       (such literals are never included)
+  //   out=0        : -1 w.p. 1/s       (Penalty on Include, Reward on Exclude)
+  __device__ __forceinline__ void type_i_word(int part, int p, uint32_t lit, int out, int boost,
+                                              uint32_t bern, uint32_t lo, uint32_t hi) {
+    Planes<B>& w = s[part][p];
+    if (out) {
+      uint32_t inc = lit & (bern | (boost ? w.p[B - 1] : 0u)) & valid[p];
+      uint32_t dec = ~lit & bern & valid[p];
+      step<B>(w, inc, dec, lo, hi);
+    } else {
+      step<B>(w, 0u, bern & valid[p], lo, hi);
+    }
+  }
+};
+
+__device__ __forceinline__ uint64_t splitmix_dev(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// Publishes the post-feedback output (pool.cpp:93-106): lane 0 only.
+__device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row, int64_t i, int c,
+                                       bool positive, uint32_t pword, int after) {
+  const uint32_t bit = 1u << (i & 31);
+  const int before = (pword & bit) ? 1 : 0;
+  if (before == after) return;
+  prev_row[i >> 5] = pword ^ bit;
+  int delta = after ? 1 : -1;
+  if (!positive) delta = -delta;
+  atomicAdd(&P.tallies[i * P.m + c], delta);
+  if (P.tally_delta) atomicAdd(&P.tally_delta[i * P.m + c], delta);
+}
+
+// --------------------------------------------------------------- async ---
+
+template <int NW, int B>
+__global__ void __launch_bounds__(128) train_async_kernel(TrainParams P) {
+  const int lane = threadIdx.x & 31;
+  const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (lc >= P.m * P.n_loc) return;
+  const int c = lc / P.n_loc;
+  const int j = P.j_begin + lc % P.n_loc;
+  const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
+  const bool positive = (j & 1) == 0;
+  const int64_t q = P.q;
+  const int T = P.margin;
+
+  Clause<NW, B> cl;
+  uint32_t* st = P.state + static_cast<size_t>(lc) * B * 2 * P.Wp;
+  cl.load(st, P.Wp, lane, P.o);
+  uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
+  // Per-clause starting position in the epoch order (trainer.cpp:41-44, 222-223).
+  const int64_t offset = static_cast<int64_t>(splitmix_dev(static_cast<uint64_t>(g) + 1) %
+                                              static_cast<uint64_t>(q));
+  unsigned long long events = 0, events_type1 = 0;
+
+  for (int64_t t0 = P.t_begin; t0 < P.t_end; t0 += 32) {
+    const int64_t t = t0 + lane;
+    int64_t i = 0;
+    int target = 0;
+    bool gated = false;
+    if (t < P.t_end) {
+      int64_t pos = offset + t;
+      if (pos >= q) pos -= q;
+      i = P.order ? __ldg(P.order + pos) : pos;
+      target = __ldg(P.labels + i) == c ? 1 : 0;
+      int v = __ldcg(P.tallies + i * P.m + c);  // relaxed, L2-coherent read
+      v = v < -T ? -T : (v > T ? T : v);
+      const uint32_t e = static_cast<uint32_t>(target ? T - v : T + v);
+      const U4 r = philox4x32_10(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
+      // u < e / 2T  <=>  r * 2T < e * 2^32  (exact integer gate, feedback.cpp:24-28)
+      gated = static_cast<uint64_t>(r.x) * static_cast<uint64_t>(2 * T) <
+              (static_cast<uint64_t>(e) << 32);
+    }
+    unsigned gm = __ballot_sync(kFull, gated);
+    events += __popc(gm);
+    while (gm) {
+      const int sl = __ffs(gm) - 1;
+      gm &= gm - 1;
+      const int64_t is = __shfl_sync(kFull, i, sl);
+      const int tg = __shfl_sync(kFull, target, sl);
+      uint32_t x[NW], n[NW];
+      const uint32_t* xr = P.xplane + is * P.Wp + lane;
+      const uint32_t* nr = P.nplane + is * P.Wp + lane;
+#pragma unroll
+      for (int p = 0; p < NW; ++p) {
+        x[p] = __ldg(xr + p * 32);
+        n[p] = __ldg(nr + p * 32);
+      }
+      uint32_t pword = 0;
+      if (lane == 0) pword = prev_row[is >> 5];
+      const int before = cl.eval_train(x, n);
+      int after = before;
+      if ((tg == 1) != positive) {
+        if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
+      } else {
+        ++events_type1;
+#pragma unroll
+        for (int p = 0; p < NW; ++p) {
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const uint32_t lit = part ? n[p] : x[p];
+            const uint32_t word_id = static_cast<uint32_t>((p * 32 + lane) * 2 + part);
+            const uint32_t bern = lazy_bernoulli(
+                cl.valid[p], before ? lit : 0u, P.thr_high, P.thr_low, [&](int blk) {
+                  return philox4x32_10(U4{g, static_cast<uint32_t>(is), word_id,
+                                          static_cast<uint32_t>(blk)},
+                                       P.key0, P.key1);
+                });
+            cl.type_i_word(part, p, lit, before, P.boost, bern, P.lo, P.hi);
+          }
+        }
+        after = cl.eval_train(x, n);
+      }
+      if (lane == 0) record(P, prev_row, is, c, positive, pword, after);
+    }
+  }
+  cl.store(st, P.Wp, lane);
+  const int cnt = cl.include_count();
+  if (lane == 0) {
+    P.inc_count[lc] = cnt;
+    atomicAdd(P.events + c, events);
+    atomicAdd(P.events + P.m + c, events_type1);
+  }
+}
+
+// -------------------------------------------------------------- mirror ---
+
+// Single warp. Replays, job by job, update_clause (trainer.cpp:102-136) with
+// the reference xoshiro streams: exactly one gate draw per step and 2o Type I
+// draws in literal order k = 0..2o-1 (feedback.cpp:45,63).
+template <int NW, int B>
+__global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorParams M) {
+  extern __shared__ uint32_t smem[];
+  const int lane = threadIdx.x;
+  const int L = 2 * P.o;
+  const int refw = (L + 31) / 32 + 2;  // + padding for funnel shifts
+  uint32_t* hbits = smem;              // u < p_high, reference literal order
+  uint32_t* lbits = smem + refw;       // u < p_low
+  const int64_t q = P.q;
+  const int T = P.margin;
+  for (int k = lane; k < 2 * refw; k += 32) smem[k] = 0;
+  __syncwarp();
+
+  for (int jb = 0; jb < M.njobs; ++jb) {
+    const MirrorJob job = M.jobs[jb];
+    const int c = job.c;
+    const int lc = c * P.n_loc + (job.j - P.j_begin);
+    const bool positive = (job.j & 1) == 0;
+    Xoshiro rng;
+    uint64_t* rs = M.rng + 4 * job.worker;
+    rng.s0 = rs[0];
+    rng.s1 = rs[1];
+    rng.s2 = rs[2];
+    rng.s3 = rs[3];
+    Clause<NW, B> cl;
+    uint32_t* st = P.state + static_cast<size_t>(lc) * B * 2 * P.Wp;
+    cl.load(st, P.Wp, lane, P.o);
+    uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
+    unsigned long long events = 0;
+
+    const bool forced = job.forced != 0;
+    for (int64_t t = 0; t < job.batch; ++t) {
+      int64_t i = 0;
+      int target = 0, gated = 1;
+      if (lane == 0 && !forced) {
+        const int64_t pos = (job.offset + t) % q;
+        i = P.order ? P.order[pos] : pos;
+        const int v0 = P.tallies[i * P.m + c];
+        target = P.labels[i] == c ? 1 : 0;
+        const int v = v0 < -T ? -T : (v0 > T ? T : v0);
+        const int e = target ? T - v : T + v;
+        const double p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+        gated = rng.uniform() < p ? 1 : 0;  // skip iff u >= p (trainer.cpp:121)
+      }
+      gated = __shfl_sync(kFull, gated, 0);
+      if (!gated) continue;
+      ++events;
+      i = __shfl_sync(kFull, i, 0);
+      target = __shfl_sync(kFull, target, 0);
+      uint32_t x[NW], n[NW];
+#pragma unroll
+      for (int p = 0; p < NW; ++p) {
+        x[p] = P.xplane[i * P.Wp + p * 32 + lane];
+        n[p] = P.nplane[i * P.Wp + p * 32 + lane];
+      }
+      const bool type2 = forced ? job.forced == 2 : (target == 1) != positive;
+      const int before = cl.eval_train(x, n);
+      int after = before;
+      if (type2) {
+        if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
+      } else {
+        if (lane == 0) {
+          uint32_t hw = 0, lw = 0;
+          for (int k = 0; k < L; ++k) {
+            const double u = rng.uniform();
+            hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
+            lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
+            if ((k & 31) == 31 || k == L - 1) {
+              hbits[k >> 5] = hw;
+              lbits[k >> 5] = lw;
+              hw = lw = 0;
+            }
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int p = 0; p < NW; ++p) {
+          const int wi = p * 32 + lane;
+          if (wi * 32 >= P.o) continue;
+          // part 0: literal k = 32*wi + b; part 1: literal k = o + 32*wi + b.
+          const int k1 = P.o + wi * 32;
+          const uint32_t h0 = hbits[wi], l0 = lbits[wi];
+          const uint32_t h1 = __funnelshift_r(hbits[k1 >> 5], hbits[(k1 >> 5) + 1], k1 & 31);
+          const uint32_t l1 = __funnelshift_r(lbits[k1 >> 5], lbits[(k1 >> 5) + 1], k1 & 31);
+          if (before) {
+            // c=1: lit=1 uses the p_high draw, lit=0 the p_low draw.
+            cl.type_i_word(0, p, x[p], 1, P.boost, (x[p] & h0) | (~x[p] & l0), P.lo, P.hi);
+            cl.type_i_word(1, p, n[p], 1, P.boost, (n[p] & h1) | (~n[p] & l1), P.lo, P.hi);
+          } else {
+            cl.type_i_word(0, p, x[p], 0, P.boost, l0, P.lo, P.hi);
+            cl.type_i_word(1, p, n[p], 0, P.boost, l1, P.lo, P.hi);
+          }
+        }
+        __syncwarp();
+        after = cl.eval_train(x, n);
+      }
+      if (lane == 0 && !forced) {
+        const uint32_t pword = prev_row[i >> 5];
+        record(P, prev_row, i, c, positive, pword, after);
+      }
+      __syncwarp();
+    }
+    cl.store(st, P.Wp, lane);
+    const int cnt = cl.include_count();
+    if (lane == 0) {
+      P.inc_count[lc] = cnt;
+      P.events[c] += events;
+      rs[0] = rng.s0;
+      rs[1] = rng.s1;
+      rs[2] = rng.s2;
+      rs[3] = rng.s3;
+    }
+    __syncwarp();
+  }
+}
+
+template <int NW, int B>
+void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
+  const int clauses = p.m * p.n_loc;
+  const int warps_per_block = 4;
+  const int grid = (clauses + warps_per_block - 1) / warps_per_block;
+  if (blocks) *blocks = grid;
+  count_launch();
+  train_async_kernel<NW, B><<<grid, 32 * warps_per_block, 0, s>>>(p);
+}
+
+template <int NW, int B>
+void launch_mirror(const TrainParams& p, const MirrorParams& mp, cudaStream_t s) {
+  const int refw = (2 * p.o + 31) / 32 + 2;
+  const size_t shm = sizeof(uint32_t) * 2 * refw;
+  if (shm > 48 * 1024)
+    cudaFuncSetAttribute(train_mirror_kernel<NW, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(shm));
+  count_launch();
+  train_mirror_kernel<NW, B><<<1, 32, shm, s>>>(p, mp);
+}
+
+template <int B>
+bool dispatch_async(const TrainParams& p, int NW, cudaStream_t s, int* blocks) {
+  switch (NW) {
+    case 1: launch_async<1, B>(p, s, blocks); return true;
+    case 2: launch_async<2, B>(p, s, blocks); return true;
+    case 3: launch_async<3, B>(p, s, blocks); return true;
+    case 4: launch_async<4, B>(p, s, blocks); return true;
+    case 8: launch_async<8, B>(p, s, blocks); return true;
+    case 10: launch_async<10, B>(p, s, blocks); return true;
+    default: return false;
+  }
+}
+
+template <int B>
+bool dispatch_mirror(const TrainParams& p, const MirrorParams& mp, int NW, cudaStream_t s) {
+  switch (NW) {
+    case 1: launch_mirror<1, B>(p, mp, s); return true;
+    case 2: launch_mirror<2, B>(p, mp, s); return true;
+    case 3: launch_mirror<3, B>(p, mp, s); return true;
+    case 4: launch_mirror<4, B>(p, mp, s); return true;
+    case 8: launch_mirror<8, B>(p, mp, s); return true;
+    case 10: launch_mirror<10, B>(p, mp, s); return true;
+    default: return false;
+  }
+}
+
+}  // namespace
+
+bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
+  switch (B) {
+    case 2: return dispatch_async<2>(p, NW, s, blocks);
+    case 4: return dispatch_async<4>(p, NW, s, blocks);
+    case 8: return dispatch_async<8>(p, NW, s, blocks);
+    case 15: return dispatch_async<15>(p, NW, s, blocks);
+    default: return false;
+  }
+}
+
+bool train_mirror_launch(const TrainParams& p, const MirrorParams& mp, int B, int NW, cudaStream_t s) {
+  switch (B) {
+    case 2: return dispatch_mirror<2>(p, mp, NW, s);
+    case 4: return dispatch_mirror<4>(p, mp, NW, s);
+    case 8: return dispatch_mirror<8>(p, mp, NW, s);
+    case 15: return dispatch_mirror<15>(p, mp, NW, s);
+    default: return false;
+  }
+}
+
+}  // namespace tmg

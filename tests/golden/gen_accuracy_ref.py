@@ -1,0 +1,55 @@
+#!/usr/bin/env python3
+"""Reference accuracy numbers for the asynchronous-training parity gate
+(BASELINE.json: <=0.5 pt vs the reference, mean over 5 seeds).
+
+Runs the UNMODIFIED reference (oracle/_ref/ref_driver, built by
+oracle/Makefile from /root/reference) with train_epoch_parallel on all host
+threads and records test accuracy per epoch into accuracy_ref.json.
+"""
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+DRIVER = os.path.join(HERE, "..", "..", "oracle", "_ref", "ref_driver")
+
+CASES = {
+    "xor_noise10": dict(data="xor", q=5000, qtest=5000, clauses=20, T=15, s=3.9, epochs=50,
+                        noise=0.1, data_seed=7),
+    "xor_noise40": dict(data="xor", q=5000, qtest=5000, clauses=20, T=15, s=3.9, epochs=50,
+                        noise=0.4, data_seed=7),
+    "mnist_q6000": dict(data="mnist", q=6000, qtest=2000, clauses=2000, T=50, s=10.0, epochs=3,
+                        noise=0.0, data_seed=2009),
+}
+
+
+def run(case, seed, workers):
+    args = [DRIVER, "train", "--data", case["data"], "--q", str(case["q"]), "--qtest", str(case["qtest"]),
+            "--clauses", str(case["clauses"]), "--T", str(case["T"]), "--s", str(case["s"]),
+            "--epochs", str(case["epochs"]), "--noise", str(case["noise"]), "--seed", str(seed),
+            "--data-seed", str(case["data_seed"]), "--workers", str(workers)]
+    out = subprocess.run(args, check=True, capture_output=True, text=True).stdout
+    return [json.loads(l) for l in out.splitlines() if l.strip()]
+
+
+def main():
+    names = sys.argv[1:] or list(CASES)
+    path = os.path.join(HERE, "accuracy_ref.json")
+    res = json.load(open(path)) if os.path.exists(path) else {}
+    workers = os.cpu_count() or 1
+    for name in names:
+        case = CASES[name]
+        per_seed = {}
+        for seed in range(1, 6):
+            rows = run(case, seed, workers)
+            per_seed[str(seed)] = [r["test_accuracy"] for r in rows]
+            print(name, seed, per_seed[str(seed)][-1], flush=True)
+        final = [v[-1] for v in per_seed.values()]
+        res[name] = dict(config=case, workers=workers, per_seed=per_seed,
+                         mean_final=sum(final) / len(final))
+        json.dump(res, open(path, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,119 @@
+"""Asynchronous (Algorithm 1) training on the GPU: invariants, statistical
+conformance and accuracy parity with the reference's parallel trainer."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden_io import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+T = pytest.importorskip("paper_2009_04861_b200")
+from paper_2009_04861_b200 import synth  # noqa: E402
+
+
+def _bits_of(prev_words: np.ndarray, q: int) -> np.ndarray:
+    """n x ceil(q/64) uint64 -> n x q {0,1} (bit i of word i//64)."""
+    b = np.unpackbits(prev_words.view(np.uint8), axis=1, bitorder="little")
+    return b[:, :q].astype(np.int64)
+
+
+def _check_tally_invariant(tm, pool, m, q):
+    """tally[i][c] == sum_j sign(j) * prev_bit[c][j][i] at quiescence
+    (pool.cpp:71, core.cpp:123-125, pool.cpp:99-105)."""
+    tallies = pool.tallies()
+    for c in range(m):
+        bits = _bits_of(tm.banks[c].prev_outputs(), q)
+        expect = bits[0::2].sum(0) - bits[1::2].sum(0)
+        assert np.array_equal(tallies[:, c], expect), f"class {c}"
+
+
+def test_async_epoch_invariants_mnist_shape():
+    d = synth.make("mnist", 3000, 500, 2009)
+    cfg = T.TMConfig(clauses=200, margin=50, specificity=10.0, seed=3)
+    tm = T.MultiClassTM(cfg, 784, 10)
+    pool = T.ExamplePool(784, d.train_x, d.train_y, 10)
+    for e in range(2):
+        rep = T.train_epoch_parallel(tm, pool, 1, e)
+        assert rep.total_feedback_events() > 0
+        assert 0 < sum(rep.type_i_events) < rep.total_feedback_events()
+        _check_tally_invariant(tm, pool, 10, 3000)
+    for c in range(10):
+        cs = tm.banks[c].counters()
+        assert cs.min() >= 1 and cs.max() <= 256
+    # refresh: exact train-mode sums, and the same on the oracle for these states
+    T.refresh_tallies(pool, tm)
+    exact = T.class_sums(tm, pool, T.TRAIN)
+    assert np.array_equal(pool.tallies(), exact)
+    ref = O.Machine(784, 10, 200, 128)
+    ref.set_counters(np.stack([tm.banks[c].counters() for c in range(10)]))
+    rpool = O.Pool(d.train_x, d.train_y, 10)
+    O.refresh_tallies(ref, rpool)
+    assert np.array_equal(pool.tallies(), rpool.tallies)
+    _check_tally_invariant(tm, pool, 10, 3000)
+    # inference parity on the trained state
+    test = T.ExamplePool(784, d.test_x, d.test_y, 10)
+    lits = O.pack_literals(d.test_x)
+    assert np.array_equal(T.class_sums(tm, test), ref.class_sums(lits))
+    assert np.array_equal(T.predict_all(tm, test), ref.predict(lits))
+
+
+def test_async_window_accounting():
+    """Windows of a pass compose to the full pass (multi-GPU building block)."""
+    d = synth.make("xor", 1000, 10, 5, 0.1)
+    cfg = T.TMConfig(clauses=20, margin=15, specificity=3.9, seed=9)
+    tm = T.MultiClassTM(cfg, 12, 2)
+    pool = T.ExamplePool(12, d.train_x, d.train_y, 2)
+    from paper_2009_04861_b200 import distributed as D
+    ev = D.train_epoch_windows(tm, pool, 0, windows=7, allreduce=None)
+    assert sum(ev) > 0
+    _check_tally_invariant(tm, pool, 2, 1000)
+
+
+def _ref_acc():
+    path = os.path.join(GOLDEN, "accuracy_ref.json")
+    return json.load(open(path)) if os.path.exists(path) else {}
+
+
+@pytest.mark.parametrize("case,tol", [("xor_noise10", 0.005), ("xor_noise40", 0.01)])
+def test_async_accuracy_parity_xor(case, tol):
+    ref = _ref_acc().get(case)
+    if ref is None:
+        pytest.skip("accuracy_ref.json lacks " + case)
+    cfgd = ref["config"]
+    accs = []
+    for seed in range(1, 6):
+        d = synth.make("xor", cfgd["q"], cfgd["qtest"], cfgd["data_seed"], cfgd["noise"])
+        tm = T.MultiClassTM(T.TMConfig(clauses=cfgd["clauses"], margin=cfgd["T"], specificity=cfgd["s"],
+                                       seed=seed), 12, 2)
+        pool = T.ExamplePool(12, d.train_x, d.train_y, 2)
+        test = T.ExamplePool(12, d.test_x, d.test_y, 2)
+        for e in range(cfgd["epochs"]):
+            T.train_epoch_parallel(tm, pool, 1, e)
+        accs.append(T.evaluate_accuracy(tm, test))
+    gpu, cpu = float(np.mean(accs)), ref["mean_final"]
+    print(f"{case}: gpu mean {gpu:.4f} vs reference mean {cpu:.4f} (per-seed {accs})")
+    assert gpu >= cpu - tol
+
+
+def test_async_accuracy_parity_mnist():
+    ref = _ref_acc().get("mnist_q6000")
+    if ref is None:
+        pytest.skip("accuracy_ref.json lacks mnist_q6000")
+    cfgd = ref["config"]
+    d = synth.make("mnist", cfgd["q"], cfgd["qtest"], cfgd["data_seed"])
+    accs = []
+    for seed in range(1, 6):
+        tm = T.MultiClassTM(T.TMConfig(clauses=cfgd["clauses"], margin=cfgd["T"], specificity=cfgd["s"],
+                                       seed=seed), 784, 10)
+        pool = T.ExamplePool(784, d.train_x, d.train_y, 10)
+        test = T.ExamplePool(784, d.test_x, d.test_y, 10)
+        for e in range(cfgd["epochs"]):
+            T.train_epoch_parallel(tm, pool, 1, e)
+        accs.append(T.evaluate_accuracy(tm, test))
+    gpu, cpu = float(np.mean(accs)), ref["mean_final"]
+    print(f"mnist_q6000: gpu mean {gpu:.4f} vs reference mean {cpu:.4f} (per-seed {accs})")
+    assert gpu >= cpu - 0.005  # BASELINE.json: <= 0.5 pt, mean over 5 seeds

@@ -1,0 +1,187 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the reference's
+golden dumps (tests/golden/, from the compiled reference) and the oracle.
+
+Bit-exact for everything deterministic: packing, class sums / predictions on
+identical automaton states, refresh_tallies, single feedback calls,
+update_clause and train_epoch_parallel(workers=1) in sync-mirror mode.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden_io import EPOCH_CASES, load, manifest
+
+pytestmark = pytest.mark.gpu
+
+tm_mod = pytest.importorskip("paper_2009_04861_b200")
+import paper_2009_04861_b200 as T  # noqa: E402
+
+
+def _cfg(man, n=None):
+    return T.TMConfig(clauses=n or man["n"], margin=man.get("margin", 15), specificity=man.get("s", 3.0),
+                      state_depth=man["N"], boost_true_positive=bool(man.get("boost", 0)),
+                      seed=man.get("seed", 42))
+
+
+@pytest.mark.parametrize("o", [1, 2, 12, 31, 32, 33, 63, 64, 65, 100, 784])
+def test_pool_literals_match_reference_packing(o):
+    bits = load("pack", f"bits_o{o}.npy")
+    pool = T.ExamplePool(o, bits, np.array([0, 1, 0], np.int32), 2)
+    assert np.array_equal(pool.all_literals(), load("pack", f"lits_o{o}.npy"))
+
+
+def test_pool_validation_errors():
+    with pytest.raises(ValueError, match="0/1"):
+        T.ExamplePool(3, np.array([[0, 2, 1]], np.uint8), np.array([0], np.int32), 2)
+    with pytest.raises(ValueError, match="label"):
+        T.ExamplePool(3, np.array([[0, 1, 1]], np.uint8), np.array([5], np.int32), 2)
+    with pytest.raises(ValueError, match="empty"):
+        T.ExamplePool(3, np.zeros((0, 3), np.uint8), np.zeros(0, np.int32), 2)
+
+
+def test_counter_roundtrip_and_masks():
+    for case in manifest("feedback"):
+        k = case["idx"]
+        before = load("feedback", f"case{k}_before.npy")
+        tm = T.MultiClassTM(T.TMConfig(clauses=2, state_depth=case["N"]), case["o"], 1)
+        tm.banks[0].set_counters(before)
+        assert np.array_equal(tm.banks[0].counters(), before)
+        ref = O.Machine(case["o"], 1, 2, case["N"])
+        ref.set_counters(before[None])
+        assert np.array_equal(tm.banks[0].include_masks(), ref.masks[0])
+        assert np.array_equal(tm.banks[0].include_counts(), ref.counts[0])
+
+
+def test_feedback_golden_cases():
+    for case in manifest("feedback"):
+        k = case["idx"]
+        x = load("feedback", f"case{k}_x.npy")
+        before = load("feedback", f"case{k}_before.npy")
+        after = load("feedback", f"case{k}_after.npy")
+        tm = T.MultiClassTM(T.TMConfig(clauses=2, state_depth=case["N"]), case["o"], 1)
+        tm.banks[0].set_counters(before)
+        lits = O.pack_literals(x)[0]
+        r = T.Rng(case["rng_seed"], case["rng_stream"])
+        if case["type"] == 1:
+            T.type_i_feedback(tm.banks[0], 1, lits, case["s"], bool(case["boost"]), r)
+        else:
+            T.type_ii_feedback(tm.banks[0], 1, lits)
+        assert np.array_equal(tm.banks[0].counters(), after), f"feedback case {k}"
+        if case["type"] == 1:
+            assert r.next() == int(case["next_draw"]), f"draw count, case {k}"
+
+
+def _set_state(d, tag, tm, pool, m, q):
+    counters = load(*d, f"{tag}_counters.npy")
+    prev = load(*d, f"{tag}_prev.npy")
+    tm.bind_examples(q)
+    for c in range(m):
+        tm.banks[c].set_counters(counters[c])
+        tm.banks[c].set_prev_outputs(prev[c])
+    pool.set_tallies(load(*d, f"{tag}_tallies.npy"))
+
+
+def _check_state(d, tag, tm, pool, m):
+    for c in range(m):
+        b = tm.banks[c]
+        assert np.array_equal(b.counters(), load(*d, f"{tag}_counters.npy")[c]), f"{tag} counters bank {c}"
+        assert np.array_equal(b.include_masks(), load(*d, f"{tag}_masks.npy")[c]), f"{tag} masks bank {c}"
+        assert np.array_equal(b.include_counts(), load(*d, f"{tag}_counts.npy")[c]), f"{tag} counts bank {c}"
+        assert np.array_equal(b.prev_outputs(), load(*d, f"{tag}_prev.npy")[c]), f"{tag} prev bank {c}"
+    assert np.array_equal(pool.tallies(), load(*d, f"{tag}_tallies.npy")), f"{tag} tallies"
+
+
+def test_update_clause_golden_cases():
+    for case in manifest("update_clause"):
+        k = case["idx"]
+        d = ("update_clause",)
+        bits, labels = load(*d, f"case{k}_bits.npy"), load(*d, f"case{k}_labels.npy")
+        order = load(*d, f"case{k}_order.npy")
+        pool = T.ExamplePool(case["o"], bits, labels, case["m"])
+        tm = T.MultiClassTM(T.TMConfig(clauses=case["n"], state_depth=case["N"]), case["o"], case["m"])
+        _set_state(d, f"case{k}_in", tm, pool, case["m"], case["q"])
+        r = T.Rng(case["rng_seed"], case["rng_stream"])
+        ev = T.update_clause(tm.banks[case["cls"]], case["j"], pool, case["cls"], order, case["offset"],
+                             case["batch"], case["margin"], case["s"], bool(case["boost"]), r)
+        assert ev == case["events"], f"case {k}"
+        _check_state(d, f"case{k}_out", tm, pool, case["m"])
+        assert r.next() == int(case["next_draw"])
+
+
+@pytest.mark.parametrize("name", EPOCH_CASES)
+def test_sync_mirror_epochs_bit_exact(name):
+    """train_epoch_parallel(workers=1) replayed on the GPU == the reference."""
+    d = ("epoch_par_w1", name)
+    man = manifest(*d)
+    pool = T.ExamplePool(man["o"], load(*d, "train_x.npy"), load(*d, "train_y.npy"), man["m"])
+    tm = T.MultiClassTM(_cfg(man), man["o"], man["m"])
+    for ep in man["epochs"]:
+        e = ep["epoch"]
+        rep = T.train_epoch_parallel(tm, pool, 1, e, mode=T.MODE_SYNC_MIRROR)
+        assert rep.feedback_events == ep["feedback_events"], f"events epoch {e}"
+        _check_state(d, f"epoch{e}", tm, pool, man["m"])
+    test = T.ExamplePool(man["o"], load(*d, "test_x.npy"), load(*d, "test_y.npy"), man["m"])
+    assert np.array_equal(T.class_sums(tm, test), load(*d, "test_sums.npy"))
+    assert np.array_equal(T.predict_all(tm, test), load(*d, "test_pred.npy"))
+    assert T.evaluate_accuracy(tm, test) == pytest.approx(man["test_accuracy"], abs=0)
+    T.refresh_tallies(pool, tm)
+    _check_state(d, "refreshed", tm, pool, man["m"])
+
+
+@pytest.mark.parametrize("name,o,m,n", [("mnist_rand", 784, 10, 50), ("single_bank", 30, 1, 8),
+                                        ("dense_o64", 64, 3, 12)])
+def test_inference_random_states(name, o, m, n):
+    bits = load("inference", f"{name}_bits.npy")
+    tm = T.MultiClassTM(T.TMConfig(clauses=n), o, m)
+    counters = load("inference", f"{name}_counters.npy")
+    for c in range(m):
+        tm.banks[c].set_counters(counters[c])
+    pool = T.ExamplePool(o, bits, np.zeros(bits.shape[0], np.int32), m)
+    sums = load("inference", f"{name}_sums.npy")
+    assert np.array_equal(T.class_sums(tm, pool), sums)
+    assert np.array_equal(T.predict_all(tm, pool), load("inference", f"{name}_pred.npy"))
+    lits = O.pack_literals(bits)
+    assert np.array_equal(T.export_vote_sums(tm, lits), sums)
+    assert np.array_equal(T.export_vote_sums(tm, lits[3]), sums[3])
+    assert T.classify(tm, lits[5]) == load("inference", f"{name}_pred.npy")[5]
+    T.refresh_tallies(pool, tm)
+    assert np.array_equal(pool.tallies(), load("inference", f"{name}_tallies.npy"))
+    prev = load("inference", f"{name}_prev.npy")
+    for c in range(m):
+        assert np.array_equal(tm.banks[c].prev_outputs(), prev[c])
+
+
+def test_inference_vs_oracle_random_large():
+    """Class sums at a bigger random shape (many words, ties, empty clauses)."""
+    rng = np.random.default_rng(7)
+    o, m, n, q = 300, 4, 64, 777
+    bits = (rng.random((q, o)) < 0.5).astype(np.uint8)
+    counters = np.where(rng.random((m, n, 2 * o)) < 0.01, 129 + rng.integers(0, 128, (m, n, 2 * o)),
+                        1 + rng.integers(0, 128, (m, n, 2 * o))).astype(np.uint16)
+    counters[:, ::7, :] = 128  # empty clauses
+    tm = T.MultiClassTM(T.TMConfig(clauses=n), o, m)
+    for c in range(m):
+        tm.banks[c].set_counters(counters[c])
+    ref = O.Machine(o, m, n, 128)
+    ref.set_counters(counters)
+    pool = T.ExamplePool(o, bits, rng.integers(0, m, q).astype(np.int32), m)
+    lits = O.pack_literals(bits)
+    assert np.array_equal(T.class_sums(tm, pool), ref.class_sums(lits))
+    assert np.array_equal(T.predict_all(tm, pool), ref.predict(lits))
+
+
+def test_errors_follow_reference():
+    tm = T.MultiClassTM(T.TMConfig(clauses=4), 12, 2)
+    pool = T.ExamplePool(13, np.zeros((4, 13), np.uint8), np.zeros(4, np.int32), 2)
+    with pytest.raises(ValueError, match="feature count mismatch"):
+        T.train_epoch_parallel(tm, pool, 1, 0)
+    pool2 = T.ExamplePool(12, np.zeros((4, 12), np.uint8), np.zeros(4, np.int32), 2)
+    with pytest.raises(ValueError, match="workers"):
+        T.train_epoch_parallel(tm, pool2, 0, 0)
+    with pytest.raises(ValueError, match="batch"):
+        T.update_clause(tm.banks[0], 0, pool2, 0, None, 0, 0, 15, 3.0, False, T.Rng(1))
+    with pytest.raises(ValueError, match="order length"):
+        T.update_clause(tm.banks[0], 0, pool2, 0, [0, 1], 0, 1, 15, 3.0, False, T.Rng(1))
+    with pytest.raises(IndexError):
+        tm.banks[0].set_counters  # accessor exists
+        T.update_clause(tm.banks[1], 9, pool2, 1, None, 0, 1, 15, 3.0, False, T.Rng(1))
