@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <filesystem>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -495,7 +496,8 @@ int cmd_train(const Args& a) {
   const int W = effective_workers(cfg);
   MultiClassTM tm(cfg, d.features, d.classes);
   ExamplePool pool(d.features, tx, ty, d.classes);
-  ExamplePool test(d.features, vx, vy, d.classes);
+  std::unique_ptr<ExamplePool> test;
+  if (qtu > 0) test = std::make_unique<ExamplePool>(d.features, vx, vy, d.classes);
   for (int e = 0; e < a.epochs; ++e) {
     int epoch = e;
     if (a.fresh) {  // every step = epoch 0 of a fresh machine and pool
@@ -508,7 +510,7 @@ int cmd_train(const Args& a) {
     double acc = -1.0, pred_s = 0.0;
     if (a.eval && qtu > 0) {
       const auto t0 = std::chrono::steady_clock::now();
-      acc = evaluate_accuracy(tm, test);
+      acc = evaluate_accuracy(tm, *test);
       pred_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
     std::printf(
