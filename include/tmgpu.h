@@ -183,9 +183,16 @@ int tmg_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t class_idx, int32_
 
 /* type_i_feedback / type_ii_feedback (feedback.cpp:87-99) on clause j of
  * `bank` for one reference-layout literal row: type 1 = Type I (draws 2o
- * uniforms from rng_state, advanced in place), type 2 = Type II. */
+ * uniforms from rng_state, advanced in place), type 2 = Type II.
+ * clause_output: -1 evaluates the clause first (type_i/ii_feedback);
+ * 0 or 1 uses the given output (detail::type_i/ii_with_output,
+ * feedback.cpp:32-83). */
 int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals, int32_t type,
-                 double s, int32_t boost, uint64_t* rng_state);
+                 double s, int32_t boost, int32_t clause_output, uint64_t* rng_state);
+/* evaluate_clause (core.hpp:208-219) of clause j of `bank` on one
+ * reference-layout literal row; mode TMG_EVAL_TRAIN / TMG_EVAL_PREDICT. */
+int tmg_evaluate_clause(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
+                        int32_t mode, int32_t* out);
 
 /* ---- inference */
 /* refresh_tallies (pool.cpp:108-124): exact Train-mode sums + prev outputs. */

@@ -79,7 +79,8 @@ SIGNATURES = {
     "tmg_epoch_begin": (C.c_int, [P, P, I32]),
     "tmg_pool_apply_reduced": (C.c_int, [P, P]),
     "tmg_update_clause": (C.c_int, [P, P, I32, I32, P, I64, I64, I64, I32, D, I32, P, P]),
-    "tmg_feedback": (C.c_int, [P, I32, I32, P, I32, D, I32, P]),
+    "tmg_feedback": (C.c_int, [P, I32, I32, P, I32, D, I32, I32, P]),
+    "tmg_evaluate_clause": (C.c_int, [P, I32, I32, P, I32, C.POINTER(I32)]),
     "tmg_refresh_tallies": (C.c_int, [P, P]),
     "tmg_class_sums": (C.c_int, [P, P, I32, P]),
     "tmg_predict": (C.c_int, [P, P, P]),

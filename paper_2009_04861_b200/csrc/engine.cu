@@ -922,7 +922,7 @@ TMG_API int tmg_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t c, int32_
 }
 
 TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals, int32_t type,
-                         double s, int32_t boost, uint64_t* rng_state) {
+                         double s, int32_t boost, int32_t clause_output, uint64_t* rng_state) {
   return guarded([&] {
     check_bank(M(tm), bank);
     if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
@@ -940,6 +940,7 @@ TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_
     jb.c = bank;
     jb.j = j;
     jb.forced = type;
+    jb.out_override = clause_output < 0 ? -1 : (clause_output ? 1 : 0);
     jb.batch = 1;
     DevBuf<tmg::MirrorJob> djobs;
     DevBuf<uint64_t> drng;
@@ -979,6 +980,31 @@ TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_
     CK(cudaMemcpyAsync(rng_state, drng.ptr, 32, cudaMemcpyDeviceToHost, tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
     tm->entries_dirty = true;
+  });
+}
+
+TMG_API int tmg_evaluate_clause(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
+                                int32_t mode, int32_t* out) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
+    DeviceGuard dg(tm->device);
+    const int W64 = (2 * tm->o + 63) / 64;
+    DevBuf<uint64_t> dl;
+    DevBuf<uint32_t> xs, ns;
+    DevBuf<int32_t> dout;
+    dl.alloc(W64);
+    xs.alloc(tm->Wp);
+    ns.alloc(tm->Wp);
+    dout.alloc(1);
+    CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    const int lc = bank * tm->n_loc + (j - tm->j_begin);
+    tmg::eval_one_launch(tm->state.ptr, lc, tm->B, tm->Wp, xs.ptr, ns.ptr, mode == TMG_EVAL_TRAIN ? 1 : 0,
+                         dout.ptr, tm->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout.ptr, 4, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
   });
 }
 

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
     }
     const int j = P.j_begin + jl;
     sum += (j & 1) ? -out : out;
-    if (TRAIN) {
+    if (TRAIN && P.prev != nullptr) {  // refresh_tallies also rewrites previous outputs
       const unsigned bits = __ballot_sync(kFull, live && out);
       if (lane == 0 && i < P.q) P.prev[static_cast<size_t>(lc) * P.Wq + (i >> 5)] = bits;
     }
@@ -225,6 +225,21 @@ __global__ void apply_remote_delta_kernel(int32_t* __restrict__ tallies, const i
   own[idx] = 0;
 }
 
+// evaluate_clause (core.hpp:208-219) for one clause and one literal row.
+__global__ void eval_one_kernel(const uint32_t* __restrict__ state, int lc, int B, int Wp,
+                                const uint32_t* __restrict__ x, const uint32_t* __restrict__ n,
+                                int train_mode, int32_t* out) {
+  const uint32_t* top = state + (static_cast<size_t>(lc) * B + (B - 1)) * 2 * Wp;
+  uint32_t viol = 0, any = 0;
+  for (int w = threadIdx.x; w < Wp; w += 32) {
+    const uint32_t ix = top[w], in = top[Wp + w];
+    viol |= (ix & ~x[w]) | (in & ~n[w]);
+    any |= ix | in;
+  }
+  const unsigned vb = __ballot_sync(kFull, viol != 0), ab = __ballot_sync(kFull, any != 0);
+  if (threadIdx.x == 0) *out = ab == 0 ? train_mode : (vb == 0 ? 1 : 0);
+}
+
 // Fresh automata (ClassBank ctor, core.cpp:96-100): counter N is plane value
 // 2^(B-1) - 1, i.e. every plane set except the top one.
 __global__ void init_state_kernel(uint32_t* __restrict__ state, int64_t words, int B, int Wp) {
@@ -303,6 +318,12 @@ void argmax_launch(const int32_t* sums, int32_t* pred, int64_t q, int m, cudaStr
     count_launch();
     argmax_kernel<<<blocks_for(q, 256), 256, 0, s>>>(sums, pred, q, m);
   }
+}
+
+void eval_one_launch(const uint32_t* state, int lc, int B, int Wp, const uint32_t* x, const uint32_t* n,
+                     int train_mode, int32_t* out, cudaStream_t s) {
+  count_launch();
+  eval_one_kernel<<<1, 32, 0, s>>>(state, lc, B, Wp, x, n, train_mode, out);
 }
 
 void init_state_launch(uint32_t* state, int clauses, int B, int Wp, cudaStream_t s) {

@@ -41,8 +41,14 @@ struct MirrorJob {
   int32_t worker;
   int32_t forced;  // 0: gated update_clause steps; 1/2: one forced Type I/II
                    // feedback on literal row 0 (type_i/ii_feedback, feedback.cpp:87-99)
+  int32_t out_override;  // forced jobs: -1 evaluate, 0/1 given clause output
+  int32_t pad;
   int64_t offset, batch;
 };
+
+// One clause on one literal row (evaluate_clause, core.hpp:208-219).
+void eval_one_launch(const uint32_t* state, int lc, int B, int Wp, const uint32_t* x, const uint32_t* n,
+                     int train_mode, int32_t* out, cudaStream_t s);
 
 struct MirrorParams {
   const MirrorJob* jobs;

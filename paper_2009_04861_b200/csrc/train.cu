@@ -281,8 +281,9 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
         n[p] = P.nplane[i * P.Wp + p * 32 + lane];
       }
       const bool type2 = forced ? job.forced == 2 : (target == 1) != positive;
-      const int before = cl.eval_train(x, n);
-      int after = before;
+      const int evald = cl.eval_train(x, n);
+      const int before = (forced && job.out_override >= 0) ? job.out_override : evald;
+      int after = evald;
       if (type2) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
       } else {

@@ -421,7 +421,15 @@ def _feedback(bank: ClassBank, j: int, literals, kind: int, s: float, boost: boo
     lits = _lits2d(bank._tm, literals)[:1].copy()
     state = rng.state if rng is not None else np.zeros(4, np.uint64)
     check(lib().tmg_feedback(bank._tm.handle, bank._c, j, _ptr(lits), kind, float(s), int(bool(boost)),
-                             _ptr(state)))
+                             -1, _ptr(state)))
+
+
+def evaluate_clause(bank: ClassBank, j: int, literals, mode: int) -> int:
+    """evaluate_clause (core.hpp:208-219) on the GPU."""
+    lits = _lits2d(bank._tm, literals)[:1].copy()
+    out = C.c_int32(0)
+    check(lib().tmg_evaluate_clause(bank._tm.handle, bank._c, j, _ptr(lits), mode, C.byref(out)))
+    return int(out.value)
 
 
 def type_i_feedback(bank: ClassBank, j: int, literals, s: float, boost_true_positive: bool, rng: Rng):
