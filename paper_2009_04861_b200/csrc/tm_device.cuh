@@ -148,4 +148,84 @@ __device__ __forceinline__ uint32_t lazy_bernoulli(uint32_t need, uint32_t sel, 
   return less;
 }
 
+// Warp-cooperative exact Bernoulli masks for one Type I event: every lane
+// owns K words of literals; bit b of word k is wanted with probability
+// P_k,b / 2^32 where P = thr_hi if bit b of sel[k] else thr_lo (SEL=false:
+// always thr_lo).
+//   phase 1 — 8 bit-serial rounds on every word (two Philox blocks per word,
+//             the K chains interleaved for ILP). A literal is still undecided
+//             afterwards only if its 8 random bits equal P's top 8 bits
+//             (probability 2^-8).
+//   phase 2 — each still-undecided literal takes one private 32-bit word
+//             from its lane's Philox blocks and compares its low 24 bits
+//             with P's low 24 bits at once.
+// Both phases together are an exact comparison of a 32-bit uniform with P,
+// i.e. an exact Bernoulli(P / 2^32) per literal, at ~2 random words per
+// word of 32 literals instead of one draw per literal.
+// gen(slot, blk) returns Philox block `blk` of word slot `slot` (< K) or of
+// the lane's phase-2 pool (slot == K).
+template <int K, bool SEL, typename Gen>
+__device__ __forceinline__ void bernoulli_words(const uint32_t (&need)[K], const uint32_t (&sel)[K],
+                                                uint32_t thr_hi, uint32_t thr_lo, uint32_t (&less)[K],
+                                                Gen&& gen) {
+  uint32_t und[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    und[k] = need[k];
+    less[k] = 0;
+  }
+#pragma unroll
+  for (int blk = 0; blk < 2; ++blk) {
+    U4 r[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) r[k] = gen(k, blk);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int bit = 31 - 4 * blk - i;
+      const uint32_t ph = ((thr_hi >> bit) & 1u) ? kFull : 0u;
+      const uint32_t pl = ((thr_lo >> bit) & 1u) ? kFull : 0u;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t rb = i == 0 ? r[k].x : (i == 1 ? r[k].y : (i == 2 ? r[k].z : r[k].w));
+        const uint32_t pk = SEL ? ((sel[k] & ph) | (~sel[k] & pl)) : pl;
+        less[k] |= und[k] & ~rb & pk;
+        und[k] &= ~(rb ^ pk);
+      }
+    }
+  }
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) cnt += __popc(und[k]);
+  const uint32_t rest_hi = thr_hi & 0x00FFFFFFu, rest_lo = thr_lo & 0x00FFFFFFu;
+  for (int blk = 2; __any_sync(kFull, cnt > 0); ++blk) {
+    const U4 r = gen(K, blk);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (cnt > 0) {
+        const uint32_t word = i == 0 ? r.x : (i == 1 ? r.y : (i == 2 ? r.z : r.w));
+        int k = 0;
+#pragma unroll
+        for (int kk = K - 1; kk >= 0; --kk)
+          if (und[kk]) k = kk;
+        uint32_t bitmask = 0, s = 0;
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
+          if (kk == k) {
+            bitmask = und[kk] & (0u - und[kk]);
+            s = sel[kk];
+          }
+        const uint32_t rest = (SEL && (s & bitmask)) ? rest_hi : rest_lo;
+        const bool lt = (word >> 8) < rest;
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk)
+          if (kk == k) {
+            und[kk] &= ~bitmask;
+            if (lt) less[kk] |= bitmask;
+          }
+        --cnt;
+      }
+    }
+  }
+}
+
 }  // namespace tmg

@@ -129,8 +129,37 @@ __device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row,
 
 // --------------------------------------------------------------- async ---
 
+// Type I (feedback.cpp:32-70) on every word of the clause with the exact
+// warp-cooperative Bernoulli sampler; counters keyed (clause g, example i,
+// literal word, block) so the draws do not depend on scheduling.
 template <int NW, int B>
-__global__ void __launch_bounds__(128) train_async_kernel(TrainParams P) {
+__device__ __forceinline__ void type_i_async(Clause<NW, B>& cl, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
+                                             int before, const TrainParams& P, uint32_t g, uint32_t i,
+                                             int lane) {
+  constexpr int K = 2 * NW;
+  uint32_t need[K], sel[K], bern[K];
+#pragma unroll
+  for (int p = 0; p < NW; ++p) {
+    need[2 * p] = need[2 * p + 1] = cl.valid[p];
+    sel[2 * p] = x[p];
+    sel[2 * p + 1] = n[p];
+  }
+  auto gen = [&](int slot, int blk) {
+    const uint32_t wid = slot < K ? static_cast<uint32_t>(((slot >> 1) * 32 + lane) * 2 + (slot & 1))
+                                  : (0xFFFF0000u | static_cast<uint32_t>(lane));
+    return philox4x32_10(U4{g, i, wid, static_cast<uint32_t>(blk)}, P.key0, P.key1);
+  };
+  if (before) bernoulli_words<K, true>(need, sel, P.thr_high, P.thr_low, bern, gen);
+  else bernoulli_words<K, false>(need, sel, P.thr_high, P.thr_low, bern, gen);
+#pragma unroll
+  for (int p = 0; p < NW; ++p) {
+    cl.type_i_word(0, p, x[p], before, P.boost, bern[2 * p], P.lo, P.hi);
+    cl.type_i_word(1, p, n[p], before, P.boost, bern[2 * p + 1], P.lo, P.hi);
+  }
+}
+
+template <int NW, int B>
+__global__ void __launch_bounds__(128, 8) train_async_kernel(TrainParams P) {
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= P.m * P.n_loc) return;
@@ -151,6 +180,8 @@ __global__ void __launch_bounds__(128) train_async_kernel(TrainParams P) {
   unsigned long long events = 0, events_type1 = 0;
 
   for (int64_t t0 = P.t_begin; t0 < P.t_end; t0 += 32) {
+    // ---- gates of 32 consecutive steps, one per lane (a legal interleaving
+    // of the reference: other workers' tally adds in this window land later).
     const int64_t t = t0 + lane;
     int64_t i = 0;
     int target = 0;
@@ -162,53 +193,75 @@ __global__ void __launch_bounds__(128) train_async_kernel(TrainParams P) {
       target = __ldg(P.labels + i) == c ? 1 : 0;
       int v = __ldcg(P.tallies + i * P.m + c);  // relaxed, L2-coherent read
       v = v < -T ? -T : (v > T ? T : v);
-      const uint32_t e = static_cast<uint32_t>(target ? T - v : T + v);
+      const int64_t e = target ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
       const U4 r = philox4x32_10(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
       // u < e / 2T  <=>  r * 2T < e * 2^32  (exact integer gate, feedback.cpp:24-28)
-      gated = static_cast<uint64_t>(r.x) * static_cast<uint64_t>(2 * T) <
-              (static_cast<uint64_t>(e) << 32);
+      gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
     }
     unsigned gm = __ballot_sync(kFull, gated);
+    if (!gm) continue;
     events += __popc(gm);
-    while (gm) {
-      const int sl = __ffs(gm) - 1;
-      gm &= gm - 1;
-      const int64_t is = __shfl_sync(kFull, i, sl);
-      const int tg = __shfl_sync(kFull, target, sl);
-      uint32_t x[NW], n[NW];
-      const uint32_t* xr = P.xplane + is * P.Wp + lane;
-      const uint32_t* nr = P.nplane + is * P.Wp + lane;
+
+    // ---- gated steps in order; the next step's literal words and previous-
+    // output word are prefetched while the current one is processed.
+    int sl = __ffs(gm) - 1;
+    gm &= gm - 1;
+    int64_t is = __shfl_sync(kFull, i, sl);
+    int tg = __shfl_sync(kFull, target, sl);
+    uint32_t x[NW], n[NW];
 #pragma unroll
-      for (int p = 0; p < NW; ++p) {
-        x[p] = __ldg(xr + p * 32);
-        n[p] = __ldg(nr + p * 32);
+    for (int p = 0; p < NW; ++p) {
+      x[p] = __ldg(P.xplane + is * P.Wp + p * 32 + lane);
+      n[p] = __ldg(P.nplane + is * P.Wp + p * 32 + lane);
+    }
+    uint32_t pword = lane == 0 ? prev_row[is >> 5] : 0u;
+    while (true) {
+      const bool more = gm != 0;
+      int64_t is2 = 0;
+      int tg2 = 0;
+      uint32_t x2[NW], n2[NW], pword2 = 0;
+      if (more) {
+        const int sl2 = __ffs(gm) - 1;
+        gm &= gm - 1;
+        is2 = __shfl_sync(kFull, i, sl2);
+        tg2 = __shfl_sync(kFull, target, sl2);
+#pragma unroll
+        for (int p = 0; p < NW; ++p) {
+          x2[p] = __ldg(P.xplane + is2 * P.Wp + p * 32 + lane);
+          n2[p] = __ldg(P.nplane + is2 * P.Wp + p * 32 + lane);
+        }
+        if (lane == 0) pword2 = prev_row[is2 >> 5];
       }
-      uint32_t pword = 0;
-      if (lane == 0) pword = prev_row[is >> 5];
       const int before = cl.eval_train(x, n);
       int after = before;
       if ((tg == 1) != positive) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
       } else {
         ++events_type1;
-#pragma unroll
-        for (int p = 0; p < NW; ++p) {
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            const uint32_t lit = part ? n[p] : x[p];
-            const uint32_t word_id = static_cast<uint32_t>((p * 32 + lane) * 2 + part);
-            const uint32_t bern = lazy_bernoulli(
-                cl.valid[p], before ? lit : 0u, P.thr_high, P.thr_low, [&](int blk) {
-                  return philox4x32_10(U4{g, static_cast<uint32_t>(is), word_id,
-                                          static_cast<uint32_t>(blk)},
-                                       P.key0, P.key1);
-                });
-            cl.type_i_word(part, p, lit, before, P.boost, bern, P.lo, P.hi);
-          }
-        }
+        type_i_async<NW, B>(cl, x, n, before, P, g, static_cast<uint32_t>(is), lane);
         after = cl.eval_train(x, n);
       }
-      if (lane == 0) record(P, prev_row, is, c, positive, pword, after);
+      if (lane == 0) {
+        const uint32_t bit = 1u << (is & 31);
+        if (((pword & bit) != 0) != (after != 0)) {
+          pword ^= bit;
+          prev_row[is >> 5] = pword;
+          int delta = after ? 1 : -1;
+          if (!positive) delta = -delta;
+          atomicAdd(&P.tallies[is * P.m + c], delta);
+          if (P.tally_delta) atomicAdd(&P.tally_delta[is * P.m + c], delta);
+        }
+        if (more && (is2 >> 5) == (is >> 5)) pword2 = pword;  // same bitmap word: forward
+      }
+      if (!more) break;
+      is = is2;
+      tg = tg2;
+#pragma unroll
+      for (int p = 0; p < NW; ++p) {
+        x[p] = x2[p];
+        n[p] = n2[p];
+      }
+      pword = pword2;
     }
   }
   cl.store(st, P.Wp, lane);

@@ -9,7 +9,9 @@ nvidia-smi > "$out/nvidia_smi_$tag.txt" 2>&1
 nproc > "$out/nproc_$tag.txt"; lscpu >> "$out/nproc_$tag.txt" 2>&1
 ( timeout 1200 python -m pytest tests -m gpu -q -rA --timeout 900 -p no:cacheprovider > "$out/pytest_gpu_$tag.txt" 2>&1; echo "exit $?" >> "$out/pytest_gpu_$tag.txt" )
 ( timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$out/smoke_$tag.txt" 2>&1; echo "exit $?" >> "$out/smoke_$tag.txt" )
-( timeout 900 python bench.py ${BENCH_ARGS:---steps 3 --warmup 3} > "$out/bench_$tag.json" 2> "$out/bench_$tag.err"; echo "exit $?" >> "$out/bench_$tag.err" )
+if [ "${BENCH:-1}" = "1" ]; then
+  ( timeout 900 python bench.py ${BENCH_ARGS:---steps 3 --warmup 3} > "$out/bench_$tag.json" 2> "$out/bench_$tag.err"; echo "exit $?" >> "$out/bench_$tag.err" )
+fi
 if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
       --log-file "$out/launches_$tag.csv" python bench.py --steps 2 --warmup 3 --no-cpu > "$out/ncu_launch_bench_$tag.txt" 2>&1
