@@ -165,6 +165,11 @@ int tmg_pool_delta_device_ptr(tmg_pool* pool, void** ptr);
  *     workers == 1 the result is bit-identical to the reference. */
 int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
                     tmg_epoch_report* report);
+/* train_epoch_sequential (trainer.cpp:138-179): the classic trainer replayed
+ * bit-exactly (one CTA; clause evaluation in parallel, the reference's single
+ * xoshiro stream serial). feedback_events: num_classes entries. */
+int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, double* seconds,
+                               uint64_t* feedback_events);
 /* Multi-GPU building blocks: one asynchronous window [t_begin, t_end) of every
  * clause's pass of `epoch`. Deltas are also accumulated in the pool's delta
  * buffer; after an allreduce of that buffer call tmg_pool_apply_reduced. */

@@ -126,6 +126,11 @@ class ClassBank {
  public:
   ClassBank(int feature_count, int clause_count, int state_depth,
             PolarityScheme scheme = PolarityScheme::Alternating);
+  ClassBank(const ClassBank& other);  // deep copy (value semantics, like the reference)
+  ClassBank& operator=(const ClassBank& other);
+  ClassBank(ClassBank&&) noexcept = default;
+  ClassBank& operator=(ClassBank&&) noexcept = default;
+  ~ClassBank();
 
   int feature_count() const { return o_; }
   int literal_count() const { return 2 * o_; }

@@ -9,12 +9,12 @@ from .tsetlin import (MODE_ASYNC, MODE_SYNC_MIRROR, PREDICT, TRAIN, ClassBank, E
                       ExamplePool, MultiClassTM, Rng, TMConfig, class_sums, classify, device_count,
                       epoch_order, evaluate_accuracy, export_vote_sums, literal_words, predict_all,
                       predict_literals, refresh_tallies, train_epoch_parallel, type_i_feedback,
-                      type_ii_feedback, update_clause, vote_sum)
+                      train_epoch_sequential, type_ii_feedback, update_clause, vote_sum)
 
 __all__ = [
     "MODE_ASYNC", "MODE_SYNC_MIRROR", "PREDICT", "TRAIN", "ClassBank", "EpochReport",
     "ExamplePool", "MultiClassTM", "Rng", "TMConfig", "class_sums", "classify", "device_count",
     "epoch_order", "evaluate_accuracy", "export_vote_sums", "literal_words", "predict_all",
     "predict_literals", "refresh_tallies", "train_epoch_parallel", "type_i_feedback",
-    "type_ii_feedback", "update_clause", "vote_sum",
+    "type_ii_feedback", "update_clause", "vote_sum", "train_epoch_sequential",
 ]

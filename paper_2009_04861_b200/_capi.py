@@ -76,6 +76,7 @@ SIGNATURES = {
     "tmg_pool_delta_device_ptr": (C.c_int, [P, PP]),
     "tmg_train_epoch": (C.c_int, [P, P, I32, I32, I32, C.POINTER(EpochReportC)]),
     "tmg_train_window": (C.c_int, [P, P, I32, I64, I64, P]),
+    "tmg_train_epoch_sequential": (C.c_int, [P, P, I32, C.POINTER(D), P]),
     "tmg_epoch_begin": (C.c_int, [P, P, I32]),
     "tmg_pool_apply_reduced": (C.c_int, [P, P]),
     "tmg_update_clause": (C.c_int, [P, P, I32, I32, P, I64, I64, I64, I32, D, I32, P, P]),

@@ -852,6 +852,45 @@ TMG_API int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32
   });
 }
 
+TMG_API int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, double* seconds,
+                                       uint64_t* feedback_events) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    if (tm->m < 2) fail(TMG_EINVAL, "classification needs at least two banks");  // trainer.cpp:141-143
+    if (tm->n_loc != tm->n) fail(TMG_EINVAL, "the sequential trainer needs the full (unsharded) machine");
+    DeviceGuard dg(tm->device);
+    const auto wall0 = std::chrono::steady_clock::now();
+    // Rng(seed, mix_stream(1, epoch)) shuffles, then keeps feeding the epoch.
+    tmg_rng r;
+    tmg_rng_seed(&r, tm->cfg.seed, tmg_mix_stream(TMG_STREAM_SEQUENTIAL, static_cast<uint64_t>(epoch), 0));
+    std::vector<int32_t> order(static_cast<size_t>(pool->q));
+    tmg_shuffled_indices(static_cast<int32_t>(pool->q), &r, order.data());
+    CK(cudaMemcpyAsync(pool->order.ptr, order.data(), order.size() * 4, cudaMemcpyHostToDevice, tm->stream));
+    DevBuf<uint64_t> drng;
+    drng.alloc(4);
+    CK(cudaMemcpyAsync(drng.ptr, r.s, 32, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
+    tmg::TrainParams p = make_params(tm, pool);
+    tmg::SeqParams sp{};
+    sp.rng = drng.ptr;
+    sp.p_high = (tm->cfg.specificity - 1.0) / tm->cfg.specificity;
+    sp.p_low = 1.0 / tm->cfg.specificity;
+    sp.events = tm->events.ptr;
+    if (!tmg::train_sequential_launch(p, sp, tm->B, tm->stream)) fail(TMG_ERUNTIME, "no sequential kernel for B");
+    CK(cudaGetLastError());
+    std::vector<unsigned long long> ev(2 * static_cast<size_t>(tm->m));
+    CK(cudaMemcpyAsync(ev.data(), tm->events.ptr, tm->events.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    tm->entries_dirty = true;
+    if (feedback_events)
+      for (int c = 0; c < tm->m; ++c) feedback_events[c] = ev[static_cast<size_t>(c)];
+    if (seconds) {
+      const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+      *seconds = secs > 0 ? secs : 1e-9;
+    }
+  });
+}
+
 TMG_API unsigned long long tmg_kernel_launches(void) {
   return __atomic_load_n(&tmg::g_launches, __ATOMIC_RELAXED);
 }

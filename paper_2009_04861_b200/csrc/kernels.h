@@ -57,6 +57,13 @@ struct MirrorParams {
   double p_high, p_low;
 };
 
+struct SeqParams {  // classic sequential trainer mirror (trainer.cpp:138-179)
+  const uint64_t* rng;  // xoshiro state after the epoch shuffle
+  double p_high, p_low;
+  unsigned long long* events;  // [m]
+};
+bool train_sequential_launch(const TrainParams& p, const SeqParams& sp, int B, cudaStream_t s);
+
 struct EvalEntry {  // one nonzero include word of a clause
   uint32_t w, inc_x, inc_n, pad;
 };

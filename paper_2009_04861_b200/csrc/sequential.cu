@@ -1,0 +1,206 @@
+// sequential.cu — bit-exact GPU mirror of the classic sequential trainer
+// (train_epoch_sequential / feed_bank_sequential, proj/src/trainer.cpp:57-85,
+// 138-179).
+//
+// One CTA per epoch. Per example the two fed banks are evaluated by all warps
+// in parallel (clause per warp, literal words per lane, Train mode), the vote
+// sum is reduced in shared memory, and warp 0 then replays the reference's
+// single xoshiro256++ stream: one gate draw per clause, 2o Type I draws in
+// literal order, the negative-class draw below(m-1) — exactly the reference's
+// draw order, so automaton states match bit for bit. The automata are read
+// and written in place in their bit-plane layout (any NW, any B).
+#include "kernels.h"
+#include "tm_device.cuh"
+
+namespace tmg {
+
+namespace {
+
+constexpr int kSeqThreads = 1024;
+
+__device__ __forceinline__ uint32_t below_dev(Xoshiro& r, uint32_t bound) {  // rng.hpp:68-79
+  uint64_t m = static_cast<uint64_t>(static_cast<uint32_t>(r.next())) * bound;
+  uint32_t low = static_cast<uint32_t>(m);
+  if (low < bound) {
+    const uint32_t cutoff = (0u - bound) % bound;
+    while (low < cutoff) {
+      m = static_cast<uint64_t>(static_cast<uint32_t>(r.next())) * bound;
+      low = static_cast<uint32_t>(m);
+    }
+  }
+  return static_cast<uint32_t>(m >> 32);
+}
+
+template <int B>
+__device__ __forceinline__ void load_word(const uint32_t* base, int Wp, int part, int w, Planes<B>& s) {
+#pragma unroll
+  for (int b = 0; b < B; ++b) s.p[b] = base[(b * 2 + part) * Wp + w];
+}
+
+template <int B>
+__device__ __forceinline__ void store_word(uint32_t* base, int Wp, int part, int w, const Planes<B>& s) {
+#pragma unroll
+  for (int b = 0; b < B; ++b) base[(b * 2 + part) * Wp + w] = s.p[b];
+}
+
+__device__ __forceinline__ uint32_t valid_bits(int w, int o) {
+  const int first = w * 32;
+  return first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
+}
+
+template <int B>
+__global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainParams P, SeqParams S) {
+  extern __shared__ uint32_t smem[];
+  const int L = 2 * P.o;
+  const int refw = (L + 31) / 32 + 2;
+  uint32_t* hbits = smem;                 // u < p_high, reference literal order
+  uint32_t* lbits = smem + refw;          // u < p_low
+  uint32_t* outs = smem + 2 * refw;       // clause outputs of the fed bank (bit per clause)
+  __shared__ int vote;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int n = P.n, Wp = P.Wp, T = P.margin;
+  const size_t cstride = static_cast<size_t>(B) * 2 * Wp;
+  Xoshiro rng{S.rng[0], S.rng[1], S.rng[2], S.rng[3]};
+  unsigned long long ev_local = 0;
+  for (int k = tid; k < 2 * refw; k += blockDim.x) smem[k] = 0;
+
+  for (int64_t t = 0; t < P.q; ++t) {
+    const int64_t i = P.order[t];
+    const int y = P.labels[i];
+    // negative class (trainer.cpp:159-165), drawn before the two feeds
+    __shared__ int neg_s;
+    if (tid == 0) {
+      int neg;
+      if (P.m == 2) {
+        neg = 1 - y;
+      } else {
+        neg = static_cast<int>(below_dev(rng, static_cast<uint32_t>(P.m - 1)));
+        if (neg >= y) ++neg;
+      }
+      neg_s = neg;
+    }
+    __syncthreads();
+    const int neg = neg_s;
+    const uint32_t* xr = P.xplane + i * Wp;
+    const uint32_t* nr = P.nplane + i * Wp;
+    for (int feed = 0; feed < 2; ++feed) {
+      const int c = feed == 0 ? y : neg;
+      const int target = feed == 0 ? 1 : 0;
+      // ---- vote pass: every clause of bank c, Train mode (trainer.cpp:62-68)
+      if (tid == 0) vote = 0;
+      for (int k = tid; k < (n + 31) / 32; k += blockDim.x) outs[k] = 0;
+      __syncthreads();
+      for (int j = warp; j < n; j += nwarps) {
+        const uint32_t* top = P.state + (static_cast<size_t>(c) * n + j) * cstride + static_cast<size_t>(B - 1) * 2 * Wp;
+        uint32_t viol = 0, any = 0;
+        for (int w = lane; w < Wp; w += 32) {
+          const uint32_t ix = top[w], in = top[Wp + w];
+          viol |= (ix & ~xr[w]) | (in & ~nr[w]);
+          any |= ix | in;
+        }
+        const unsigned vb = __ballot_sync(kFull, viol != 0), ab = __ballot_sync(kFull, any != 0);
+        const int out = ab == 0 ? 1 : (vb == 0 ? 1 : 0);
+        if (lane == 0 && out) {
+          atomicOr(&outs[j >> 5], 1u << (j & 31));
+          atomicAdd(&vote, (j & 1) ? -1 : 1);
+        }
+      }
+      __syncthreads();
+      // ---- serial gate + feedback replay by warp 0 (trainer.cpp:69-83)
+      if (warp == 0) {
+        const int v0 = vote;
+        const int vc = v0 < -T ? -T : (v0 > T ? T : v0);
+        const int e = target ? T - vc : T + vc;
+        const double p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+        for (int j = 0; j < n; ++j) {
+          int gated = 0;
+          if (lane == 0) gated = rng.uniform() < p ? 1 : 0;
+          gated = __shfl_sync(kFull, gated, 0);
+          if (!gated) continue;
+          ++ev_local;
+          const int out = (outs[j >> 5] >> (j & 31)) & 1;
+          uint32_t* base = P.state + (static_cast<size_t>(c) * n + j) * cstride;
+          const bool positive = (j & 1) == 0;
+          if ((target == 1) != positive) {  // Type II (feedback.cpp:72-83)
+            if (out) {
+              for (int w = lane; w < Wp; w += 32) {
+                const uint32_t vm = valid_bits(w, P.o);
+                for (int part = 0; part < 2; ++part) {
+                  Planes<B> s;
+                  load_word<B>(base, Wp, part, w, s);
+                  const uint32_t lit = part ? nr[w] : xr[w];
+                  const uint32_t inc = ~lit & ~s.p[B - 1] & vm;
+                  if (inc) {
+                    add_one<B>(s, inc);
+                    store_word<B>(base, Wp, part, w, s);
+                  }
+                }
+              }
+            }
+          } else {  // Type I: 2o draws in literal order (feedback.cpp:45,63)
+            if (lane == 0) {
+              uint32_t hw = 0, lw = 0;
+              for (int k = 0; k < L; ++k) {
+                const double u = rng.uniform();
+                hw |= (u < S.p_high ? 1u : 0u) << (k & 31);
+                lw |= (u < S.p_low ? 1u : 0u) << (k & 31);
+                if ((k & 31) == 31 || k == L - 1) {
+                  hbits[k >> 5] = hw;
+                  lbits[k >> 5] = lw;
+                  hw = lw = 0;
+                }
+              }
+            }
+            __syncwarp();
+            for (int w = lane; w < Wp; w += 32) {
+              if (w * 32 >= P.o) continue;
+              const uint32_t vm = valid_bits(w, P.o);
+              const int k1 = P.o + w * 32;
+              const uint32_t hsel[2] = {hbits[w], __funnelshift_r(hbits[k1 >> 5], hbits[(k1 >> 5) + 1], k1 & 31)};
+              const uint32_t lsel[2] = {lbits[w], __funnelshift_r(lbits[k1 >> 5], lbits[(k1 >> 5) + 1], k1 & 31)};
+              for (int part = 0; part < 2; ++part) {
+                Planes<B> s;
+                load_word<B>(base, Wp, part, w, s);
+                const uint32_t lit = part ? nr[w] : xr[w];
+                uint32_t inc = 0, dec;
+                if (out) {
+                  const uint32_t bern = (lit & hsel[part]) | (~lit & lsel[part]);
+                  inc = lit & (bern | (P.boost ? s.p[B - 1] : 0u)) & vm;
+                  dec = ~lit & bern & vm;
+                } else {
+                  dec = lsel[part] & vm;
+                }
+                step<B>(s, inc, dec, P.lo, P.hi);
+                store_word<B>(base, Wp, part, w, s);
+              }
+            }
+            __syncwarp();
+          }
+          if (lane == 0) S.events[c] += 1;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  (void)ev_local;
+}
+
+}  // namespace
+
+bool train_sequential_launch(const TrainParams& p, const SeqParams& sp, int B, cudaStream_t s) {
+  const int refw = (2 * p.o + 31) / 32 + 2;
+  const size_t shm = sizeof(uint32_t) * (2 * refw + (p.n + 31) / 32);
+  auto go = [&](auto kern) {
+    if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
+    count_launch();
+    kern<<<1, kSeqThreads, shm, s>>>(p, sp);
+  };
+  switch (B) {
+    case 4: go(train_sequential_kernel<4>); return true;
+    case 8: go(train_sequential_kernel<8>); return true;
+    case 15: go(train_sequential_kernel<15>); return true;
+    default: return false;
+  }
+}
+
+}  // namespace tmg

@@ -19,6 +19,10 @@ namespace tmg {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+#ifndef TMG_PHILOX_ROUNDS
+#define TMG_PHILOX_ROUNDS 10
+#endif
+
 // ---------------------------------------------------------------- Philox ---
 // Counter-based Philox4x32-10 (Salmon et al., SC'11). Keyed per (seed, epoch);
 // counters carry (clause, example, literal word, draw block).
@@ -28,7 +32,7 @@ struct U4 {
 
 __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int r = 0; r < TMG_PHILOX_ROUNDS; ++r) {
     const uint32_t lo0 = 0xD2511F53u * c.x;
     const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
     const uint32_t lo1 = 0xCD9E8D57u * c.z;

@@ -159,7 +159,15 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B>& cl, const uint32_t (
 }
 
 template <int NW, int B>
-__global__ void __launch_bounds__(128, 8) train_async_kernel(TrainParams P) {
+#ifndef TMG_ASYNC_MINB
+#define TMG_ASYNC_MINB 0
+#endif
+#if TMG_ASYNC_MINB > 0
+#define TMG_ASYNC_BOUNDS __launch_bounds__(128, TMG_ASYNC_MINB)
+#else
+#define TMG_ASYNC_BOUNDS __launch_bounds__(128)
+#endif
+__global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= P.m * P.n_loc) return;
@@ -446,7 +454,6 @@ bool dispatch_mirror(const TrainParams& p, const MirrorParams& mp, int NW, cudaS
 
 bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
   switch (B) {
-    case 2: return dispatch_async<2>(p, NW, s, blocks);
     case 4: return dispatch_async<4>(p, NW, s, blocks);
     case 8: return dispatch_async<8>(p, NW, s, blocks);
     case 15: return dispatch_async<15>(p, NW, s, blocks);
@@ -456,7 +463,6 @@ bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int
 
 bool train_mirror_launch(const TrainParams& p, const MirrorParams& mp, int B, int NW, cudaStream_t s) {
   switch (B) {
-    case 2: return dispatch_mirror<2>(p, mp, NW, s);
     case 4: return dispatch_mirror<4>(p, mp, NW, s);
     case 8: return dispatch_mirror<8>(p, mp, NW, s);
     case 15: return dispatch_mirror<15>(p, mp, NW, s);

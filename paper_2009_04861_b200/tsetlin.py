@@ -331,6 +331,14 @@ def train_epoch_parallel(tm: MultiClassTM, pool: ExamplePool, workers: int, epoc
     return r
 
 
+def train_epoch_sequential(tm: MultiClassTM, pool: ExamplePool, epoch: int) -> EpochReport:
+    """train_epoch_sequential (trainer.cpp:138-179), replayed bit-exactly on the GPU."""
+    ev = np.zeros(tm.num_banks(), np.uint64)
+    secs = C.c_double(0)
+    check(lib().tmg_train_epoch_sequential(tm.handle, pool.handle, epoch, C.byref(secs), _ptr(ev)))
+    return EpochReport(epoch, secs.value, secs.value, [int(v) for v in ev])
+
+
 def update_clause(bank: ClassBank, j: int, pool: ExamplePool, class_idx: int, order, offset: int,
                   batch: int, margin: int, s: float, boost_true_positive: bool, rng: Rng) -> int:
     """update_clause (trainer.cpp:102-136) with the reference stream `rng`."""

@@ -10,3 +10,5 @@ for d in rng pack gate feedback update_clause epoch_par_w1 epoch_seq inference; 
   rm -rf "$here/$d"
 done
 "$repo/oracle/_ref/ref_driver" golden "$here"
+# Transcript of the same-source drop-in driver built against the reference.
+"$repo/oracle/_ref/api_driver_ref" > "$here/api_driver_ref.txt"

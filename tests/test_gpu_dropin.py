@@ -1,0 +1,55 @@
+"""The drop-in check: tests/cpp/api_driver.cpp, written only against the
+reference's public C++ API, is compiled once against the reference (CPU,
+oracle/_ref/api_driver_ref; transcript in tests/golden/api_driver_ref.txt)
+and once against include/tsetlin/*.hpp + libtsetlin_b200.so (GPU). Every
+deterministic result must be identical."""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+from tests.golden_io import EPOCH_CASES, GOLDEN, load, manifest
+
+pytestmark = pytest.mark.gpu
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GPU_DRIVER = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "api_driver_gpu")
+REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "api_driver_ref")
+
+
+def _lines(text):
+    return [l for l in text.splitlines() if l.strip()]
+
+
+def test_same_source_driver_matches_reference():
+    assert os.path.exists(GPU_DRIVER), "build first (make -C paper_2009_04861_b200/csrc)"
+    gpu = subprocess.run([GPU_DRIVER], capture_output=True, text=True, timeout=600)
+    assert gpu.returncode == 0, gpu.stderr
+    want = _lines(open(os.path.join(GOLDEN, "api_driver_ref.txt")).read())
+    if os.path.exists(REF_DRIVER):  # the live reference binary, when it travelled
+        want = _lines(subprocess.run([REF_DRIVER], capture_output=True, text=True, check=True).stdout)
+    got = _lines(gpu.stdout)
+    diffs = [(w, g) for w, g in zip(want, got) if w != g]
+    assert len(got) == len(want) and not diffs, f"first differences: {diffs[:5]}"
+
+
+@pytest.mark.parametrize("name", EPOCH_CASES)
+def test_sequential_trainer_bit_exact(name):
+    """train_epoch_sequential (f1) replayed on the GPU == the reference."""
+    import paper_2009_04861_b200 as T
+    d = ("epoch_seq", name)
+    man = manifest(*d)
+    pool = T.ExamplePool(man["o"], load(*d, "train_x.npy"), load(*d, "train_y.npy"), man["m"])
+    cfg = T.TMConfig(clauses=man["n"], margin=man["margin"], specificity=man["s"], state_depth=man["N"],
+                     boost_true_positive=bool(man["boost"]), seed=man["seed"])
+    tm = T.MultiClassTM(cfg, man["o"], man["m"])
+    for ep in man["epochs"]:
+        e = ep["epoch"]
+        rep = T.train_epoch_sequential(tm, pool, e)
+        assert rep.feedback_events == ep["feedback_events"], f"events epoch {e}"
+        counters = load(*d, f"epoch{e}_counters.npy")
+        for c in range(man["m"]):
+            assert np.array_equal(tm.banks[c].counters(), counters[c]), f"epoch {e} bank {c}"
+    test = T.ExamplePool(man["o"], load(*d, "test_x.npy"), load(*d, "test_y.npy"), man["m"])
+    assert np.array_equal(T.class_sums(tm, test), load(*d, "test_sums.npy"))
+    assert np.array_equal(T.predict_all(tm, test), load(*d, "test_pred.npy"))
