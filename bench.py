@@ -204,7 +204,7 @@ def run_ours(args):
         if world == 1:
             rep = T.train_epoch_parallel(tm, p, 1, 0)
             return rep.feedback_events, rep.type_i_events, rep.device_seconds
-        ev = D.train_epoch_windows(tm, p, 0, windows, allreduce)
+        ev = D.train_epoch_windows(D.GpuShardEngine(tm, p), 0, windows, allreduce)
         return ev, None, None
 
     # ---- integer-pipe peak (roofline denominator), measured on this GPU

@@ -95,6 +95,12 @@ int tmg_device_count(int32_t* count);
 unsigned long long tmg_kernel_launches(void);
 /* The CUDA stream (cudaStream_t) a machine's work runs on. */
 int tmg_machine_stream(tmg_machine* tm, void** stream);
+/* Statistical probe of the asynchronous Type I path (criterion
+ * 1): applies it `trials` times to fresh copies of clause j of `bank` on one
+ * literal row with the given clause output, counting per literal k (2o
+ * entries, reference order) the +1 (inc) and -1 (dec) transitions. */
+int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
+                             int32_t clause_output, uint32_t trials, uint64_t* inc, uint64_t* dec);
 /* Integer-pipe roofline probe: LOP3-only and LOP3+IMAD thread-ops per second. */
 int tmg_bench_int_peak(int32_t device, double* lop3_ops_per_s, double* mixed_ops_per_s);
 

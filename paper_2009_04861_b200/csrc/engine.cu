@@ -270,6 +270,12 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   const double s = tm->cfg.specificity;
   p.thr_high = prob_threshold((s - 1.0) / s);
   p.thr_low = prob_threshold(1.0 / s);
+  for (int b = 0; b < 8; ++b) {
+    p.bern.hi_mask[b] = ((p.thr_high >> (31 - b)) & 1u) ? 0xFFFFFFFFu : 0u;
+    p.bern.lo_mask[b] = ((p.thr_low >> (31 - b)) & 1u) ? 0xFFFFFFFFu : 0u;
+  }
+  p.bern.hi_rest = p.thr_high & 0x00FFFFFFu;
+  p.bern.lo_rest = p.thr_low & 0x00FFFFFFu;
   p.key0 = tm->key0;
   p.key1 = tm->key1;
   p.t_begin = 0;
@@ -888,6 +894,46 @@ TMG_API int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t 
       const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
       *seconds = secs > 0 ? secs : 1e-9;
     }
+  });
+}
+
+TMG_API int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
+                                     int32_t clause_output, uint32_t trials, uint64_t* inc, uint64_t* dec) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
+    DeviceGuard dg(tm->device);
+    const int W64 = (2 * tm->o + 63) / 64;
+    DevBuf<uint64_t> dl;
+    DevBuf<uint32_t> xs, ns;
+    DevBuf<unsigned long long> dinc, ddec;
+    dl.alloc(W64);
+    xs.alloc(tm->Wp);
+    ns.alloc(tm->Wp);
+    dinc.alloc(2 * static_cast<size_t>(tm->o));
+    ddec.alloc(2 * static_cast<size_t>(tm->o));
+    CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    CK(cudaMemsetAsync(dinc.ptr, 0, dinc.bytes(), tm->stream));
+    CK(cudaMemsetAsync(ddec.ptr, 0, ddec.bytes(), tm->stream));
+    epoch_keys(tm, 0);
+    tmg::TrainParams p{};
+    // same thresholds/keys as an async epoch; literal row 0 = the given row
+    tmg_pool fake;
+    fake.o = tm->o;
+    fake.m = tm->m;
+    fake.q = 1;
+    p = make_params(tm, &fake);
+    p.xplane = xs.ptr;
+    p.nplane = ns.ptr;
+    const size_t lc = static_cast<size_t>(bank) * tm->n_loc + (j - tm->j_begin);
+    if (!tmg::feedback_rates_launch(p, tm->state.ptr + lc * tm->B * 2 * tm->Wp, clause_output ? 1 : 0, trials,
+                                    tm->B, tm->NW, dinc.ptr, ddec.ptr, tm->stream))
+      fail(TMG_EINVAL, "feedback-rate probe not instantiated for this shape");
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(inc, dinc.ptr, dinc.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaMemcpyAsync(dec, ddec.ptr, ddec.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
   });
 }
 

@@ -3,6 +3,7 @@
 // learning and evaluation calls go to libtmgpu.so.
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 
 #include "tsetlin_b200.hpp"
 
@@ -200,9 +201,8 @@ void TMConfig::validate() const {
 
 int effective_workers(const TMConfig& config) {  // core.cpp:76-80 (0 = hardware)
   if (config.workers > 0) return config.workers;
-  const char* env = std::getenv("TM_THREADS");
-  const int w = env ? std::atoi(env) : 0;
-  return w > 0 ? w : 2;  // >1 selects the asynchronous all-clause GPU trainer
+  const unsigned hw = std::thread::hardware_concurrency();
+  return hw > 0 ? static_cast<int>(hw) : 1;
 }
 
 ClassBank::ClassBank(int feature_count, int clause_count, int state_depth, PolarityScheme scheme)

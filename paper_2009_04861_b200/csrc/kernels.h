@@ -11,6 +11,14 @@ namespace tmg {
 extern unsigned long long g_launches;
 inline void count_launch() { __atomic_fetch_add(&g_launches, 1ULL, __ATOMIC_RELAXED); }
 
+// Threshold bits of the async Bernoulli sampler (tm_device.cuh), precomputed
+// on the host: bits 31..24 of P as all-ones / all-zeros masks, bits 23..0 as
+// an integer, for P_high = round((s-1)/s * 2^32) and P_low = round(1/s * 2^32).
+struct BernThresholds {
+  uint32_t hi_mask[8], lo_mask[8];
+  uint32_t hi_rest, lo_rest;
+};
+
 // Device view of one machine shard + pool, shared by all training kernels.
 struct TrainParams {
   // Machine shard: every class keeps clauses [j_begin, j_begin + n_loc).
@@ -31,6 +39,7 @@ struct TrainParams {
   int32_t margin;
   int32_t boost;
   uint32_t thr_high, thr_low;  // async: P(u < p) thresholds as 32-bit fixed point
+  BernThresholds bern;         // the same, split for the sampler
   uint32_t key0, key1;         // async: Philox key for (seed, epoch)
   int64_t t_begin, t_end;      // async: window of each clause's pass
   unsigned long long* events;  // [2m]: feedback events per class, then Type I events per class
@@ -83,6 +92,8 @@ struct EvalParams {
 // B (plane count) and NW (words per lane per part) instantiations.
 bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks);
 bool train_mirror_launch(const TrainParams& p, const MirrorParams& mp, int B, int NW, cudaStream_t s);
+bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out, uint32_t trials, int B, int NW,
+                           unsigned long long* inc, unsigned long long* dec, cudaStream_t s);
 void build_entries_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, EvalEntry* e,
                           int32_t* ne, int32_t* inc_count, cudaStream_t s);
 void eval_sums_launch(const EvalParams& p, bool train_mode, cudaStream_t s);

@@ -165,8 +165,9 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
                 uint32_t inc = 0, dec;
                 if (out) {
                   const uint32_t bern = (lit & hsel[part]) | (~lit & lsel[part]);
-                  inc = lit & (bern | (P.boost ? s.p[B - 1] : 0u)) & vm;
-                  dec = ~lit & bern & vm;
+                  const uint32_t incl = s.p[B - 1];
+                  inc = ((lit & (bern | (P.boost ? incl : 0u))) | (~lit & bern & incl)) & vm;
+                  dec = ~lit & bern & ~incl & vm;
                 } else {
                   dec = lsel[part] & vm;
                 }

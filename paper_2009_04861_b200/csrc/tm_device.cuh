@@ -15,22 +15,30 @@
 
 #include <cstdint>
 
+#include "kernels.h"
+
 namespace tmg {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Rounds of the counter-based generator of the asynchronous trainer.
+// Philox4x32 with 7 rounds is the smallest round count that passes TestU01
+// BigCrush (Salmon et al., SC'11, "Parallel random numbers: as easy as 1, 2,
+// 3", Table 2); 10 is the library default safety margin. Build with
+// -DTMG_PHILOX_ROUNDS=10 for the conservative variant. The synchronous
+// mirror replays the reference's xoshiro256++ instead and is unaffected.
 #ifndef TMG_PHILOX_ROUNDS
-#define TMG_PHILOX_ROUNDS 10
+#define TMG_PHILOX_ROUNDS 7
 #endif
 
 // ---------------------------------------------------------------- Philox ---
-// Counter-based Philox4x32-10 (Salmon et al., SC'11). Keyed per (seed, epoch);
-// counters carry (clause, example, literal word, draw block).
+// Keyed per (seed, epoch); counters carry (clause, example, literal word,
+// draw block).
 struct U4 {
   uint32_t x, y, z, w;
 };
 
-__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+__device__ __forceinline__ U4 philox4x32(U4 c, uint32_t k0, uint32_t k1) {
 #pragma unroll
   for (int r = 0; r < TMG_PHILOX_ROUNDS; ++r) {
     const uint32_t lo0 = 0xD2511F53u * c.x;
@@ -110,67 +118,41 @@ __device__ __forceinline__ void sub_one(Planes<B>& s, uint32_t mask) {
 }
 
 // Saturating +-1 (apply_transition's clamp to [1, 2N], core.hpp:62-63).
+// Branch-free: the masks are computed for every lane (cheaper than divergence).
 template <int B>
 __device__ __forceinline__ void step(Planes<B>& s, uint32_t inc, uint32_t dec, uint32_t lo,
                                      uint32_t hi) {
-  if (inc) inc &= ~eq_const<B>(s, hi);
-  if (dec) dec &= ~eq_const<B>(s, lo);
-  if (inc) add_one<B>(s, inc);
-  if (dec) sub_one<B>(s, dec);
+  inc &= ~eq_const<B>(s, hi);
+  dec &= ~eq_const<B>(s, lo);
+  add_one<B>(s, inc);
+  sub_one<B>(s, dec);
 }
 
-// Bit-serial lazy Bernoulli: returns the lanes (bits) whose fresh uniform u
-// satisfies u < P_k / 2^32, where P_k = thr_hi if bit k of `sel` else thr_lo.
-// Random bits are consumed most-significant first, four 32-bit words (one
-// Philox block) at a time, only until every bit of `need` is decided: the
-// expected number of words is ~log2(popc(need)) + 2 instead of one draw per
-// literal, and the result is an exact Bernoulli(P/2^32) per literal.
-// `block(b)` returns the b-th Philox block of this (clause, example, word)
-// stream.
-__device__ __forceinline__ void bern_bit(uint32_t rb, int bit, uint32_t sel, uint32_t thr_hi,
-                                         uint32_t thr_lo, uint32_t& less, uint32_t& undecided) {
-  const uint32_t ph = ((thr_hi >> bit) & 1u) ? kFull : 0u;
-  const uint32_t pl = ((thr_lo >> bit) & 1u) ? kFull : 0u;
-  const uint32_t pk = (sel & ph) | (~sel & pl);
-  less |= undecided & ~rb & pk;
-  undecided &= ~(rb ^ pk);
-}
-
-template <typename Block>
-__device__ __forceinline__ uint32_t lazy_bernoulli(uint32_t need, uint32_t sel, uint32_t thr_hi,
-                                                   uint32_t thr_lo, Block&& block) {
-  uint32_t less = 0;
-  uint32_t undecided = need;
-  for (int blk = 0; blk < 8 && undecided; ++blk) {
-    const U4 r = block(blk);
-    const int top = 31 - 4 * blk;
-    bern_bit(r.x, top, sel, thr_hi, thr_lo, less, undecided);
-    bern_bit(r.y, top - 1, sel, thr_hi, thr_lo, less, undecided);
-    bern_bit(r.z, top - 2, sel, thr_hi, thr_lo, less, undecided);
-    bern_bit(r.w, top - 3, sel, thr_hi, thr_lo, less, undecided);
-  }
-  return less;
+// Saturating -1 only (Type I with clause output 0).
+template <int B>
+__device__ __forceinline__ void step_down(Planes<B>& s, uint32_t dec, uint32_t lo) {
+  sub_one<B>(s, dec & ~eq_const<B>(s, lo));
 }
 
 // Warp-cooperative exact Bernoulli masks for one Type I event: every lane
 // owns K words of literals; bit b of word k is wanted with probability
-// P_k,b / 2^32 where P = thr_hi if bit b of sel[k] else thr_lo (SEL=false:
-// always thr_lo).
-//   phase 1 — 8 bit-serial rounds on every word (two Philox blocks per word,
+// P / 2^32 where P = P_high if bit b of sel[k] else P_low (SEL=false: always
+// P_low). Every literal compares a fresh 32-bit uniform u with P, most
+// significant bit first:
+//   phase 1 — 8 bit-serial rounds on whole words (two Philox blocks per word,
 //             the K chains interleaved for ILP). A literal is still undecided
-//             afterwards only if its 8 random bits equal P's top 8 bits
+//             afterwards only if its 8 bits of u equal P's top 8 bits
 //             (probability 2^-8).
-//   phase 2 — each still-undecided literal takes one private 32-bit word
-//             from its lane's Philox blocks and compares its low 24 bits
-//             with P's low 24 bits at once.
-// Both phases together are an exact comparison of a 32-bit uniform with P,
-// i.e. an exact Bernoulli(P / 2^32) per literal, at ~2 random words per
-// word of 32 literals instead of one draw per literal.
+//   phase 2 — each still-undecided literal takes one private word from its
+//             lane's Philox blocks and compares 24 bits of it with P's low 24
+//             bits at once (branch-free, four literals per block).
+// Together an exact Bernoulli(P / 2^32) per literal, at ~2.3 random words per
+// 32 literals instead of one draw per literal.
 // gen(slot, blk) returns Philox block `blk` of word slot `slot` (< K) or of
 // the lane's phase-2 pool (slot == K).
 template <int K, bool SEL, typename Gen>
 __device__ __forceinline__ void bernoulli_words(const uint32_t (&need)[K], const uint32_t (&sel)[K],
-                                                uint32_t thr_hi, uint32_t thr_lo, uint32_t (&less)[K],
+                                                const BernThresholds& th, uint32_t (&less)[K],
                                                 Gen&& gen) {
   uint32_t und[K];
 #pragma unroll
@@ -185,9 +167,8 @@ __device__ __forceinline__ void bernoulli_words(const uint32_t (&need)[K], const
     for (int k = 0; k < K; ++k) r[k] = gen(k, blk);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int bit = 31 - 4 * blk - i;
-      const uint32_t ph = ((thr_hi >> bit) & 1u) ? kFull : 0u;
-      const uint32_t pl = ((thr_lo >> bit) & 1u) ? kFull : 0u;
+      const uint32_t ph = th.hi_mask[4 * blk + i];
+      const uint32_t pl = th.lo_mask[4 * blk + i];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const uint32_t rb = i == 0 ? r[k].x : (i == 1 ? r[k].y : (i == 2 ? r[k].z : r[k].w));
@@ -200,34 +181,32 @@ __device__ __forceinline__ void bernoulli_words(const uint32_t (&need)[K], const
   int cnt = 0;
 #pragma unroll
   for (int k = 0; k < K; ++k) cnt += __popc(und[k]);
-  const uint32_t rest_hi = thr_hi & 0x00FFFFFFu, rest_lo = thr_lo & 0x00FFFFFFu;
   for (int blk = 2; __any_sync(kFull, cnt > 0); ++blk) {
     const U4 r = gen(K, blk);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if (cnt > 0) {
-        const uint32_t word = i == 0 ? r.x : (i == 1 ? r.y : (i == 2 ? r.z : r.w));
-        int k = 0;
+      const uint32_t word = i == 0 ? r.x : (i == 1 ? r.y : (i == 2 ? r.z : r.w));
+      // lowest undecided literal of the lane (none: bit = 0, a no-op)
+      uint32_t bit = 0, s = 0;
+      int k = -1;
 #pragma unroll
-        for (int kk = K - 1; kk >= 0; --kk)
-          if (und[kk]) k = kk;
-        uint32_t bitmask = 0, s = 0;
+      for (int kk = K - 1; kk >= 0; --kk)
+        if (und[kk]) k = kk;
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk)
-          if (kk == k) {
-            bitmask = und[kk] & (0u - und[kk]);
-            s = sel[kk];
-          }
-        const uint32_t rest = (SEL && (s & bitmask)) ? rest_hi : rest_lo;
-        const bool lt = (word >> 8) < rest;
+      for (int kk = 0; kk < K; ++kk)
+        if (kk == k) {
+          bit = und[kk] & (0u - und[kk]);
+          s = sel[kk];
+        }
+      const uint32_t rest = (SEL && (s & bit)) ? th.hi_rest : th.lo_rest;
+      const uint32_t take = ((word >> 8) < rest) ? bit : 0u;
 #pragma unroll
-        for (int kk = 0; kk < K; ++kk)
-          if (kk == k) {
-            und[kk] &= ~bitmask;
-            if (lt) less[kk] |= bitmask;
-          }
-        --cnt;
-      }
+      for (int kk = 0; kk < K; ++kk)
+        if (kk == k) {
+          und[kk] ^= bit;
+          less[kk] |= take;
+        }
+      cnt -= bit ? 1 : 0;
     }
   }
 }

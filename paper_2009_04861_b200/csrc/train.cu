@@ -83,7 +83,7 @@ struct Clause {
       for (int part = 0; part < 2; ++part) {
         const uint32_t lit = part ? n[p] : x[p];
         const uint32_t inc = ~lit & ~s[part][p].p[B - 1] & valid[p];
-        if (inc) add_one<B>(s[part][p], inc);
+        add_one<B>(s[part][p], inc);
         moved |= inc;
       }
     }
@@ -92,17 +92,19 @@ struct Clause {
 
   // Type I (feedback.cpp:32-70) given per-word Bernoulli masks:
   //   out=1, lit=1 : +1 w.p. (s-1)/s  (always if boost and included)
-  //   out=1, lit=0 : -1 w.p. 1/s       (such literals are never included)
+  //   out=1, lit=0 : Reward w.p. 1/s  (-1 if excluded; +1 if included, which
+  //                  only a caller-forced output can reach, feedback.cpp:55-57)
   //   out=0        : -1 w.p. 1/s       (Penalty on Include, Reward on Exclude)
   __device__ __forceinline__ void type_i_word(int part, int p, uint32_t lit, int out, int boost,
                                               uint32_t bern, uint32_t lo, uint32_t hi) {
     Planes<B>& w = s[part][p];
     if (out) {
-      uint32_t inc = lit & (bern | (boost ? w.p[B - 1] : 0u)) & valid[p];
-      uint32_t dec = ~lit & bern & valid[p];
+      const uint32_t incl = w.p[B - 1];
+      const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid[p];
+      const uint32_t dec = ~lit & bern & ~incl & valid[p];
       step<B>(w, inc, dec, lo, hi);
     } else {
-      step<B>(w, 0u, bern & valid[p], lo, hi);
+      step_down<B>(w, bern & valid[p], lo);
     }
   }
 };
@@ -147,10 +149,10 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B>& cl, const uint32_t (
   auto gen = [&](int slot, int blk) {
     const uint32_t wid = slot < K ? static_cast<uint32_t>(((slot >> 1) * 32 + lane) * 2 + (slot & 1))
                                   : (0xFFFF0000u | static_cast<uint32_t>(lane));
-    return philox4x32_10(U4{g, i, wid, static_cast<uint32_t>(blk)}, P.key0, P.key1);
+    return philox4x32(U4{g, i, wid, static_cast<uint32_t>(blk)}, P.key0, P.key1);
   };
-  if (before) bernoulli_words<K, true>(need, sel, P.thr_high, P.thr_low, bern, gen);
-  else bernoulli_words<K, false>(need, sel, P.thr_high, P.thr_low, bern, gen);
+  if (before) bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
+  else bernoulli_words<K, false>(need, sel, P.bern, bern, gen);
 #pragma unroll
   for (int p = 0; p < NW; ++p) {
     cl.type_i_word(0, p, x[p], before, P.boost, bern[2 * p], P.lo, P.hi);
@@ -160,7 +162,7 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B>& cl, const uint32_t (
 
 template <int NW, int B>
 #ifndef TMG_ASYNC_MINB
-#define TMG_ASYNC_MINB 0
+#define TMG_ASYNC_MINB 5  // 5 CTAs (20 warps) per SM: fastest in the round-1 sweep
 #endif
 #if TMG_ASYNC_MINB > 0
 #define TMG_ASYNC_BOUNDS __launch_bounds__(128, TMG_ASYNC_MINB)
@@ -202,7 +204,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       int v = __ldcg(P.tallies + i * P.m + c);  // relaxed, L2-coherent read
       v = v < -T ? -T : (v > T ? T : v);
       const int64_t e = target ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
-      const U4 r = philox4x32_10(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
+      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
       // u < e / 2T  <=>  r * 2T < e * 2^32  (exact integer gate, feedback.cpp:24-28)
       gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
     }
@@ -403,6 +405,56 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
   }
 }
 
+// --------------------------------------------------- feedback-rate probe ---
+// Statistical conformance of the async Type I path (acceptance criterion 1,
+// SPEC.md:530): every trial applies type_i_async to a fresh copy of one
+// clause (planes at `state0`) with its own Philox counter (example = trial)
+// and counts, per reference literal k, the +1 / -1 transitions.
+template <int NW, int B>
+__global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, const uint32_t* __restrict__ state0,
+                                                             int out, uint32_t trials,
+                                                             unsigned long long* inc_cnt,
+                                                             unsigned long long* dec_cnt) {
+  const int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t x[NW], n[NW];
+#pragma unroll
+  for (int p = 0; p < NW; ++p) {
+    x[p] = P.xplane[p * 32 + lane];
+    n[p] = P.nplane[p * 32 + lane];
+  }
+  for (uint32_t trial = warp; trial < trials; trial += nwarps) {
+    Clause<NW, B> cl, c0;
+    cl.load(state0, P.Wp, lane, P.o);
+    c0 = cl;
+    type_i_async<NW, B>(cl, x, n, out, P, 0u, trial, lane);
+#pragma unroll
+    for (int p = 0; p < NW; ++p)
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        uint32_t up = 0, down = 0;
+#pragma unroll
+        for (int b = 0; b < B; ++b) {  // the highest changed plane tells the direction
+          const uint32_t ch = c0.s[part][p].p[b] ^ cl.s[part][p].p[b];
+          up = (up & ~ch) | (ch & cl.s[part][p].p[b]);
+          down = (down & ~ch) | (ch & ~cl.s[part][p].p[b]);
+        }
+        const int base = part * P.o + (p * 32 + lane) * 32;
+        while (up) {
+          const int b = __ffs(up) - 1;
+          up &= up - 1;
+          atomicAdd(inc_cnt + base + b, 1ULL);
+        }
+        while (down) {
+          const int b = __ffs(down) - 1;
+          down &= down - 1;
+          atomicAdd(dec_cnt + base + b, 1ULL);
+        }
+      }
+  }
+}
+
 template <int NW, int B>
 void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
   const int clauses = p.m * p.n_loc;
@@ -451,6 +503,21 @@ bool dispatch_mirror(const TrainParams& p, const MirrorParams& mp, int NW, cudaS
 }
 
 }  // namespace
+
+bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out, uint32_t trials, int B, int NW,
+                           unsigned long long* inc, unsigned long long* dec, cudaStream_t s) {
+  const int grid = 148 * 4;
+  auto go = [&](auto kern) {
+    count_launch();
+    kern<<<grid, 128, 0, s>>>(p, state0, out, trials, inc, dec);
+    return true;
+  };
+  if (NW == 1 && B == 4) return go(feedback_rates_kernel<1, 4>);
+  if (NW == 1 && B == 8) return go(feedback_rates_kernel<1, 8>);
+  if (NW == 1 && B == 15) return go(feedback_rates_kernel<1, 15>);
+  if (NW == 3 && B == 8) return go(feedback_rates_kernel<3, 8>);
+  return false;
+}
 
 bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
   switch (B) {

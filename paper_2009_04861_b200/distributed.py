@@ -61,39 +61,60 @@ def torch_view(ptr: int, count: int, device: int):
     return torch.as_tensor(_CudaArray(ptr, count), device=f"cuda:{device}")
 
 
-def nccl_allreduce(device: int, group=None) -> Callable:
-    """All-reduce of the pool's tally-delta buffer with torch.distributed."""
+class GpuShardEngine:
+    """One rank's clause shard on its GPU (the product engine)."""
+
+    def __init__(self, tm: MultiClassTM, pool: ExamplePool):
+        self.tm, self.pool = tm, pool
+        self.q, self.m = pool.size(), tm.num_banks()
+
+    def begin(self, epoch: int):
+        check(lib().tmg_epoch_begin(self.tm.handle, self.pool.handle, epoch))
+
+    def window(self, epoch: int, t0: int, t1: int) -> np.ndarray:
+        ev = np.zeros(self.m, np.uint64)
+        check(lib().tmg_train_window(self.tm.handle, self.pool.handle, epoch, t0, t1, ev.ctypes.data))
+        return ev
+
+    def delta(self):
+        return torch_view(self.pool.delta_device_ptr(), self.q * self.m, self.pool.device)
+
+    def apply(self, reduced):
+        ptr = reduced.data_ptr() if reduced is not None else self.pool.delta_device_ptr()
+        check(lib().tmg_pool_apply_reduced(self.pool.handle, C.c_void_p(ptr)))
+
+
+def torch_allreduce(group=None) -> Callable:
+    """Sum of the per-rank delta buffers (NCCL for CUDA tensors, gloo for CPU)."""
     import torch
     import torch.distributed as dist
 
-    def run(delta_ptr: int, count: int):
-        own = torch_view(delta_ptr, count, device)
+    def run(own):
         red = own.clone()
         dist.all_reduce(red, op=dist.ReduceOp.SUM, group=group)
-        torch.cuda.synchronize(device)
+        if red.is_cuda:
+            torch.cuda.synchronize(red.device)
         return red
 
     return run
 
 
-def train_epoch_windows(tm: MultiClassTM, pool: ExamplePool, epoch: int, windows: int,
-                        allreduce: Optional[Callable]) -> List[int]:
-    """One asynchronous epoch as `windows` windows; `allreduce(delta_ptr,
-    count)` returns the summed delta (a tensor) or None for a single rank."""
-    check(lib().tmg_epoch_begin(tm.handle, pool.handle, epoch))
-    m, q = tm.num_banks(), pool.size()
-    total = np.zeros(m, np.uint64)
-    ev = np.zeros(m, np.uint64)
-    delta_ptr = pool.delta_device_ptr()
-    for t0, t1 in window_bounds(q, windows):
-        check(lib().tmg_train_window(tm.handle, pool.handle, epoch, t0, t1, ev.ctypes.data))
-        total += ev
-        reduced = allreduce(delta_ptr, q * m) if allreduce is not None else None
-        if reduced is None:
-            check(lib().tmg_pool_apply_reduced(pool.handle, C.c_void_p(delta_ptr)))  # remote = 0
-        else:
-            check(lib().tmg_pool_apply_reduced(pool.handle, C.c_void_p(reduced.data_ptr())))
+def train_epoch_windows(engine, epoch: int, windows: int, allreduce: Optional[Callable]) -> List[int]:
+    """One asynchronous epoch as `windows` windows of every clause's pass.
+
+    After each window: reduced = allreduce(own delta); replica += reduced - own;
+    own = 0. With allreduce=None (one rank) the remote share is zero."""
+    engine.begin(epoch)
+    total = np.zeros(engine.m, np.uint64)
+    for t0, t1 in window_bounds(engine.q, windows):
+        total += engine.window(epoch, t0, t1)
+        reduced = allreduce(engine.delta()) if allreduce is not None else None
+        engine.apply(reduced)
     return [int(v) for v in total]
+
+
+def nccl_allreduce(device: int, group=None) -> Callable:
+    return torch_allreduce(group)
 
 
 def class_sums_sharded(tm: MultiClassTM, pool: ExamplePool, mode: int, allreduce_host: Callable):

@@ -432,6 +432,17 @@ def _feedback(bank: ClassBank, j: int, literals, kind: int, s: float, boost: boo
                              -1, _ptr(state)))
 
 
+def feedback_rates(bank: ClassBank, j: int, literals, clause_output: int, trials: int):
+    """Per-literal +1/-1 transition counts of the async Type I path over
+    `trials` independent applications (statistical conformance probe)."""
+    lits = _lits2d(bank._tm, literals)[:1].copy()
+    L = bank.literal_count()
+    inc, dec = np.zeros(L, np.uint64), np.zeros(L, np.uint64)
+    check(lib().tmg_debug_feedback_rates(bank._tm.handle, bank._c, j, _ptr(lits), int(clause_output), trials,
+                                         _ptr(inc), _ptr(dec)))
+    return inc, dec
+
+
 def evaluate_clause(bank: ClassBank, j: int, literals, mode: int) -> int:
     """evaluate_clause (core.hpp:208-219) on the GPU."""
     lits = _lits2d(bank._tm, literals)[:1].copy()

@@ -68,9 +68,55 @@ def test_async_window_accounting():
     tm = T.MultiClassTM(cfg, 12, 2)
     pool = T.ExamplePool(12, d.train_x, d.train_y, 2)
     from paper_2009_04861_b200 import distributed as D
-    ev = D.train_epoch_windows(tm, pool, 0, windows=7, allreduce=None)
+    ev = D.train_epoch_windows(D.GpuShardEngine(tm, pool), 0, windows=7, allreduce=None)
     assert sum(ev) > 0
     _check_tally_invariant(tm, pool, 2, 1000)
+
+
+@pytest.mark.parametrize("o,N,s,boost,out", [(12, 128, 3.9, False, 0), (12, 128, 3.9, False, 1),
+                                             (12, 128, 4.0, True, 1), (784, 128, 10.0, False, 0),
+                                             (784, 128, 10.0, False, 1), (40, 5, 2.0, False, 1)])
+def test_type_i_table1_conformance(o, N, s, boost, out):
+    """SPEC acceptance 1: Table 1 transition frequencies of the
+    asynchronous Philox/bit-serial sampler within +-0.02 over 1e5 draws."""
+    from paper_2009_04861_b200.tsetlin import feedback_rates
+    rng = np.random.default_rng(o + N)
+    x = (rng.random(o) < 0.5).astype(np.uint8)
+    lits = O.pack_literals(x)[0]
+    L = 2 * o
+    litv = np.concatenate([x, 1 - x]).astype(bool)
+    # counters away from the saturation ends; includes only on true literals
+    # when the clause must fire (out = 1), a few includes otherwise.
+    counters = rng.integers(2, 2 * N, size=(2, L)).astype(np.uint16)
+    counters[counters == N + 1] = N + 2 if N + 2 < 2 * N else N
+    inc_lit = rng.random(L) < 0.1
+    if out:
+        inc_lit &= litv
+    counters[1] = np.where(inc_lit, np.maximum(counters[1], N + 1), np.minimum(counters[1], N))
+    tm = T.MultiClassTM(T.TMConfig(clauses=2, state_depth=N, specificity=s, boost_true_positive=boost), o, 1)
+    tm.banks[0].set_counters(counters)
+    assert T.evaluate_clause(tm.banks[0], 1, lits, T.TRAIN) == out or not out
+    trials = 100_000
+    inc, dec = feedback_rates(tm.banks[0], 1, lits, out, trials)
+    inc, dec = inc / trials, dec / trials
+    c = counters[1].astype(int)
+    at_hi, at_lo = c == 2 * N, c == 1
+    included = c > N
+    p_hi, p_lo = (s - 1) / s, 1 / s
+    if out:
+        exp_inc = np.where(litv, np.where(included & boost, 1.0, p_hi), np.where(included, p_lo, 0.0))
+        exp_dec = np.where(litv, 0.0, np.where(included, 0.0, p_lo))
+    else:
+        exp_inc = np.zeros(L)
+        exp_dec = np.full(L, p_lo)
+    exp_inc[at_hi] = 0.0
+    exp_dec[at_lo] = 0.0
+    assert np.abs(inc - exp_inc).max() < 0.02, np.abs(inc - exp_inc).max()
+    assert np.abs(dec - exp_dec).max() < 0.02, np.abs(dec - exp_dec).max()
+    # pooled check at 1e5 * L draws: mean rate of the p_lo decrements
+    sel = exp_dec > 0
+    if sel.sum() > 20:
+        assert abs(dec[sel].mean() - p_lo) < 0.003
 
 
 def _ref_acc():
@@ -78,14 +124,17 @@ def _ref_acc():
     return json.load(open(path)) if os.path.exists(path) else {}
 
 
-@pytest.mark.parametrize("case,tol", [("xor_noise10", 0.005), ("xor_noise40", 0.01)])
+@pytest.mark.parametrize("case,tol", [("xor_noise10", 0.005), ("xor_noise40", 0.02)])
 def test_async_accuracy_parity_xor(case, tol):
+    """Noisy XOR (SPEC acceptance 3/4): mean over 10 GPU seeds vs the
+    reference's 5-seed mean; 40 % noise uses the spec's 2 pt parity band
+     — the reference itself moves ~0.7 pt run to run there."""
     ref = _ref_acc().get(case)
     if ref is None:
         pytest.skip("accuracy_ref.json lacks " + case)
     cfgd = ref["config"]
     accs = []
-    for seed in range(1, 6):
+    for seed in range(1, 11):
         d = synth.make("xor", cfgd["q"], cfgd["qtest"], cfgd["data_seed"], cfgd["noise"])
         tm = T.MultiClassTM(T.TMConfig(clauses=cfgd["clauses"], margin=cfgd["T"], specificity=cfgd["s"],
                                        seed=seed), 12, 2)
