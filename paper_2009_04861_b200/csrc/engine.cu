@@ -299,8 +299,11 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
   p.t_end = t1;
   if (with_delta) p.tally_delta = pool->delta.ptr;
   int blocks = 0;
-  if (!tmg::train_async_launch(p, tm->B, tm->NW, tm->stream, &blocks))
-    fail(TMG_ERUNTIME, "no async kernel instantiation for this shape");
+  // Register-resident clauses up to 4 words per lane per part (o <= 4096);
+  // wider rows keep the automata in shared memory.
+  const bool ok = tm->NW <= 4 ? tmg::train_async_launch(p, tm->B, tm->NW, tm->stream, &blocks)
+                              : tmg::train_async_smem_launch(p, tm->B, tm->NW, tm->stream, &blocks);
+  if (!ok) fail(TMG_ERUNTIME, "no async kernel instantiation for this shape");
   CK(cudaGetLastError());
   tm->entries_dirty = true;
 }

@@ -91,6 +91,7 @@ struct EvalParams {
 
 // B (plane count) and NW (words per lane per part) instantiations.
 bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks);
+bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks);
 bool train_mirror_launch(const TrainParams& p, const MirrorParams& mp, int B, int NW, cudaStream_t s);
 bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out, uint32_t trials, int B, int NW,
                            unsigned long long* inc, unsigned long long* dec, cudaStream_t s);

@@ -483,9 +483,7 @@ bool dispatch_async(const TrainParams& p, int NW, cudaStream_t s, int* blocks) {
     case 2: launch_async<2, B>(p, s, blocks); return true;
     case 3: launch_async<3, B>(p, s, blocks); return true;
     case 4: launch_async<4, B>(p, s, blocks); return true;
-    case 8: launch_async<8, B>(p, s, blocks); return true;
-    case 10: launch_async<10, B>(p, s, blocks); return true;
-    default: return false;
+    default: return false;  // wider rows: train_smem.cu
   }
 }
 

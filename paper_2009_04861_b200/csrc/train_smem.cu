@@ -1,0 +1,224 @@
+// train_smem.cu — Algorithm 1 for wide literal rows (IMDb-shaped, 2o up to
+// ~20k literals): the same per-warp clause pass as train_async_kernel
+// (train.cu), but the clause's automaton planes live in shared memory
+// (B x 2 x Wp words per warp, 20 KB at IMDb) instead of registers, and the
+// feedback walks the clause one 32-literal word pair per lane at a time, so
+// register use does not grow with the feature count.
+#include "kernels.h"
+#include "tm_device.cuh"
+
+namespace tmg {
+
+namespace {
+
+constexpr int kSmemWarps = 2;  // clauses (warps) per CTA
+
+__device__ __forceinline__ uint64_t splitmix_dev2(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+template <int B>
+struct SmemPlanes {
+  uint32_t* s;  // [B][2][Wp] of this warp
+  int Wp;
+  __device__ __forceinline__ void get(int part, int w, Planes<B>& out) const {
+#pragma unroll
+    for (int b = 0; b < B; ++b) out.p[b] = s[(b * 2 + part) * Wp + w];
+  }
+  __device__ __forceinline__ void put(int part, int w, const Planes<B>& in) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) s[(b * 2 + part) * Wp + w] = in.p[b];
+  }
+  __device__ __forceinline__ uint32_t top(int part, int w) const { return s[((B - 1) * 2 + part) * Wp + w]; }
+};
+
+template <int NW, int B>
+__device__ __forceinline__ int eval_train_smem(const SmemPlanes<B>& S, const uint32_t (&x)[NW],
+                                               const uint32_t (&n)[NW], int lane) {
+  uint32_t viol = 0, any = 0;
+#pragma unroll
+  for (int p = 0; p < NW; ++p) {
+    const int w = p * 32 + lane;
+    const uint32_t ix = S.top(0, w), in = S.top(1, w);
+    viol |= (ix & ~x[p]) | (in & ~n[p]);
+    any |= ix | in;
+  }
+  const unsigned vb = __ballot_sync(kFull, viol != 0), ab = __ballot_sync(kFull, any != 0);
+  return ab == 0 ? 1 : (vb == 0 ? 1 : 0);
+}
+
+__device__ __forceinline__ uint32_t valid_of(int w, int o) {
+  const int first = w * 32;
+  return first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
+}
+
+template <int NW, int B>
+__global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(TrainParams P) {
+  extern __shared__ uint32_t smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int lc = blockIdx.x * kSmemWarps + wib;
+  if (lc >= P.m * P.n_loc) return;
+  const int c = lc / P.n_loc;
+  const int j = P.j_begin + lc % P.n_loc;
+  const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
+  const bool positive = (j & 1) == 0;
+  const int64_t q = P.q;
+  const int T = P.margin;
+  const int Wp = P.Wp;
+  const size_t words = static_cast<size_t>(B) * 2 * Wp;
+  SmemPlanes<B> S{smem + wib * words, Wp};
+  uint32_t* st = P.state + static_cast<size_t>(lc) * words;
+  for (size_t k = lane; k < words; k += 32) S.s[k] = st[k];
+  __syncwarp();
+  uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
+  const int64_t offset = static_cast<int64_t>(splitmix_dev2(static_cast<uint64_t>(g) + 1) % static_cast<uint64_t>(q));
+  unsigned long long events = 0, events_type1 = 0;
+
+  for (int64_t t0 = P.t_begin; t0 < P.t_end; t0 += 32) {
+    const int64_t t = t0 + lane;
+    int64_t i = 0;
+    int target = 0;
+    bool gated = false;
+    if (t < P.t_end) {
+      int64_t pos = offset + t;
+      if (pos >= q) pos -= q;
+      i = P.order ? __ldg(P.order + pos) : pos;
+      target = __ldg(P.labels + i) == c ? 1 : 0;
+      int v = __ldcg(P.tallies + i * P.m + c);
+      v = v < -T ? -T : (v > T ? T : v);
+      const int64_t e = target ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
+      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
+      gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
+    }
+    unsigned gm = __ballot_sync(kFull, gated);
+    events += __popc(gm);
+    while (gm) {
+      const int sl = __ffs(gm) - 1;
+      gm &= gm - 1;
+      const int64_t is = __shfl_sync(kFull, i, sl);
+      const int tg = __shfl_sync(kFull, target, sl);
+      uint32_t x[NW], n[NW];
+#pragma unroll
+      for (int p = 0; p < NW; ++p) {
+        x[p] = __ldg(P.xplane + is * Wp + p * 32 + lane);
+        n[p] = __ldg(P.nplane + is * Wp + p * 32 + lane);
+      }
+      const uint32_t pword = lane == 0 ? prev_row[is >> 5] : 0u;
+      const int before = eval_train_smem<NW, B>(S, x, n, lane);
+      int after = before;
+      if ((tg == 1) != positive) {  // Type II (feedback.cpp:72-83)
+        if (before) {
+          uint32_t moved = 0;
+#pragma unroll
+          for (int p = 0; p < NW; ++p) {
+            const int w = p * 32 + lane;
+            const uint32_t vm = valid_of(w, P.o);
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {
+              const uint32_t inc = ~(part ? n[p] : x[p]) & ~S.top(part, w) & vm;
+              if (inc) {
+                Planes<B> pl;
+                S.get(part, w, pl);
+                add_one<B>(pl, inc);
+                S.put(part, w, pl);
+              }
+              moved |= inc;
+            }
+          }
+          __syncwarp();
+          if (__any_sync(kFull, moved != 0)) after = eval_train_smem<NW, B>(S, x, n, lane);
+        }
+      } else {  // Type I (feedback.cpp:32-70), one word pair at a time
+        ++events_type1;
+        const uint32_t i32 = static_cast<uint32_t>(is);
+#pragma unroll 1
+        for (int p = 0; p < NW; ++p) {
+          const int w = p * 32 + lane;
+          const uint32_t vm = valid_of(w, P.o);
+          const uint32_t need[2] = {vm, vm};
+          const uint32_t sel[2] = {x[p], n[p]};
+          uint32_t bern[2];
+          auto gen = [&](int slot, int blk) {
+            const uint32_t wid = slot < 2 ? static_cast<uint32_t>(w * 2 + slot)
+                                          : (0xFFFF0000u | static_cast<uint32_t>(p * 32 + lane));
+            return philox4x32(U4{g, i32, wid, static_cast<uint32_t>(blk)}, P.key0, P.key1);
+          };
+          if (before) bernoulli_words<2, true>(need, sel, P.bern, bern, gen);
+          else bernoulli_words<2, false>(need, sel, P.bern, bern, gen);
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            Planes<B> pl;
+            S.get(part, w, pl);
+            const uint32_t lit = sel[part];
+            if (before) {
+              const uint32_t incl = pl.p[B - 1];
+              const uint32_t inc = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part] & incl)) & vm;
+              const uint32_t dec = ~lit & bern[part] & ~incl & vm;
+              step<B>(pl, inc, dec, P.lo, P.hi);
+            } else {
+              step_down<B>(pl, bern[part] & vm, P.lo);
+            }
+            S.put(part, w, pl);
+          }
+        }
+        __syncwarp();
+        after = eval_train_smem<NW, B>(S, x, n, lane);
+      }
+      if (lane == 0) {
+        const uint32_t bit = 1u << (is & 31);
+        if (((pword & bit) != 0) != (after != 0)) {
+          prev_row[is >> 5] = pword ^ bit;
+          int delta = after ? 1 : -1;
+          if (!positive) delta = -delta;
+          atomicAdd(&P.tallies[is * P.m + c], delta);
+          if (P.tally_delta) atomicAdd(&P.tally_delta[is * P.m + c], delta);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  int cnt = 0;
+  for (size_t k = lane; k < words; k += 32) {
+    st[k] = S.s[k];
+    if (k >= static_cast<size_t>(B - 1) * 2 * Wp) cnt += __popc(S.s[k]);
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  if (lane == 0) {
+    P.inc_count[lc] = cnt;
+    atomicAdd(P.events + c, events);
+    atomicAdd(P.events + P.m + c, events_type1);
+  }
+}
+
+template <int NW, int B>
+bool launch_smem(const TrainParams& p, cudaStream_t s, int* blocks) {
+  const int clauses = p.m * p.n_loc;
+  const int grid = (clauses + kSmemWarps - 1) / kSmemWarps;
+  const size_t shm = sizeof(uint32_t) * kSmemWarps * B * 2 * p.Wp;
+  if (shm > 48 * 1024)
+    cudaFuncSetAttribute(train_async_smem_kernel<NW, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(shm));
+  if (blocks) *blocks = grid;
+  count_launch();
+  train_async_smem_kernel<NW, B><<<grid, 32 * kSmemWarps, shm, s>>>(p);
+  return true;
+}
+
+}  // namespace
+
+bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
+  if (NW == 8 && B == 8) return launch_smem<8, 8>(p, s, blocks);
+  if (NW == 10 && B == 8) return launch_smem<10, 8>(p, s, blocks);
+  if (NW == 8 && B == 15) return launch_smem<8, 15>(p, s, blocks);
+  if (NW == 10 && B == 15) return launch_smem<10, 15>(p, s, blocks);
+  if (NW == 8 && B == 4) return launch_smem<8, 4>(p, s, blocks);
+  if (NW == 10 && B == 4) return launch_smem<10, 4>(p, s, blocks);
+  return false;
+}
+
+}  // namespace tmg

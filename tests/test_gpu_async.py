@@ -126,15 +126,17 @@ def _ref_acc():
 
 @pytest.mark.parametrize("case,tol", [("xor_noise10", 0.005), ("xor_noise40", 0.02)])
 def test_async_accuracy_parity_xor(case, tol):
-    """Noisy XOR (SPEC acceptance 3/4): mean over 10 GPU seeds vs the
+    """Noisy XOR (SPEC acceptance 3/4): mean over 20 GPU seeds vs the
     reference's 5-seed mean; 40 % noise uses the spec's 2 pt parity band
-     — the reference itself moves ~0.7 pt run to run there."""
+    (SPEC.md:533). At 40 % noise the accuracy depends on the asynchronous
+    schedule itself: the reference measures 0.953 with one worker and
+    0.982-0.988 with eight."""
     ref = _ref_acc().get(case)
     if ref is None:
         pytest.skip("accuracy_ref.json lacks " + case)
     cfgd = ref["config"]
     accs = []
-    for seed in range(1, 11):
+    for seed in range(1, 21):
         d = synth.make("xor", cfgd["q"], cfgd["qtest"], cfgd["data_seed"], cfgd["noise"])
         tm = T.MultiClassTM(T.TMConfig(clauses=cfgd["clauses"], margin=cfgd["T"], specificity=cfgd["s"],
                                        seed=seed), 12, 2)
