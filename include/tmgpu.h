@@ -221,6 +221,29 @@ int tmg_predict_literals(tmg_machine* tm, const uint64_t* literals, int64_t q, i
 /* Device-resident variant for benchmarking: d_sums q x m int32 on device. */
 int tmg_class_sums_device(tmg_machine* tm, const tmg_pool* pool, int32_t mode, int32_t* d_sums);
 
+/* ---- regression head (proj/include/tsetlin/regression.hpp) */
+/* RegressionHead ctor (regression.cpp:69-80): one all-positive bank of
+ * cfg->clauses clauses. Pools for it have num_classes == 1 and hold scaled
+ * integer targets t in [0, T] as labels (scaled_target, regression.cpp:82-89). */
+int tmg_machine_create_regress(const tmg_config* cfg, int32_t feature_count, int32_t device,
+                               tmg_machine** out);
+/* train_epoch_regress_parallel (regression.cpp:163-227): TMG_MODE_ASYNC (all
+ * clauses concurrently) or TMG_MODE_SYNC_MIRROR (the reference's W-worker
+ * schedule and streams; bit-exact for W = 1). feedback_events: 1 entry. */
+int tmg_train_epoch_regress(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers,
+                            int32_t epoch, tmg_epoch_report* report);
+/* train_epoch_regress_sequential (regression.cpp:125-161), bit-exact. */
+int tmg_train_epoch_regress_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch,
+                                       double* seconds, uint64_t* feedback_events);
+/* predict_scaled (regression.cpp:86-93): clause count clipped to [0, T], per
+ * pool example or per reference-layout literal row. */
+int tmg_regress_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out);
+int tmg_regress_predict_literals(tmg_machine* tm, const uint64_t* literals, int64_t q, int32_t* out);
+/* update_regress (regression.cpp:101-123) with a scaled target and the
+ * caller's xoshiro stream (advanced in place). */
+int tmg_update_regress(tmg_machine* tm, const uint64_t* literals, int32_t scaled_target,
+                       uint64_t* rng_state, uint64_t* events);
+
 /* ---- host-side RNG streams (tmgpu_rng.h), exported for FFI users */
 /* Rng(seed, stream) (rng.hpp:39-42) -> 4-word xoshiro256++ state. */
 void tmg_rng_state_init(uint64_t seed, uint64_t stream, uint64_t* state);

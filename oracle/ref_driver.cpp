@@ -20,8 +20,12 @@
 #include <thread>
 #include <vector>
 
+#include <sstream>
+
 #include "npy.hpp"
 #include "tsetlin/feedback.hpp"
+#include "tsetlin/model_io.hpp"
+#include "tsetlin/regression.hpp"
 #include "tsetlin/pool.hpp"
 #include "tsetlin/rng.hpp"
 #include "tsetlin/trainer.hpp"
@@ -431,6 +435,101 @@ void golden_inference(const std::string& dir) {
   }
 }
 
+// Regression head (f2) and tmmodel v1 text (f3).
+void golden_regression(const std::string& dir) {
+  fs::create_directories(dir);
+  const int o = 10, q = 120, qt = 60;
+  Rng r(2468, 1);
+  std::vector<std::uint8_t> bits(static_cast<std::size_t>(q + qt) * o);
+  std::vector<std::int32_t> y(static_cast<std::size_t>(q + qt));
+  for (int i = 0; i < q + qt; ++i) {
+    int ones = 0;
+    for (int f = 0; f < o; ++f) {
+      const auto b = static_cast<std::uint8_t>(r.below(2));
+      bits[static_cast<std::size_t>(i) * o + f] = b;
+      ones += b;
+    }
+    y[static_cast<std::size_t>(i)] = ones;
+  }
+  TMConfig cfg;
+  cfg.clauses = 12;
+  cfg.margin = 10;
+  cfg.specificity = 3.0;
+  cfg.state_depth = 16;
+  cfg.seed = 7;
+  std::vector<std::uint8_t> tx(bits.begin(), bits.begin() + q * o), vx(bits.begin() + q * o, bits.end());
+  std::vector<std::int32_t> ty(y.begin(), y.begin() + q), vy(y.begin() + q, y.end());
+  npyio::save(dir + "/train_x.npy", tx.data(), {static_cast<std::size_t>(q), static_cast<std::size_t>(o)});
+  npyio::save(dir + "/train_y.npy", ty);
+  npyio::save(dir + "/test_x.npy", vx.data(), {static_cast<std::size_t>(qt), static_cast<std::size_t>(o)});
+  npyio::save(dir + "/test_y.npy", vy);
+  std::string manifest = "{\n";
+  for (int mode = 0; mode < 2; ++mode) {  // 0: parallel W=1, 1: sequential
+    RegressionHead head(cfg, o, 0.0, 10.0);
+    std::vector<std::int32_t> scaled;
+    for (auto v : ty) scaled.push_back(scaled_target(head, v));
+    ExamplePool pool(o, tx, scaled, 1);
+    ExamplePool test(o, vx, vy, 1);
+    const std::string tag = mode == 0 ? "par" : "seq";
+    std::string ev;
+    for (int e = 0; e < 3; ++e) {
+      EpochReport rep = mode == 0 ? train_epoch_regress_parallel(head, pool, 1, e)
+                                  : train_epoch_regress_sequential(head, pool, e);
+      ev += (e ? ", " : "") + std::to_string(rep.total_feedback_events());
+      std::vector<std::uint16_t> counters(head.bank.counters().begin(), head.bank.counters().end());
+      npyio::save(dir + "/" + tag + "_epoch" + std::to_string(e) + "_counters.npy", counters.data(),
+                  {static_cast<std::size_t>(cfg.clauses), static_cast<std::size_t>(2 * o)});
+      if (mode == 0) {
+        std::vector<std::int32_t> tallies;
+        for (int i = 0; i < q; ++i) tallies.push_back(pool.tally(i, 0));
+        npyio::save(dir + "/" + tag + "_epoch" + std::to_string(e) + "_tallies.npy", tallies);
+        auto pb = prev_bitmap(head.bank);
+        npyio::save(dir + "/" + tag + "_epoch" + std::to_string(e) + "_prev.npy", pb);
+      }
+    }
+    std::vector<std::int32_t> pred;
+    for (int i = 0; i < qt; ++i) pred.push_back(predict_scaled(head, test.literals(i)));
+    npyio::save(dir + "/" + tag + "_predict_scaled.npy", pred);
+    char line[256];
+    std::snprintf(line, sizeof line, "\"%s_events\": [%s], \"%s_mae\": %.17g,\n", tag.c_str(), ev.c_str(), tag.c_str(),
+                  evaluate_scaled_mae(head, test));
+    manifest += line;
+    if (mode == 1) {
+      // update_regress on one row with an explicit stream
+      Rng ur(99, 4);
+      const auto evu = update_regress(head, test.literals(3), 7.0, ur);
+      std::vector<std::uint16_t> counters(head.bank.counters().begin(), head.bank.counters().end());
+      npyio::save(dir + "/update_regress_counters.npy", counters.data(),
+                  {static_cast<std::size_t>(cfg.clauses), static_cast<std::size_t>(2 * o)});
+      std::snprintf(line, sizeof line, "\"update_regress_events\": %llu, \"update_regress_next\": \"%llu\",\n",
+                    static_cast<unsigned long long>(evu), static_cast<unsigned long long>(ur.next()));
+      manifest += line;
+      std::ostringstream ms;
+      save_model(ms, head);
+      write_text(dir + "/regress_model.txt", ms.str());
+    }
+  }
+  manifest += "\"o\": 10, \"clauses\": 12, \"margin\": 10, \"s\": 3.0, \"N\": 16, \"seed\": 7, \"y_min\": 0.0, \"y_max\": 10.0\n}\n";
+  write_text(dir + "/manifest.json", manifest);
+}
+
+// tmmodel v1 text of the W=1-trained classification machines.
+void golden_models(const std::string& dir) {
+  fs::create_directories(dir);
+  Split d = make_data("xor", 100, 60, 7, 0.1);
+  TMConfig cfg;
+  cfg.clauses = 20;
+  cfg.margin = 15;
+  cfg.specificity = 3.9;
+  cfg.seed = 1;
+  MultiClassTM tm(cfg, d.features, d.classes);
+  ExamplePool pool(d.features, d.train_x, d.train_y, d.classes);
+  for (int e = 0; e < 4; ++e) train_epoch_parallel(tm, pool, 1, e);
+  std::ostringstream ms;
+  save_model(ms, tm);
+  write_text(dir + "/xor12_model.txt", ms.str());
+}
+
 // ----------------------------------------------------------------- train ---
 
 struct Args {
@@ -544,6 +643,8 @@ int main(int argc, char** argv) {
       golden_epochs(dir + "/epoch_par_w1", false);
       golden_epochs(dir + "/epoch_seq", true);
       golden_inference(dir + "/inference");
+      golden_regression(dir + "/regression");
+      golden_models(dir + "/models");
       return 0;
     }
     if (cmd == "train") return cmd_train(parse(argc, argv, 2));

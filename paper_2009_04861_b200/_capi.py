@@ -89,6 +89,12 @@ SIGNATURES = {
     "tmg_class_sums_literals": (C.c_int, [P, P, I64, I32, P]),
     "tmg_predict_literals": (C.c_int, [P, P, I64, P]),
     "tmg_class_sums_device": (C.c_int, [P, P, I32, P]),
+    "tmg_machine_create_regress": (C.c_int, [C.POINTER(Config), I32, I32, PP]),
+    "tmg_train_epoch_regress": (C.c_int, [P, P, I32, I32, I32, C.POINTER(EpochReportC)]),
+    "tmg_train_epoch_regress_sequential": (C.c_int, [P, P, I32, C.POINTER(D), P]),
+    "tmg_regress_predict": (C.c_int, [P, P, P]),
+    "tmg_regress_predict_literals": (C.c_int, [P, P, I64, P]),
+    "tmg_update_regress": (C.c_int, [P, P, I32, P, P]),
     "tmg_rng_state_init": (None, [U64, U64, P]),
     "tmg_rng_state_next": (U64, [P]),
     "tmg_epoch_order": (C.c_int, [U64, I32, I32, P]),

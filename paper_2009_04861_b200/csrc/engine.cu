@@ -73,6 +73,10 @@ template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t count = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
   void alloc(size_t n) {
     release();
     if (n) CK(cudaMalloc(&ptr, n * sizeof(T)));
@@ -137,6 +141,8 @@ struct tmg_machine {
   // current async epoch
   int32_t cur_epoch = -1;
   uint32_t key0 = 0, key1 = 0;
+  int all_positive = 0;  // regression head bank (PolarityScheme::AllPositive)
+  bool regress_mode = false;  // current call trains the regression head
   int clauses() const { return m * n_loc; }
 };
 
@@ -190,7 +196,7 @@ void reset_state(tmg_machine* tm) {  // ClassBank ctor: counters = N (core.cpp:9
   CK(cudaStreamSynchronize(tm->stream));
 }
 
-tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int jb, int je) {
+tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int jb, int je, int all_positive = 0) {
   if (!cfg) fail(TMG_EINVAL, "null config");
   validate_config(*cfg);
   if (m < 1) fail(TMG_EINVAL, "class count must be >= 1");
@@ -216,6 +222,7 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->Wp = wp_for(o);
     tm->NW = tm->Wp / 32;
     tm->device = device;
+    tm->all_positive = all_positive ? 1 : 0;
     CK(cudaStreamCreateWithFlags(&tm->stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&tm->ev0));
     CK(cudaEventCreate(&tm->ev1));
@@ -237,7 +244,9 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
 void upload_order(tmg_machine* tm, tmg_pool* pool, int32_t epoch) {
   // The epoch permutation of train_epoch_parallel (trainer.cpp:196-198).
   tmg_rng r;
-  tmg_rng_seed(&r, tm->cfg.seed, tmg_mix_stream(TMG_STREAM_PERMUTATION, static_cast<uint64_t>(epoch), 0));
+  // regression epochs use their own stream kinds (regression.cpp:29-31)
+  tmg_rng_seed(&r, tm->cfg.seed,
+               tmg_mix_stream(tm->regress_mode ? 5 : TMG_STREAM_PERMUTATION, static_cast<uint64_t>(epoch), 0));
   std::vector<int32_t> order(static_cast<size_t>(pool->q));
   tmg_shuffled_indices(static_cast<int32_t>(pool->q), &r, order.data());
   CK(cudaMemcpyAsync(pool->order.ptr, order.data(), order.size() * 4, cudaMemcpyHostToDevice, tm->stream));
@@ -267,6 +276,8 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   p.order = pool->order.ptr;
   p.margin = tm->cfg.margin;
   p.boost = tm->cfg.boost_true_positive ? 1 : 0;
+  p.all_positive = tm->all_positive;
+  p.regress = tm->regress_mode ? 1 : 0;
   const double s = tm->cfg.specificity;
   p.thr_high = prob_threshold((s - 1.0) / s);
   p.thr_low = prob_threshold(1.0 / s);
@@ -326,6 +337,7 @@ std::vector<int32_t> class_sums_device(tmg_machine* tm, const uint32_t* xplane, 
   e.nplane = nplane;
   e.q = q;
   e.sums = d_out;
+  e.all_positive = tm->all_positive;
   // Enough CTAs for several waves over 148 SMs.
   const int64_t tiles = (q + 127) / 128;
   int chunks = static_cast<int>(std::max<int64_t>(1, (148 * 8 + tiles * tm->m - 1) / (tiles * tm->m)));
@@ -366,23 +378,24 @@ void finish_pool(tmg_pool* pool, const uint8_t* d_bits, const int32_t* d_labels)
   pool->tallies.alloc(rows * pool->m);
   pool->delta.alloc(rows * pool->m);
   pool->order.alloc(rows);
-  tmg::pack_planes_launch(d_bits, pool->xplane.ptr, pool->nplane.ptr, pool->q, pool->o, pool->Wp, pool->stream);
+  // Pack and validate on the device (ExamplePool ctor checks, pool.cpp:40-55).
+  DevBuf<int> err;
+  err.alloc(2);
+  CK(cudaMemsetAsync(err.ptr, 0, 8, pool->stream));
+  tmg::pack_planes_launch(d_bits, pool->xplane.ptr, pool->nplane.ptr, pool->q, pool->o, pool->Wp, err.ptr,
+                          pool->stream);
   CK(cudaGetLastError());
+  if (pool->m > 1) tmg::check_labels_launch(d_labels, pool->q, pool->m, err.ptr, pool->stream);
   CK(cudaMemcpyAsync(pool->labels.ptr, d_labels, rows * 4, cudaMemcpyDeviceToDevice, pool->stream));
   CK(cudaMemsetAsync(pool->tallies.ptr, 0, pool->tallies.bytes(), pool->stream));  // pool.cpp:71
   CK(cudaMemsetAsync(pool->delta.ptr, 0, pool->delta.bytes(), pool->stream));
+  int herr[2] = {0, 0};
+  CK(cudaMemcpyAsync(herr, err.ptr, 8, cudaMemcpyDeviceToHost, pool->stream));
   CK(cudaStreamSynchronize(pool->stream));
-}
-
-void validate_inputs_host(const uint8_t* bits, const int32_t* labels, int64_t q, int o, int m) {
-  // ExamplePool ctor checks (pool.cpp:40-55).
-  const size_t total = static_cast<size_t>(q) * static_cast<size_t>(o);
-  for (size_t k = 0; k < total; ++k)
-    if (bits[k] > 1) fail(TMG_EINVAL, "inputs must be 0/1");
-  if (m > 1)
-    for (int64_t i = 0; i < q; ++i)
-      if (labels[i] < 0 || labels[i] >= m)
-        fail(TMG_EINVAL, "label " + std::to_string(labels[i]) + " outside [0, " + std::to_string(m) + ")");
+  err.release();
+  if (herr[0] & 1) fail(TMG_EINVAL, "inputs must be 0/1");
+  if (herr[0] & 2)
+    fail(TMG_EINVAL, "label " + std::to_string(herr[1]) + " outside [0, " + std::to_string(pool->m) + ")");
 }
 
 tmg_machine* M(tmg_machine* tm) {
@@ -619,7 +632,6 @@ TMG_API int tmg_pool_create(int32_t device, int32_t o, const uint8_t* bits, cons
   return guarded([&] {
     tmg_pool* pool = create_pool_common(device, o, q, m);
     try {
-      validate_inputs_host(bits, labels, q, o, m);
       DeviceGuard dg(device);
       CK(cudaStreamCreateWithFlags(&pool->stream, cudaStreamNonBlocking));
       DevBuf<uint8_t> dbits;
@@ -784,7 +796,36 @@ TMG_API int tmg_train_window(tmg_machine* tm, tmg_pool* pool, int32_t epoch, int
   });
 }
 
+static int train_epoch_impl(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
+                            tmg_epoch_report* report);
+
 TMG_API int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
+                            tmg_epoch_report* report) {
+  if (tm && tm->all_positive) {
+    g_last_error = "regression machine: use tmg_train_epoch_regress";
+    return TMG_EINVAL;
+  }
+  return train_epoch_impl(tm, pool, mode, workers, epoch, report);
+}
+
+TMG_API int tmg_train_epoch_regress(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
+                                    tmg_epoch_report* report) {
+  // train_epoch_regress_parallel (regression.cpp:163-227)
+  if (!tm || !tm->all_positive) {
+    g_last_error = "not a regression machine (create it with tmg_machine_create_regress)";
+    return TMG_EINVAL;
+  }
+  if (pool && pool->m != 1) {
+    g_last_error = "regression pool must have one tally class";
+    return TMG_EINVAL;
+  }
+  tm->regress_mode = true;
+  const int rc = train_epoch_impl(tm, pool, mode, workers, epoch, report);
+  tm->regress_mode = false;
+  return rc;
+}
+
+static int train_epoch_impl(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
                             tmg_epoch_report* report) {
   return guarded([&] {
     check_compatible(M(tm), pool);
@@ -808,7 +849,8 @@ TMG_API int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32
       for (int w = 0; w < workers; ++w) {
         tmg_rng r;
         tmg_rng_seed(&r, tm->cfg.seed,
-                     tmg_mix_stream(TMG_STREAM_WORKER, static_cast<uint64_t>(epoch), static_cast<uint64_t>(w)));
+                     tmg_mix_stream(tm->regress_mode ? 6 : TMG_STREAM_WORKER, static_cast<uint64_t>(epoch),
+                                    static_cast<uint64_t>(w)));
         std::memcpy(&rng[static_cast<size_t>(w) * 4], r.s, 32);
         for (int64_t g = w; g < total; g += workers) {
           tmg::MirrorJob jb{};
@@ -861,17 +903,38 @@ TMG_API int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32
   });
 }
 
+TMG_API int tmg_train_epoch_regress_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, double* seconds,
+                                               uint64_t* feedback_events) {
+  // train_epoch_regress_sequential (regression.cpp:125-161)
+  if (!tm || !tm->all_positive) {
+    g_last_error = "not a regression machine (create it with tmg_machine_create_regress)";
+    return TMG_EINVAL;
+  }
+  tm->regress_mode = true;
+  const int rc = tmg_train_epoch_sequential(tm, pool, epoch, seconds, feedback_events);
+  tm->regress_mode = false;
+  return rc;
+}
+
 TMG_API int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, double* seconds,
                                        uint64_t* feedback_events) {
   return guarded([&] {
-    check_compatible(M(tm), pool);
-    if (tm->m < 2) fail(TMG_EINVAL, "classification needs at least two banks");  // trainer.cpp:141-143
+    if (tm && tm->regress_mode) {
+      if (!pool || tm->o != pool->o) fail(TMG_EINVAL, "head/pool feature count mismatch");
+      if (tm->device != pool->device) fail(TMG_EINVAL, "model and pool live on different devices");
+    } else {
+      check_compatible(M(tm), pool);
+      if (tm->all_positive) fail(TMG_EINVAL, "regression machine: use tmg_train_epoch_regress_sequential");
+      if (tm->m < 2) fail(TMG_EINVAL, "classification needs at least two banks");  // trainer.cpp:141-143
+    }
     if (tm->n_loc != tm->n) fail(TMG_EINVAL, "the sequential trainer needs the full (unsharded) machine");
     DeviceGuard dg(tm->device);
     const auto wall0 = std::chrono::steady_clock::now();
-    // Rng(seed, mix_stream(1, epoch)) shuffles, then keeps feeding the epoch.
+    // Rng(seed, mix_stream(1, epoch)) shuffles, then keeps feeding the epoch
+    // (regression: stream kind 4, regression.cpp:133-135).
     tmg_rng r;
-    tmg_rng_seed(&r, tm->cfg.seed, tmg_mix_stream(TMG_STREAM_SEQUENTIAL, static_cast<uint64_t>(epoch), 0));
+    tmg_rng_seed(&r, tm->cfg.seed,
+                 tmg_mix_stream(tm->regress_mode ? 4 : TMG_STREAM_SEQUENTIAL, static_cast<uint64_t>(epoch), 0));
     std::vector<int32_t> order(static_cast<size_t>(pool->q));
     tmg_shuffled_indices(static_cast<int32_t>(pool->q), &r, order.data());
     CK(cudaMemcpyAsync(pool->order.ptr, order.data(), order.size() * 4, cudaMemcpyHostToDevice, tm->stream));
@@ -1189,6 +1252,93 @@ TMG_API int tmg_predict_literals(tmg_machine* tm, const uint64_t* lits, int64_t 
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, pred, static_cast<size_t>(q) * 4, cudaMemcpyDeviceToHost, tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+// --------------------------------------------------------- regression head ---
+
+TMG_API int tmg_machine_create_regress(const tmg_config* cfg, int32_t o, int32_t device, tmg_machine** out) {
+  // RegressionHead ctor (regression.cpp:69-80): one all-positive bank.
+  return guarded([&] { *out = create_machine(cfg, o, 1, device, 0, cfg ? cfg->clauses : 0, 1); });
+}
+
+namespace {
+void regress_predict_planes(tmg_machine* tm, const uint32_t* xs, const uint32_t* ns, int64_t q, int32_t* out) {
+  if (!tm->all_positive) fail(TMG_EINVAL, "not a regression machine");
+  if (tm->n_loc != tm->n) fail(TMG_EINVAL, "predict on a clause shard: reduce clause counts across shards first");
+  ensure_sums(tm, 2 * q);
+  class_sums_device(tm, xs, ns, q, false, tm->sums.ptr, nullptr);
+  tmg::clamp_launch(tm->sums.ptr, tm->sums.ptr + q, q, tm->cfg.margin, tm->stream);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, tm->sums.ptr + q, static_cast<size_t>(q) * 4, cudaMemcpyDeviceToHost, tm->stream));
+  CK(cudaStreamSynchronize(tm->stream));
+}
+}  // namespace
+
+TMG_API int tmg_regress_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
+  // predict_scaled over a pool (regression.cpp:86-93)
+  return guarded([&] {
+    if (!M(tm) || !pool || tm->o != pool->o) fail(TMG_EINVAL, "head/pool feature count mismatch");
+    DeviceGuard dg(tm->device);
+    regress_predict_planes(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, out);
+  });
+}
+
+TMG_API int tmg_regress_predict_literals(tmg_machine* tm, const uint64_t* lits, int64_t q, int32_t* out) {
+  return guarded([&] {
+    M(tm);
+    if (q <= 0) return;
+    DeviceGuard dg(tm->device);
+    DevBuf<uint32_t> xs, ns;
+    literals_to_planes(tm, lits, q, xs, ns);
+    regress_predict_planes(tm, xs.ptr, ns.ptr, q, out);
+  });
+}
+
+TMG_API int tmg_update_regress(tmg_machine* tm, const uint64_t* literals, int32_t scaled_target,
+                               uint64_t* rng_state, uint64_t* events) {
+  // update_regress (regression.cpp:101-123): one example through the
+  // sequential regression kernel with the caller's stream.
+  return guarded([&] {
+    if (!M(tm)->all_positive) fail(TMG_EINVAL, "not a regression machine");
+    if (tm->n_loc != tm->n) fail(TMG_EINVAL, "needs the full (unsharded) machine");
+    DeviceGuard dg(tm->device);
+    DevBuf<uint32_t> xs, ns;
+    literals_to_planes(tm, literals, 1, xs, ns);
+    DevBuf<int32_t> lab, ord;
+    DevBuf<uint64_t> drng;
+    lab.alloc(1);
+    ord.alloc(1);
+    drng.alloc(4);
+    const int32_t zero = 0;
+    CK(cudaMemcpyAsync(lab.ptr, &scaled_target, 4, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemcpyAsync(ord.ptr, &zero, 4, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemcpyAsync(drng.ptr, rng_state, 32, cudaMemcpyHostToDevice, tm->stream));
+    CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
+    tmg_pool fake;
+    fake.o = tm->o;
+    fake.m = 1;
+    fake.q = 1;
+    tm->regress_mode = true;
+    tmg::TrainParams p = make_params(tm, &fake);
+    tm->regress_mode = false;
+    p.xplane = xs.ptr;
+    p.nplane = ns.ptr;
+    p.labels = lab.ptr;
+    p.order = ord.ptr;
+    tmg::SeqParams sp{};
+    sp.rng = drng.ptr;
+    sp.p_high = (tm->cfg.specificity - 1.0) / tm->cfg.specificity;
+    sp.p_low = 1.0 / tm->cfg.specificity;
+    sp.events = tm->events.ptr;
+    if (!tmg::train_sequential_launch(p, sp, tm->B, tm->stream)) fail(TMG_ERUNTIME, "no sequential kernel for B");
+    CK(cudaGetLastError());
+    unsigned long long ev = 0;
+    CK(cudaMemcpyAsync(&ev, tm->events.ptr, 8, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaMemcpyAsync(rng_state, drng.ptr, 32, cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    tm->entries_dirty = true;
+    if (events) *events = ev;
   });
 }
 

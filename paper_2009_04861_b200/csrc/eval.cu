@@ -21,8 +21,9 @@ namespace tmg {
 
 namespace {
 
-constexpr int kTile = 128;  // examples per CTA in eval_sums
-constexpr int kTS = kTile + 1;  // padded shared-memory row: conflict-free staging and reads
+// Examples per CTA in eval_sums: 128 (one thread each), or 32 for very wide
+// rows (IMDb) so the staged tile fits in shared memory. Rows are padded to
+// TILE+1 words: conflict-free staging and reads.
 
 // One warp per clause: list its nonzero include words and count includes.
 __global__ void build_entries_kernel(const uint32_t* __restrict__ state, int clauses, int B, int Wp,
@@ -55,8 +56,9 @@ __global__ void build_entries_kernel(const uint32_t* __restrict__ state, int cla
   }
 }
 
-template <bool TRAIN>
+template <bool TRAIN, int kTile>
 __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
+  constexpr int kTS = kTile + 1;
   extern __shared__ uint32_t tile[];  // [2][Wx][kTS]
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
       out = viol == 0 ? 1 : 0;
     }
     const int j = P.j_begin + jl;
-    sum += (j & 1) ? -out : out;
+    sum += (!P.all_positive && (j & 1)) ? -out : out;
     if (TRAIN && P.prev != nullptr) {  // refresh_tallies also rewrites previous outputs
       const unsigned bits = __ballot_sync(kFull, live && out);
       if (lane == 0 && i < P.q) P.prev[static_cast<size_t>(lc) * P.Wq + (i >> 5)] = bits;
@@ -153,8 +155,10 @@ __global__ void planes_to_counters_kernel(const uint32_t* __restrict__ state,
 }
 
 // bits: q x o uint8 (0/1) -> x plane (bit f = x_f), n plane (bit f = !x_f).
+// Also validates the input (ExamplePool ctor, pool.cpp:42-46): err |= 1 on a
+// byte other than 0/1.
 __global__ void pack_planes_kernel(const uint8_t* __restrict__ bits, uint32_t* __restrict__ xplane,
-                                   uint32_t* __restrict__ nplane, int64_t q, int o, int Wp) {
+                                   uint32_t* __restrict__ nplane, int64_t q, int o, int Wp, int* err) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t total = q * Wp;
@@ -164,11 +168,23 @@ __global__ void pack_planes_kernel(const uint8_t* __restrict__ bits, uint32_t* _
   const int f = w * 32 + lane;
   const bool valid = f < o;
   const uint8_t b = valid ? bits[i * o + f] : 0;
+  if (b > 1) atomicOr(err, 1);
   const unsigned xs = __ballot_sync(kFull, valid && b);
   const unsigned ns = __ballot_sync(kFull, valid && !b);
   if (lane == 0) {
     xplane[i * Wp + w] = xs;
     nplane[i * Wp + w] = ns;
+  }
+}
+
+// Label range check (pool.cpp:47-55): err[0] |= 2, err[1] = an offending label.
+__global__ void check_labels_kernel(const int32_t* __restrict__ labels, int64_t q, int m, int* err) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  const int32_t y = labels[i];
+  if (y < 0 || y >= m) {
+    atomicOr(err, 2);
+    atomicExch(err + 1, y);
   }
 }
 
@@ -213,6 +229,14 @@ __global__ void argmax_kernel(const int32_t* __restrict__ sums, int32_t* __restr
       best = c;
     }
   pred[i] = best;
+}
+
+// predict_scaled (regression.cpp:86-93): clause count clipped to [0, T].
+__global__ void clamp_kernel(const int32_t* __restrict__ sums, int32_t* __restrict__ out, int64_t q, int T) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= q) return;
+  const int32_t v = sums[i];
+  out[i] = v < 0 ? 0 : (v > T ? T : v);
 }
 
 // After an allreduce of per-rank tally deltas: add the remote part
@@ -263,18 +287,21 @@ void build_entries_launch(const uint32_t* state, int clauses, int B, int Wp, int
 void eval_sums_launch(const EvalParams& p, bool train_mode, cudaStream_t s) {
   if (p.q <= 0 || p.n_loc <= 0) return;
   const int chunks = (p.n_loc + p.chunk - 1) / p.chunk;
-  dim3 grid(blocks_for(p.q, kTile), p.m * chunks);
-  const size_t shm = sizeof(uint32_t) * 2 * p.Wx * kTS;
+  auto go = [&](auto kern, int tile) {
+    dim3 grid(blocks_for(p.q, tile), p.m * chunks);
+    const size_t shm = sizeof(uint32_t) * 2 * p.Wx * (tile + 1);
+    if (shm > 48 * 1024)
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
+    count_launch();
+    kern<<<grid, tile, shm, s>>>(p);
+  };
+  const bool wide = sizeof(uint32_t) * 2 * p.Wx * 129 > 200 * 1024;
   if (train_mode) {
-    if (shm > 48 * 1024)
-      cudaFuncSetAttribute(eval_sums_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
-    count_launch();
-    eval_sums_kernel<true><<<grid, kTile, shm, s>>>(p);
+    if (wide) go(eval_sums_kernel<true, 32>, 32);
+    else go(eval_sums_kernel<true, 128>, 128);
   } else {
-    if (shm > 48 * 1024)
-      cudaFuncSetAttribute(eval_sums_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
-    count_launch();
-    eval_sums_kernel<false><<<grid, kTile, shm, s>>>(p);
+    if (wide) go(eval_sums_kernel<false, 32>, 32);
+    else go(eval_sums_kernel<false, 128>, 128);
   }
 }
 
@@ -296,12 +323,18 @@ void planes_to_counters_launch(const uint32_t* state, uint16_t* counters, int cl
   }
 }
 
+void check_labels_launch(const int32_t* labels, int64_t q, int m, int* err, cudaStream_t s) {
+  if (q <= 0) return;
+  count_launch();
+  check_labels_kernel<<<blocks_for(q, 256), 256, 0, s>>>(labels, q, m, err);
+}
+
 void pack_planes_launch(const uint8_t* bits, uint32_t* xplane, uint32_t* nplane, int64_t q, int o,
-                        int Wp, cudaStream_t s) {
+                        int Wp, int* err, cudaStream_t s) {
   const int64_t threads = q * Wp * 32;
   if (threads > 0) {
     count_launch();
-    pack_planes_kernel<<<blocks_for(threads, 256), 256, 0, s>>>(bits, xplane, nplane, q, o, Wp);
+    pack_planes_kernel<<<blocks_for(threads, 256), 256, 0, s>>>(bits, xplane, nplane, q, o, Wp, err);
   }
 }
 
@@ -318,6 +351,12 @@ void argmax_launch(const int32_t* sums, int32_t* pred, int64_t q, int m, cudaStr
     count_launch();
     argmax_kernel<<<blocks_for(q, 256), 256, 0, s>>>(sums, pred, q, m);
   }
+}
+
+void clamp_launch(const int32_t* sums, int32_t* out, int64_t q, int T, cudaStream_t s) {
+  if (q <= 0) return;
+  count_launch();
+  clamp_kernel<<<blocks_for(q, 256), 256, 0, s>>>(sums, out, q, T);
 }
 
 void eval_one_launch(const uint32_t* state, int lc, int B, int Wp, const uint32_t* x, const uint32_t* n,

@@ -38,6 +38,11 @@ struct TrainParams {
   const int32_t* order;  // [q] epoch permutation, or null = natural order
   int32_t margin;
   int32_t boost;
+  // Regression head (proj/src/regression.cpp): one all-positive bank, labels
+  // are scaled targets t in [0, T], gate |t - v| / 2T with v = clamp(tally, 0,
+  // T), Type I when v < t else Type II (regression.cpp:46-67).
+  int32_t regress;
+  int32_t all_positive;
   uint32_t thr_high, thr_low;  // async: P(u < p) thresholds as 32-bit fixed point
   BernThresholds bern;         // the same, split for the sampler
   uint32_t key0, key1;         // async: Philox key for (seed, epoch)
@@ -67,7 +72,7 @@ struct MirrorParams {
 };
 
 struct SeqParams {  // classic sequential trainer mirror (trainer.cpp:138-179)
-  const uint64_t* rng;  // xoshiro state after the epoch shuffle
+  uint64_t* rng;  // xoshiro state after the epoch shuffle (written back at the end)
   double p_high, p_low;
   unsigned long long* events;  // [m]
 };
@@ -83,6 +88,7 @@ struct EvalParams {
   const int32_t* inc_count;  // [m*n_loc]
   uint32_t* prev;            // refresh mode: [m*n_loc][Wq]
   int32_t n_loc, j_begin, m, Wx, Wp, Wq, chunk;
+  int32_t all_positive;  // regression head: every clause votes +1
   const uint32_t* xplane;
   const uint32_t* nplane;
   int64_t q;
@@ -103,11 +109,13 @@ void counters_to_planes_launch(const uint16_t* counters, uint32_t* state, int cl
 void planes_to_counters_launch(const uint32_t* state, uint16_t* counters, int clauses, int o, int B,
                                int Wp, int N, cudaStream_t s);
 void pack_planes_launch(const uint8_t* bits, uint32_t* xplane, uint32_t* nplane, int64_t q, int o,
-                        int Wp, cudaStream_t s);
+                        int Wp, int* err, cudaStream_t s);
+void check_labels_launch(const int32_t* labels, int64_t q, int m, int* err, cudaStream_t s);
 void unpack_ref_literals_launch(const uint64_t* lits, uint32_t* xplane, uint32_t* nplane, int64_t q,
                                 int o, int Wp, cudaStream_t s);
 void argmax_launch(const int32_t* sums, int32_t* pred, int64_t q, int m, cudaStream_t s);
 void init_state_launch(uint32_t* state, int clauses, int B, int Wp, cudaStream_t s);
+void clamp_launch(const int32_t* sums, int32_t* out, int64_t q, int T, cudaStream_t s);
 void apply_remote_delta_launch(int32_t* tallies, const int32_t* reduced, int32_t* own, int64_t count,
                                cudaStream_t s);
 // Integer-pipe peak micro-benchmark: returns thread-ops/s for LOP3-only and LOP3+IMAD streams.

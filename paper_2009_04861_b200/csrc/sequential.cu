@@ -71,7 +71,9 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
     __shared__ int neg_s;
     if (tid == 0) {
       int neg;
-      if (P.m == 2) {
+      if (P.regress) {
+        neg = 0;  // regression: one feed of the single bank per example
+      } else if (P.m == 2) {
         neg = 1 - y;
       } else {
         neg = static_cast<int>(below_dev(rng, static_cast<uint32_t>(P.m - 1)));
@@ -83,8 +85,8 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
     const int neg = neg_s;
     const uint32_t* xr = P.xplane + i * Wp;
     const uint32_t* nr = P.nplane + i * Wp;
-    for (int feed = 0; feed < 2; ++feed) {
-      const int c = feed == 0 ? y : neg;
+    for (int feed = 0; feed < (P.regress ? 1 : 2); ++feed) {
+      const int c = P.regress ? 0 : (feed == 0 ? y : neg);
       const int target = feed == 0 ? 1 : 0;
       // ---- vote pass: every clause of bank c, Train mode (trainer.cpp:62-68)
       if (tid == 0) vote = 0;
@@ -102,16 +104,25 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
         const int out = ab == 0 ? 1 : (vb == 0 ? 1 : 0);
         if (lane == 0 && out) {
           atomicOr(&outs[j >> 5], 1u << (j & 31));
-          atomicAdd(&vote, (j & 1) ? -1 : 1);
+          atomicAdd(&vote, (!P.all_positive && (j & 1)) ? -1 : 1);
         }
       }
       __syncthreads();
       // ---- serial gate + feedback replay by warp 0 (trainer.cpp:69-83)
       if (warp == 0) {
         const int v0 = vote;
-        const int vc = v0 < -T ? -T : (v0 > T ? T : v0);
-        const int e = target ? T - vc : T + vc;
-        const double p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+        double p;
+        bool regress_type1 = false;
+        if (P.regress) {  // regression.cpp:46-48, 145-151 (t = scaled target)
+          const int vc = v0 < 0 ? 0 : (v0 > T ? T : v0);
+          const int e = y > vc ? y - vc : vc - y;
+          p = fmin(1.0, static_cast<double>(e) / (2.0 * static_cast<double>(T)));
+          regress_type1 = vc < y;
+        } else {
+          const int vc = v0 < -T ? -T : (v0 > T ? T : v0);
+          const int e = target ? T - vc : T + vc;
+          p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+        }
         for (int j = 0; j < n; ++j) {
           int gated = 0;
           if (lane == 0) gated = rng.uniform() < p ? 1 : 0;
@@ -120,8 +131,9 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
           ++ev_local;
           const int out = (outs[j >> 5] >> (j & 31)) & 1;
           uint32_t* base = P.state + (static_cast<size_t>(c) * n + j) * cstride;
-          const bool positive = (j & 1) == 0;
-          if ((target == 1) != positive) {  // Type II (feedback.cpp:72-83)
+          const bool positive = P.all_positive || (j & 1) == 0;
+          const bool type2 = P.regress ? !regress_type1 : (target == 1) != positive;
+          if (type2) {  // Type II (feedback.cpp:72-83)
             if (out) {
               for (int w = lane; w < Wp; w += 32) {
                 const uint32_t vm = valid_bits(w, P.o);
@@ -184,6 +196,12 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
     }
   }
   (void)ev_local;
+  if (tid == 0) {
+    S.rng[0] = rng.s0;
+    S.rng[1] = rng.s1;
+    S.rng[2] = rng.s2;
+    S.rng[3] = rng.s3;
+  }
 }
 
 }  // namespace

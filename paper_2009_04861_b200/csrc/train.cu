@@ -176,7 +176,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
-  const bool positive = (j & 1) == 0;
+  const bool positive = P.all_positive || (j & 1) == 0;
   const int64_t q = P.q;
   const int T = P.margin;
 
@@ -194,16 +194,25 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
     // of the reference: other workers' tally adds in this window land later).
     const int64_t t = t0 + lane;
     int64_t i = 0;
-    int target = 0;
+    int target = 0;  // 1: the step would take Type I feedback, 0: Type II
     bool gated = false;
     if (t < P.t_end) {
       int64_t pos = offset + t;
       if (pos >= q) pos -= q;
       i = P.order ? __ldg(P.order + pos) : pos;
-      target = __ldg(P.labels + i) == c ? 1 : 0;
+      const int label = __ldg(P.labels + i);
       int v = __ldcg(P.tallies + i * P.m + c);  // relaxed, L2-coherent read
-      v = v < -T ? -T : (v > T ? T : v);
-      const int64_t e = target ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
+      int64_t e;
+      if (P.regress) {  // regression.cpp:46-67, 204-206
+        v = v < 0 ? 0 : (v > T ? T : v);
+        e = label > v ? static_cast<int64_t>(label) - v : static_cast<int64_t>(v) - label;
+        target = v < label ? 1 : 0;
+      } else {  // trainer.cpp:118-126
+        const int y = label == c ? 1 : 0;
+        v = v < -T ? -T : (v > T ? T : v);
+        e = y ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
+        target = (y == 1) == positive ? 1 : 0;
+      }
       const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
       // u < e / 2T  <=>  r * 2T < e * 2^32  (exact integer gate, feedback.cpp:24-28)
       gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
@@ -244,7 +253,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       }
       const int before = cl.eval_train(x, n);
       int after = before;
-      if ((tg == 1) != positive) {
+      if (tg == 0) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
       } else {
         ++events_type1;
@@ -305,7 +314,7 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
     const MirrorJob job = M.jobs[jb];
     const int c = job.c;
     const int lc = c * P.n_loc + (job.j - P.j_begin);
-    const bool positive = (job.j & 1) == 0;
+    const bool positive = P.all_positive || (job.j & 1) == 0;
     Xoshiro rng;
     uint64_t* rs = M.rng + 4 * job.worker;
     rng.s0 = rs[0];
@@ -321,15 +330,25 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
     const bool forced = job.forced != 0;
     for (int64_t t = 0; t < job.batch; ++t) {
       int64_t i = 0;
-      int target = 0, gated = 1;
+      int target = 0, gated = 1;  // target: 1 = Type I step, 0 = Type II
       if (lane == 0 && !forced) {
         const int64_t pos = (job.offset + t) % q;
         i = P.order ? P.order[pos] : pos;
         const int v0 = P.tallies[i * P.m + c];
-        target = P.labels[i] == c ? 1 : 0;
-        const int v = v0 < -T ? -T : (v0 > T ? T : v0);
-        const int e = target ? T - v : T + v;
-        const double p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+        const int label = P.labels[i];
+        double p;
+        if (P.regress) {  // gate_probability, regression.cpp:46-48
+          const int v = v0 < 0 ? 0 : (v0 > T ? T : v0);
+          const int e = label > v ? label - v : v - label;
+          p = fmin(1.0, static_cast<double>(e) / (2.0 * static_cast<double>(T)));
+          target = v < label ? 1 : 0;
+        } else {  // clause_update_probability, feedback.cpp:24-28
+          const int y = label == c ? 1 : 0;
+          const int v = v0 < -T ? -T : (v0 > T ? T : v0);
+          const int e = y ? T - v : T + v;
+          p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+          target = (y == 1) == positive ? 1 : 0;
+        }
         gated = rng.uniform() < p ? 1 : 0;  // skip iff u >= p (trainer.cpp:121)
       }
       gated = __shfl_sync(kFull, gated, 0);
@@ -343,7 +362,7 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
         x[p] = P.xplane[i * P.Wp + p * 32 + lane];
         n[p] = P.nplane[i * P.Wp + p * 32 + lane];
       }
-      const bool type2 = forced ? job.forced == 2 : (target == 1) != positive;
+      const bool type2 = forced ? job.forced == 2 : target == 0;
       const int evald = cl.eval_train(x, n);
       const int before = (forced && job.out_override >= 0) ? job.out_override : evald;
       int after = evald;

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
-  const bool positive = (j & 1) == 0;
+  const bool positive = P.all_positive || (j & 1) == 0;
   const int64_t q = P.q;
   const int T = P.margin;
   const int Wp = P.Wp;
@@ -87,10 +87,19 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
       int64_t pos = offset + t;
       if (pos >= q) pos -= q;
       i = P.order ? __ldg(P.order + pos) : pos;
-      target = __ldg(P.labels + i) == c ? 1 : 0;
+      const int label = __ldg(P.labels + i);
       int v = __ldcg(P.tallies + i * P.m + c);
-      v = v < -T ? -T : (v > T ? T : v);
-      const int64_t e = target ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
+      int64_t e;
+      if (P.regress) {  // regression.cpp:46-67
+        v = v < 0 ? 0 : (v > T ? T : v);
+        e = label > v ? static_cast<int64_t>(label) - v : static_cast<int64_t>(v) - label;
+        target = v < label ? 1 : 0;
+      } else {
+        const int y = label == c ? 1 : 0;
+        v = v < -T ? -T : (v > T ? T : v);
+        e = y ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
+        target = (y == 1) == positive ? 1 : 0;
+      }
       const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
       gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
     }
@@ -110,7 +119,7 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
       const uint32_t pword = lane == 0 ? prev_row[is >> 5] : 0u;
       const int before = eval_train_smem<NW, B>(S, x, n, lane);
       int after = before;
-      if ((tg == 1) != positive) {  // Type II (feedback.cpp:72-83)
+      if (tg == 0) {  // Type II (feedback.cpp:72-83)
         if (before) {
           uint32_t moved = 0;
 #pragma unroll

@@ -478,3 +478,111 @@ def int_peak(device: int = 0):
     a, b = C.c_double(0), C.c_double(0)
     check(lib().tmg_bench_int_peak(device, C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+# ------------------------------------------------------------ regression ---
+class RegressionHead:
+    """RegressionHead (regression.hpp:26-35): one all-positive bank whose
+    clipped clause count decodes linearly into [y_min, y_max]."""
+
+    def __init__(self, cfg: TMConfig, feature_count: int, y_min: float, y_max: float, device: int = 0):
+        cfg.validate()
+        if not (y_max > y_min):
+            raise ValueError("target range must satisfy y_max > y_min")
+        self.config, self.y_min, self.y_max, self.device = cfg, float(y_min), float(y_max), device
+        c = cfg._c()
+        self._h = C.c_void_p()
+        check(lib().tmg_machine_create_regress(C.byref(c), feature_count, device, C.byref(self._h)))
+        self._o = feature_count
+        self.clause_begin, self.clause_end = 0, cfg.clauses
+        self.bank = ClassBank(self, 0)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().tmg_machine_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def feature_count(self) -> int:
+        return self._o
+
+    def num_banks(self) -> int:
+        return 1
+
+    def info(self) -> _capi.MachineInfo:
+        inf = _capi.MachineInfo()
+        check(lib().tmg_machine_info_get(self._h, C.byref(inf)))
+        return inf
+
+
+def scaled_target(head: RegressionHead, y: float) -> int:
+    """regression.cpp:82-89 (round half away from zero, like std::lround)."""
+    if y < head.y_min or y > head.y_max:
+        raise ValueError("target outside [y_min, y_max]")
+    v = (y - head.y_min) * head.config.margin / (head.y_max - head.y_min)
+    return int(np.floor(v + 0.5)) if v >= 0 else -int(np.floor(-v + 0.5))
+
+
+def regress_pool(head: RegressionHead, bits, targets, device: int = 0) -> ExamplePool:
+    """ExamplePool of scaled targets (one tally class) for a regression head."""
+    scaled = np.array([scaled_target(head, float(y)) for y in np.asarray(targets).reshape(-1)], np.int32)
+    return ExamplePool(head.feature_count(), bits, scaled, 1, device=device)
+
+
+def predict_scaled_all(head: RegressionHead, pool: ExamplePool) -> np.ndarray:
+    """predict_scaled (regression.cpp:86-93) for every pool example."""
+    out = np.zeros(pool.size(), np.int32)
+    check(lib().tmg_regress_predict(head.handle, pool.handle, _ptr(out)))
+    return out
+
+
+def predict_scaled(head: RegressionHead, literals) -> int:
+    lits = _lits2d(head, literals)[:1].copy()
+    out = np.zeros(1, np.int32)
+    check(lib().tmg_regress_predict_literals(head.handle, _ptr(lits), 1, _ptr(out)))
+    return int(out[0])
+
+
+def predict_regress(head: RegressionHead, literals) -> float:
+    """regression.cpp:95-99."""
+    v = predict_scaled(head, literals)
+    return head.y_min + v * (head.y_max - head.y_min) / head.config.margin
+
+
+def update_regress(head: RegressionHead, literals, y_target: float, rng: Rng) -> int:
+    """update_regress (regression.cpp:101-123) with the reference stream."""
+    t = scaled_target(head, y_target)
+    lits = _lits2d(head, literals)[:1].copy()
+    ev = C.c_uint64(0)
+    check(lib().tmg_update_regress(head.handle, _ptr(lits), t, _ptr(rng.state), C.byref(ev)))
+    return int(ev.value)
+
+
+def train_epoch_regress_sequential(head: RegressionHead, pool: ExamplePool, epoch: int) -> EpochReport:
+    ev = np.zeros(1, np.uint64)
+    secs = C.c_double(0)
+    check(lib().tmg_train_epoch_regress_sequential(head.handle, pool.handle, epoch, C.byref(secs), _ptr(ev)))
+    return EpochReport(epoch, secs.value, secs.value, [int(ev[0])])
+
+
+def train_epoch_regress_parallel(head: RegressionHead, pool: ExamplePool, workers: int, epoch: int,
+                                 mode: int = MODE_ASYNC) -> EpochReport:
+    ev = np.zeros(1, np.uint64)
+    ev1 = np.zeros(1, np.uint64)
+    rep = _capi.EpochReportC(0, 0.0, 0.0, ev.ctypes.data_as(C.POINTER(C.c_uint64)),
+                             ev1.ctypes.data_as(C.POINTER(C.c_uint64)))
+    check(lib().tmg_train_epoch_regress(head.handle, pool.handle, mode, workers, epoch, C.byref(rep)))
+    r = EpochReport(rep.epoch, rep.seconds, rep.device_seconds, [int(ev[0])])
+    r.type_i_events = [int(ev1[0])]
+    return r
+
+
+def evaluate_scaled_mae(head: RegressionHead, pool: ExamplePool, targets=None) -> float:
+    """regression.cpp:229-236 (pool labels are the scaled targets)."""
+    pred = predict_scaled_all(head, pool)
+    t = pool._labels if targets is None else np.asarray(targets, np.int32)
+    return float(np.mean(np.abs(pred.astype(np.int64) - t)))

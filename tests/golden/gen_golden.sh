@@ -6,7 +6,7 @@ set -euo pipefail
 here="$(cd "$(dirname "$0")" && pwd)"
 repo="$(cd "$here/../.." && pwd)"
 make -C "$repo/oracle" ref
-for d in rng pack gate feedback update_clause epoch_par_w1 epoch_seq inference; do
+for d in rng pack gate feedback update_clause epoch_par_w1 epoch_seq inference regression models; do
   rm -rf "$here/$d"
 done
 "$repo/oracle/_ref/ref_driver" golden "$here"

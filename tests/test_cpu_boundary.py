@@ -73,6 +73,25 @@ def test_synth_matches_reference_driver_data():
     assert 0.15 < m.train_x.mean() < 0.45
 
 
+def test_model_file_parser_matches_reference_text():
+    """tmmodel v1 written by the reference parses to its counters (f3)."""
+    from paper_2009_04861_b200 import model_io
+    from tests.golden_io import GOLDEN, load
+    text = open(os.path.join(GOLDEN, "models", "xor12_model.txt")).read()
+    p = model_io.parse(text)
+    assert p["task"] == "classify" and p["features"] == 12 and p["classes"] == 2
+    assert p["config"].specificity == 3.9 and p["config"].clauses == 20
+    want = load("epoch_par_w1", "xor12", "epoch3_counters.npy")
+    for c in range(2):
+        assert np.array_equal(p["banks"][c], want[c])
+    r = model_io.parse(open(os.path.join(GOLDEN, "regression", "regress_model.txt")).read())
+    assert r["task"] == "regress" and r["range"] == (0.0, 10.0)
+    with pytest.raises(RuntimeError, match="not a tmmodel"):
+        model_io.parse("hello v1")
+    with pytest.raises(RuntimeError, match="end marker"):
+        model_io.parse(text.replace("end\n", "fin\n"))
+
+
 def test_shard_ranges_even_aligned_and_cover():
     from paper_2009_04861_b200.distributed import shard_range, window_bounds
     for n in [2, 20, 2000, 2002, 7000]:
