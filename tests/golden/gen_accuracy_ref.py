@@ -19,12 +19,15 @@ CASES = {
                         noise=0.1, data_seed=7),
     "xor_noise40": dict(data="xor", q=5000, qtest=5000, clauses=20, T=15, s=3.9, epochs=50,
                         noise=0.4, data_seed=7),
+    "xor_noise40_w1": dict(data="xor", q=5000, qtest=5000, clauses=20, T=15, s=3.9, epochs=50,
+                           noise=0.4, data_seed=7, workers=1),
     "mnist_q6000": dict(data="mnist", q=6000, qtest=2000, clauses=2000, T=50, s=10.0, epochs=3,
                         noise=0.0, data_seed=2009),
 }
 
 
 def run(case, seed, workers):
+    workers = case.get("workers", workers)
     args = [DRIVER, "train", "--data", case["data"], "--q", str(case["q"]), "--qtest", str(case["qtest"]),
             "--clauses", str(case["clauses"]), "--T", str(case["T"]), "--s", str(case["s"]),
             "--epochs", str(case["epochs"]), "--noise", str(case["noise"]), "--seed", str(seed),
@@ -46,7 +49,7 @@ def main():
             per_seed[str(seed)] = [r["test_accuracy"] for r in rows]
             print(name, seed, per_seed[str(seed)][-1], flush=True)
         final = [v[-1] for v in per_seed.values()]
-        res[name] = dict(config=case, workers=workers, per_seed=per_seed,
+        res[name] = dict(config=case, workers=case.get("workers", workers), per_seed=per_seed,
                          mean_final=sum(final) / len(final))
         json.dump(res, open(path, "w"), indent=1)
 
