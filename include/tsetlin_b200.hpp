@@ -257,4 +257,25 @@ std::vector<std::int32_t> export_vote_sums(const MultiClassTM& tm, std::span<con
 std::vector<std::int32_t> predict_all(const MultiClassTM& tm, const ExamplePool& pool);
 double evaluate_accuracy(const MultiClassTM& tm, const ExamplePool& pool);
 
+// ============================================================ regression ==
+// regression.hpp: one all-positive bank; the clipped clause count decodes
+// linearly into [y_min, y_max].
+struct RegressionHead {
+  TMConfig config;
+  double y_min;
+  double y_max;
+  ClassBank bank;
+
+  RegressionHead(TMConfig cfg, int feature_count, double y_min, double y_max);
+};
+
+int scaled_target(const RegressionHead& head, double y);
+int predict_scaled(const RegressionHead& head, std::span<const std::uint64_t> literals);
+double predict_regress(const RegressionHead& head, std::span<const std::uint64_t> literals);
+std::uint64_t update_regress(RegressionHead& head, std::span<const std::uint64_t> literals, double y_target,
+                             Rng& rng);
+EpochReport train_epoch_regress_sequential(RegressionHead& head, const ExamplePool& pool, int epoch);
+EpochReport train_epoch_regress_parallel(RegressionHead& head, ExamplePool& pool, int workers, int epoch);
+double evaluate_scaled_mae(const RegressionHead& head, const ExamplePool& pool);
+
 }  // namespace tsetlin

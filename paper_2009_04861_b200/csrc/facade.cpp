@@ -1,6 +1,7 @@
 // facade.cpp — the reference's C++ API (namespace tsetlin) implemented over
 // the B200 C ABI (tmgpu.h). Host mirrors are synchronised lazily; all
 // learning and evaluation calls go to libtmgpu.so.
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -92,17 +93,25 @@ void download(const ClassBank& b, Link& l) {
   l.host_stale = false;
 }
 
+void make_device_cfg(const ClassBank& b, Link& l, const TMConfig& cfg);
+
 void make_device(const ClassBank& b, Link& l) {
   if (l.dev) return;
-  if (b.scheme() != PolarityScheme::Alternating)
-    throw std::invalid_argument("AllPositive banks (regression head) are not supported on the GPU");
   TMConfig cfg;
   cfg.clauses = b.clause_count();
   cfg.state_depth = b.state_depth();
+  make_device_cfg(b, l, cfg);
+}
+
+void make_device_cfg(const ClassBank& b, Link& l, const TMConfig& cfg) {
+  if (l.dev) return;
   const tmg_config cc = to_c(cfg);
   auto dm = std::make_shared<detail::DeviceMachine>();
   dm->device = default_device();
-  check(tmg_machine_create(&cc, b.feature_count(), 1, dm->device, &dm->h));
+  if (b.scheme() == PolarityScheme::AllPositive)  // the regression head's bank
+    check(tmg_machine_create_regress(&cc, b.feature_count(), dm->device, &dm->h));
+  else
+    check(tmg_machine_create(&cc, b.feature_count(), 1, dm->device, &dm->h));
   dm->links.push_back(&l);
   l.dev = dm;
   l.bank = 0;
@@ -593,6 +602,97 @@ double evaluate_accuracy(const MultiClassTM& tm, const ExamplePool& pool) {
   for (int i = 0; i < pool.size(); ++i)
     if (pred[static_cast<std::size_t>(i)] == pool.label(i)) ++correct;
   return static_cast<double>(correct) / static_cast<double>(pool.size());
+}
+
+// ============================================================ regression ==
+
+RegressionHead::RegressionHead(TMConfig cfg, int feature_count, double lo, double hi)
+    : config(cfg), y_min(lo), y_max(hi),
+      bank(feature_count, cfg.clauses, cfg.state_depth, PolarityScheme::AllPositive) {
+  config.validate();  // regression.cpp:69-80
+  if (!(y_max > y_min)) throw std::invalid_argument("target range must satisfy y_max > y_min");
+  make_device_cfg(bank, *bank.link_, config);
+}
+
+namespace {
+// The head's device machine carries its configuration (T, s, seed, boost).
+detail::DeviceMachine& head_device(const RegressionHead& head) {
+  make_device_cfg(head.bank, *head.bank.link_, head.config);
+  push_machine(*head.bank.link_->dev, {});
+  return *head.bank.link_->dev;
+}
+}  // namespace
+
+int scaled_target(const RegressionHead& head, double y) {  // regression.cpp:82-89
+  if (y < head.y_min || y > head.y_max) throw std::invalid_argument("target outside [y_min, y_max]");
+  const double span = head.y_max - head.y_min;
+  return static_cast<int>(std::lround((y - head.y_min) * head.config.margin / span));
+}
+
+int predict_scaled(const RegressionHead& head, std::span<const std::uint64_t> literals) {
+  auto& dm = head_device(head);
+  std::int32_t out = 0;
+  check(tmg_regress_predict_literals(dm.h, literals.data(), 1, &out));
+  return out;
+}
+
+double predict_regress(const RegressionHead& head, std::span<const std::uint64_t> literals) {
+  const int v = predict_scaled(head, literals);
+  return head.y_min + v * (head.y_max - head.y_min) / head.config.margin;
+}
+
+std::uint64_t update_regress(RegressionHead& head, std::span<const std::uint64_t> literals, double y_target,
+                             Rng& rng) {
+  const int t = scaled_target(head, y_target);
+  auto& dm = head_device(head);
+  std::uint64_t events = 0;
+  check(tmg_update_regress(dm.h, literals.data(), t, rng.raw_state(), &events));
+  mark_stale(dm);
+  return events;
+}
+
+EpochReport train_epoch_regress_sequential(RegressionHead& head, const ExamplePool& pool, int epoch) {
+  if (pool.feature_count() != head.bank.feature_count())
+    throw std::invalid_argument("head/pool feature count mismatch");
+  auto& dm = head_device(head);
+  EpochReport rep;
+  rep.epoch = epoch;
+  rep.feedback_events.assign(1, 0);
+  double seconds = 0.0;
+  check(tmg_train_epoch_regress_sequential(dm.h, pool.device()->h, epoch, &seconds, rep.feedback_events.data()));
+  rep.seconds = seconds > 0 ? seconds : 1e-9;
+  mark_stale(dm);
+  return rep;
+}
+
+EpochReport train_epoch_regress_parallel(RegressionHead& head, ExamplePool& pool, int workers, int epoch) {
+  if (pool.feature_count() != head.bank.feature_count())
+    throw std::invalid_argument("head/pool feature count mismatch");
+  if (pool.num_classes() != 1) throw std::invalid_argument("regression pool must have one tally class");
+  if (workers < 1) throw std::invalid_argument("workers must be >= 1");
+  auto& dm = head_device(head);
+  push_pool(pool);
+  EpochReport rep;
+  rep.epoch = epoch;
+  rep.feedback_events.assign(1, 0);
+  tmg_epoch_report r{};
+  r.feedback_events = rep.feedback_events.data();
+  check(tmg_train_epoch_regress(dm.h, pool.device()->h, workers == 1 ? TMG_MODE_SYNC_MIRROR : TMG_MODE_ASYNC,
+                                workers, epoch, &r));
+  rep.seconds = r.seconds;
+  sync_bound_after(dm);
+  mark_stale(dm);
+  pool_changed(pool);
+  return rep;
+}
+
+double evaluate_scaled_mae(const RegressionHead& head, const ExamplePool& pool) {  // regression.cpp:229-236
+  auto& dm = head_device(head);
+  std::vector<std::int32_t> pred(static_cast<std::size_t>(pool.size()));
+  check(tmg_regress_predict(dm.h, pool.device()->h, pred.data()));
+  double total = 0.0;
+  for (int i = 0; i < pool.size(); ++i) total += std::abs(static_cast<double>(pred[static_cast<std::size_t>(i)] - pool.label(i)));
+  return total / static_cast<double>(pool.size());
 }
 
 }  // namespace tsetlin

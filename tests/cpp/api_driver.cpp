@@ -10,12 +10,16 @@
 #include <cstdio>
 #include <exception>
 #include <span>
+#include <sstream>
 #include <stdexcept>
 #include <string>
+#include <variant>
 #include <vector>
 
 #include "tsetlin/feedback.hpp"
+#include "tsetlin/model_io.hpp"
 #include "tsetlin/pool.hpp"
+#include "tsetlin/regression.hpp"
 #include "tsetlin/rng.hpp"
 #include "tsetlin/trainer.hpp"
 
@@ -254,6 +258,61 @@ int main() {
     auto r1 = train_epoch_parallel(tm2, p2, 1, 2);
     line("seq.par_after", r1.total_feedback_events());
     line("seq.par_bank3", hash_bank(tm2.banks[3]));
+    // ---- model files (tmmodel v1): identical text, and a load round trip
+    std::ostringstream ms;
+    save_model(ms, tm2);
+    std::uint64_t ht = 1469598103934665603ULL;
+    for (char ch : ms.str()) ht = fnv(ht, static_cast<unsigned char>(ch));
+    line("model.text", ht);
+    std::istringstream is(ms.str());
+    AnyModel back = load_model(is);
+    line("model.load_bank2", hash_bank(std::get<MultiClassTM>(back).banks[2]) == hash_bank(tm2.banks[2]) ? 1 : 0);
+    std::istringstream junk("tmmodel v2");
+    expect_throw("model.bad", [&] { load_model(junk); });
+  }
+  // ---- regression head: sequential, one-worker parallel, update, predict
+  {
+    Rng r(1357, 2);
+    const int o = 10, q = 80;
+    std::vector<std::uint8_t> bits;
+    std::vector<std::int32_t> ys;
+    for (int i = 0; i < q; ++i) {
+      int ones = 0;
+      for (int f = 0; f < o; ++f) {
+        bits.push_back(static_cast<std::uint8_t>(r.below(2)));
+        ones += bits.back();
+      }
+      ys.push_back(ones);
+    }
+    TMConfig rc;
+    rc.clauses = 8;
+    rc.margin = 10;
+    rc.specificity = 2.5;
+    rc.state_depth = 32;
+    rc.seed = 3;
+    RegressionHead head(rc, o, 0.0, 10.0);
+    std::vector<std::int32_t> scaled;
+    for (auto y : ys) scaled.push_back(scaled_target(head, y));
+    ExamplePool rp(o, bits, scaled, 1);
+    for (int e = 0; e < 2; ++e) line("regress.seq.e" + std::to_string(e), train_epoch_regress_sequential(head, rp, e).total_feedback_events());
+    line("regress.seq.bank", hash_bank(head.bank));
+    RegressionHead head2 = head;  // value copy: continues independently
+    for (int e = 0; e < 2; ++e) line("regress.par.e" + std::to_string(e), train_epoch_regress_parallel(head2, rp, 1, e).total_feedback_events());
+    line("regress.par.bank", hash_bank(head2.bank));
+    line("regress.par.tallies", hash_tallies(rp));
+    line("regress.mae_x1e6", static_cast<std::uint64_t>(evaluate_scaled_mae(head2, rp) * 1e6 + 0.5));
+    line("regress.predict_scaled", static_cast<std::uint64_t>(predict_scaled(head2, rp.literals(5))));
+    line("regress.predict_x1e6", static_cast<std::uint64_t>(predict_regress(head2, rp.literals(6)) * 1e6 + 0.5));
+    Rng ur(8, 8);
+    line("regress.update", update_regress(head, rp.literals(9), 4.0, ur));
+    line("regress.update_next", ur.next());
+    line("regress.update_bank", hash_bank(head.bank));
+    expect_throw("regress.range", [&] { scaled_target(head, 11.0); });
+    std::ostringstream ms;
+    save_model(ms, head);
+    std::uint64_t ht = 1469598103934665603ULL;
+    for (char ch : ms.str()) ht = fnv(ht, static_cast<unsigned char>(ch));
+    line("regress.model_text", ht);
   }
   return 0;
 }
