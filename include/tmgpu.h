@@ -259,11 +259,16 @@ int tmg_synth_mnist(uint64_t seed, int features, int classes, double r_class, do
                     double flip, int64_t train_rows, int64_t test_rows, uint8_t* train_bits,
                     int32_t* train_labels, uint8_t* test_bits, int32_t* test_labels);
 int tmg_synth_fmnist(uint64_t seed, int pixels, int classes, double r_class, double r_sub, int amp,
-                     int64_t train_rows, int64_t test_rows, uint8_t* train_bits,
+                     double mix, int64_t train_rows, int64_t test_rows, uint8_t* train_bits,
                      int32_t* train_labels, uint8_t* test_bits, int32_t* test_labels);
 int tmg_synth_imdb(uint64_t seed, int vocab, int sentiment, double p_sent, double cross,
                    int64_t train_rows, int64_t test_rows, uint8_t* train_bits,
                    int32_t* train_labels, uint8_t* test_bits, int32_t* test_labels);
+/* The canonical BASELINE.json datasets: kind 0 XOR12, 1 MNIST-, 2 FMNIST-,
+ * 3 IMDb-shaped (features 12, 784, 2352, 10000). */
+int tmg_synth_preset(int kind, uint64_t seed, double noise, int64_t train_rows, int64_t test_rows,
+                     uint8_t* train_bits, int32_t* train_labels, uint8_t* test_bits,
+                     int32_t* test_labels);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,16 @@ def lib():
         L.orc_class_sums.argtypes = [C.POINTER(_Machine), P, C.c_int64, P]
         L.orc_predict.argtypes = [C.POINTER(_Machine), P, C.c_int64, P]
         L.orc_refresh_tallies.argtypes = [C.POINTER(_Machine), C.POINTER(_Pool)]
+        L.orc_update_regress.argtypes = [C.POINTER(_Machine), P, C.c_int32, C.c_int32, C.c_double, C.c_int,
+                                         C.POINTER(_Rng)]
+        L.orc_update_regress.restype = C.c_uint64
+        L.orc_train_epoch_regress_sequential.argtypes = [C.POINTER(_Machine), C.POINTER(_Pool), C.c_int32,
+                                                         C.c_double, C.c_int, C.c_uint64, C.c_int32]
+        L.orc_train_epoch_regress_sequential.restype = C.c_uint64
+        L.orc_train_epoch_regress_parallel.argtypes = [C.POINTER(_Machine), C.POINTER(_Pool), C.c_int32,
+                                                       C.c_double, C.c_int, C.c_uint64, C.c_int32, C.c_int32]
+        L.orc_train_epoch_regress_parallel.restype = C.c_uint64
+        L.orc_predict_scaled.argtypes = [C.POINTER(_Machine), P, C.c_int64, C.c_int32, P]
         _lib = L
     return _lib
 
@@ -240,6 +250,30 @@ def train_epoch_sequential(tm: Machine, pool: Pool, margin, s, boost, seed, epoc
     lib().orc_train_epoch_sequential(tm._sync(), pool._sync(), margin, s, int(boost), seed, epoch,
                                      _ptr(ev))
     return ev
+
+
+def train_epoch_regress_sequential(tm: Machine, pool: Pool, margin, s, boost, seed, epoch) -> int:
+    return int(lib().orc_train_epoch_regress_sequential(tm._sync(), pool._sync(), margin, s, int(boost), seed,
+                                                        epoch))
+
+
+def train_epoch_regress_parallel(tm: Machine, pool: Pool, margin, s, boost, seed, workers, epoch) -> int:
+    if tm._s.q_bound != pool.q:
+        tm.bind(pool.q)
+    return int(lib().orc_train_epoch_regress_parallel(tm._sync(), pool._sync(), margin, s, int(boost), seed,
+                                                      workers, epoch))
+
+
+def update_regress(tm: Machine, lits, t, margin, s, boost, rng: Rng) -> int:
+    lits = np.ascontiguousarray(lits, np.uint64)
+    return int(lib().orc_update_regress(tm._sync(), _ptr(lits), t, margin, s, int(boost), C.byref(rng._r)))
+
+
+def predict_scaled(tm: Machine, lits, margin) -> np.ndarray:
+    lits = np.ascontiguousarray(lits, np.uint64)
+    out = np.zeros(lits.shape[0], np.int32)
+    lib().orc_predict_scaled(tm._sync(), _ptr(lits), lits.shape[0], margin, _ptr(out))
+    return out
 
 
 def refresh_tallies(tm: Machine, pool: Pool):

@@ -31,21 +31,10 @@
 #include "tsetlin/trainer.hpp"
 
 extern "C" {
-int tmg_synth_xor(std::uint64_t seed, std::int64_t rows, int features, double noise,
-                  int with_noise, std::uint8_t* bits, std::int32_t* labels);
-int tmg_synth_mnist(std::uint64_t seed, int features, int classes, double r_class,
-                    double r_sub, double flip, std::int64_t train_rows,
-                    std::int64_t test_rows, std::uint8_t* train_bits,
-                    std::int32_t* train_labels, std::uint8_t* test_bits,
-                    std::int32_t* test_labels);
-int tmg_synth_fmnist(std::uint64_t seed, int pixels, int classes, double r_class,
-                     double r_sub, int amp, std::int64_t train_rows, std::int64_t test_rows,
-                     std::uint8_t* train_bits, std::int32_t* train_labels,
+// csrc/synth.c: the canonical BASELINE.json datasets (shared with the GPU side)
+int tmg_synth_preset(int kind, std::uint64_t seed, double noise, std::int64_t train_rows,
+                     std::int64_t test_rows, std::uint8_t* train_bits, std::int32_t* train_labels,
                      std::uint8_t* test_bits, std::int32_t* test_labels);
-int tmg_synth_imdb(std::uint64_t seed, int vocab, int sentiment, double p_sent,
-                   double cross, std::int64_t train_rows, std::int64_t test_rows,
-                   std::uint8_t* train_bits, std::int32_t* train_labels,
-                   std::uint8_t* test_bits, std::int32_t* test_labels);
 }
 
 namespace fs = std::filesystem;
@@ -82,21 +71,10 @@ Split make_data(const std::string& kind, std::int64_t q, std::int64_t qt, std::u
   s.test_x.resize(static_cast<std::size_t>(qt) * s.features);
   s.train_y.resize(static_cast<std::size_t>(q));
   s.test_y.resize(static_cast<std::size_t>(qt));
-  int rc = 0;
-  if (kind == "xor") {
-    rc = tmg_synth_xor(seed, q, 12, noise, 1, s.train_x.data(), s.train_y.data());
-    if (!rc) rc = tmg_synth_xor(seed + 1000003, qt, 12, noise, 0, s.test_x.data(), s.test_y.data());
-  } else if (kind == "mnist") {
-    rc = tmg_synth_mnist(seed, 784, 10, 0.10, 0.10, 0.30, q, qt, s.train_x.data(),
-                         s.train_y.data(), s.test_x.data(), s.test_y.data());
-  } else if (kind == "fmnist") {
-    rc = tmg_synth_fmnist(seed, 784, 10, 0.10, 0.15, 40, q, qt, s.train_x.data(),
-                          s.train_y.data(), s.test_x.data(), s.test_y.data());
-  } else {
-    rc = tmg_synth_imdb(seed, 10000, 250, 0.04, 0.5, q, qt, s.train_x.data(), s.train_y.data(),
-                        s.test_x.data(), s.test_y.data());
-  }
-  if (rc) throw std::runtime_error("synthetic generator failed");
+  const int k = kind == "xor" ? 0 : kind == "mnist" ? 1 : kind == "fmnist" ? 2 : 3;
+  if (tmg_synth_preset(k, seed, noise, q, qt, s.train_x.data(), s.train_y.data(), s.test_x.data(),
+                       s.test_y.data()))
+    throw std::runtime_error("synthetic generator failed");
   return s;
 }
 

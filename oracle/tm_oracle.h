@@ -73,4 +73,14 @@ void orc_class_sums(const orc_machine* tm, const uint64_t* lits, int64_t q, int3
 void orc_predict(const orc_machine* tm, const uint64_t* lits, int64_t q, int32_t* pred);
 void orc_refresh_tallies(orc_machine* tm, orc_pool* pool);
 
+/* Regression head (tm_oracle_regress.c; m = 1 all-positive bank). */
+double orc_regress_gate(int32_t t, int32_t v, int32_t T);
+uint64_t orc_update_regress(orc_machine* tm, const uint64_t* lits, int32_t t, int32_t T, double s, int boost,
+                            orc_rng* r);
+uint64_t orc_train_epoch_regress_sequential(orc_machine* tm, orc_pool* pool, int32_t T, double s, int boost,
+                                            uint64_t seed, int32_t epoch);
+uint64_t orc_train_epoch_regress_parallel(orc_machine* tm, orc_pool* pool, int32_t T, double s, int boost,
+                                          uint64_t seed, int32_t workers, int32_t epoch);
+void orc_predict_scaled(const orc_machine* tm, const uint64_t* lits, int64_t q, int32_t T, int32_t* out);
+
 #endif

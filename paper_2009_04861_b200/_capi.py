@@ -100,8 +100,9 @@ SIGNATURES = {
     "tmg_epoch_order": (C.c_int, [U64, I32, I32, P]),
     "tmg_synth_xor": (C.c_int, [U64, I64, C.c_int, D, C.c_int, P, P]),
     "tmg_synth_mnist": (C.c_int, [U64, C.c_int, C.c_int, D, D, D, I64, I64, P, P, P, P]),
-    "tmg_synth_fmnist": (C.c_int, [U64, C.c_int, C.c_int, D, D, C.c_int, I64, I64, P, P, P, P]),
+    "tmg_synth_fmnist": (C.c_int, [U64, C.c_int, C.c_int, D, D, C.c_int, D, I64, I64, P, P, P, P]),
     "tmg_synth_imdb": (C.c_int, [U64, C.c_int, C.c_int, D, D, I64, I64, P, P, P, P]),
+    "tmg_synth_preset": (C.c_int, [C.c_int, U64, D, I64, I64, P, P, P, P]),
 }
 
 _lib = None

@@ -96,12 +96,14 @@ TMG_EXPORT int tmg_synth_mnist(uint64_t seed, int features, int classes, double 
 }
 
 /* Fashion-MNIST-shaped: `pixels` grey levels from per-class grey prototypes
- * (resampled at r_class from a shared base, 8 sub-prototypes at r_sub), plus
- * uniform additive noise of +-amp, thermometer-coded at 64/128/192 into
- * 3*pixels bits (bit 3*i+t = grey_i > threshold_t). */
+ * (resampled at r_class from a shared base, 8 sub-prototypes at r_sub),
+ * blended with a random other class's prototype at weight w ~ U[0, mix)
+ * (ambiguous, non-saturating examples), plus uniform additive noise of +-amp,
+ * thermometer-coded at 64/128/192 into 3*pixels bits (bit 3*i+t =
+ * grey_i > threshold_t). */
 TMG_EXPORT int tmg_synth_fmnist(uint64_t seed, int pixels, int classes, double r_class,
-                                double r_sub, int amp, int64_t train_rows, int64_t test_rows,
-                                uint8_t* train_bits, int32_t* train_labels,
+                                double r_sub, int amp, double mix, int64_t train_rows,
+                                int64_t test_rows, uint8_t* train_bits, int32_t* train_labels,
                                 uint8_t* test_bits, int32_t* test_labels) {
   enum { SUBS = 8 };
   static const int thresholds[3] = {64, 128, 192};
@@ -135,8 +137,14 @@ TMG_EXPORT int tmg_synth_fmnist(uint64_t seed, int pixels, int classes, double r
     const int cls = (int)tmg_rng_below(&g, (uint32_t)classes);
     const int kk = (int)tmg_rng_below(&g, SUBS);
     const uint8_t* proto = sub + ((size_t)cls * SUBS + kk) * pixels;
+    int other = (int)tmg_rng_below(&g, (uint32_t)(classes - 1));
+    const double w = tmg_rng_uniform(&g) * mix;
+    const uint8_t* oproto;
+    if (other >= cls) ++other;
+    oproto = sub + ((size_t)other * SUBS + kk) * pixels;
     for (i = 0; i < pixels; ++i) {
-      int v = (int)proto[i] + (int)tmg_rng_below(&g, (uint32_t)(2 * amp + 1)) - amp;
+      const double blend = (1.0 - w) * (double)proto[i] + w * (double)oproto[i];
+      int v = (int)(blend + 0.5) + (int)tmg_rng_below(&g, (uint32_t)(2 * amp + 1)) - amp;
       if (v < 0) v = 0;
       if (v > 255) v = 255;
       for (t = 0; t < 3; ++t) x[3 * i + t] = (uint8_t)(v > thresholds[t]);
@@ -145,6 +153,36 @@ TMG_EXPORT int tmg_synth_fmnist(uint64_t seed, int pixels, int classes, double r
   }
   free(base); free(pc); free(sub);
   return 0;
+}
+
+/* The canonical datasets of BASELINE.json configs (single source of truth for
+ * the GPU bench/tests and oracle/ref_driver): kind 0 XOR12 (label noise
+ * `noise`), 1 MNIST-shaped, 2 FMNIST-shaped, 3 IMDb-shaped. Returns the
+ * feature count via *features (bits must hold rows x features). */
+int tmg_synth_imdb(uint64_t seed, int vocab, int sentiment, double p_sent, double cross,
+                   int64_t train_rows, int64_t test_rows, uint8_t* train_bits,
+                   int32_t* train_labels, uint8_t* test_bits, int32_t* test_labels);
+
+TMG_EXPORT int tmg_synth_preset(int kind, uint64_t seed, double noise, int64_t train_rows, int64_t test_rows,
+                                uint8_t* train_bits, int32_t* train_labels, uint8_t* test_bits,
+                                int32_t* test_labels) {
+  switch (kind) {
+    case 0: {
+      const int rc = tmg_synth_xor(seed, train_rows, 12, noise, 1, train_bits, train_labels);
+      return rc ? rc : tmg_synth_xor(seed + 1000003, test_rows, 12, noise, 0, test_bits, test_labels);
+    }
+    case 1:  /* SURVEY.md §8(d) calibrated recipe */
+      return tmg_synth_mnist(seed, 784, 10, 0.10, 0.10, 0.30, train_rows, test_rows, train_bits,
+                             train_labels, test_bits, test_labels);
+    case 2:
+      return tmg_synth_fmnist(seed, 784, 10, 0.10, 0.15, 60, 0.8, train_rows, test_rows, train_bits,
+                              train_labels, test_bits, test_labels);
+    case 3:
+      return tmg_synth_imdb(seed, 10000, 250, 0.10, 0.3, train_rows, test_rows, train_bits, train_labels,
+                            test_bits, test_labels);
+    default:
+      return -1;
+  }
 }
 
 /* IMDb-shaped bag of words: vocabulary `vocab`, Zipf(1) frequencies with rank

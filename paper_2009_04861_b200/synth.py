@@ -25,31 +25,14 @@ def _alloc(q, o):
 
 
 def make(kind: str, q: int, qt: int, seed: int, noise: float = 0.0) -> Split:
-    """Same recipes and seeds as oracle/ref_driver.cpp make_data()."""
-    if kind == "xor":
-        o, m = 12, 2
-        tx, ty = _alloc(q, o)
-        vx, vy = _alloc(qt, o)
-        assert lib().tmg_synth_xor(seed, q, o, noise, 1, tx.ctypes.data, ty.ctypes.data) == 0
-        assert lib().tmg_synth_xor(seed + 1000003, qt, o, noise, 0, vx.ctypes.data, vy.ctypes.data) == 0
-    elif kind == "mnist":
-        o, m = 784, 10
-        tx, ty = _alloc(q, o)
-        vx, vy = _alloc(qt, o)
-        assert lib().tmg_synth_mnist(seed, 784, 10, 0.10, 0.10, 0.30, q, qt, tx.ctypes.data,
-                                     ty.ctypes.data, vx.ctypes.data, vy.ctypes.data) == 0
-    elif kind == "fmnist":
-        o, m = 2352, 10
-        tx, ty = _alloc(q, o)
-        vx, vy = _alloc(qt, o)
-        assert lib().tmg_synth_fmnist(seed, 784, 10, 0.10, 0.15, 40, q, qt, tx.ctypes.data,
-                                      ty.ctypes.data, vx.ctypes.data, vy.ctypes.data) == 0
-    elif kind == "imdb":
-        o, m = 10000, 2
-        tx, ty = _alloc(q, o)
-        vx, vy = _alloc(qt, o)
-        assert lib().tmg_synth_imdb(seed, 10000, 250, 0.04, 0.5, q, qt, tx.ctypes.data,
-                                    ty.ctypes.data, vx.ctypes.data, vy.ctypes.data) == 0
-    else:
+    """The canonical presets of csrc/synth.c (tmg_synth_preset), shared with
+    oracle/ref_driver.cpp make_data()."""
+    shapes = {"xor": (0, 12, 2), "mnist": (1, 784, 10), "fmnist": (2, 2352, 10), "imdb": (3, 10000, 2)}
+    if kind not in shapes:
         raise ValueError(f"unknown dataset {kind}")
+    k, o, m = shapes[kind]
+    tx, ty = _alloc(q, o)
+    vx, vy = _alloc(qt, o)
+    assert lib().tmg_synth_preset(k, seed, noise, q, qt, tx.ctypes.data, ty.ctypes.data, vx.ctypes.data,
+                                  vy.ctypes.data) == 0
     return Split(o, m, tx, ty, vx, vy)

@@ -112,6 +112,32 @@ def test_epochs(mode, name):
         _check_state(d, "refreshed", tm, pool)
 
 
+@pytest.mark.parametrize("mode", ["par", "seq"])
+def test_regression_head(mode):
+    man = manifest("regression")
+    x, y = load("regression", "train_x.npy"), load("regression", "train_y.npy")
+    pool = O.Pool(x, y, 1)  # scaled targets == y here (T = y_max - y_min = 10)
+    tm = O.Machine(man["o"], 1, man["clauses"], man["N"], pool.q)
+    T_, s, seed = man["margin"], man["s"], man["seed"]
+    for e, want in enumerate(man[f"{mode}_events"]):
+        if mode == "par":
+            ev = O.train_epoch_regress_parallel(tm, pool, T_, s, False, seed, 1, e)
+            assert np.array_equal(pool.tallies[:, 0], load("regression", f"par_epoch{e}_tallies.npy"))
+            assert np.array_equal(tm.prev[0].reshape(-1), load("regression", f"par_epoch{e}_prev.npy"))
+        else:
+            ev = O.train_epoch_regress_sequential(tm, pool, T_, s, False, seed, e)
+        assert ev == want
+        assert np.array_equal(tm.counters[0], load("regression", f"{mode}_epoch{e}_counters.npy"))
+    tx = load("regression", "test_x.npy")
+    pred = O.predict_scaled(tm, O.pack_literals(tx), T_)
+    assert np.array_equal(pred, load("regression", f"{mode}_predict_scaled.npy"))
+    if mode == "seq":
+        r = O.Rng(99, 4)
+        assert O.update_regress(tm, O.pack_literals(tx[3])[0], 7, T_, s, False, r) == man["update_regress_events"]
+        assert np.array_equal(tm.counters[0], load("regression", "update_regress_counters.npy"))
+        assert r.next() == int(man["update_regress_next"])
+
+
 @pytest.mark.parametrize("name,o,m,n", [("mnist_rand", 784, 10, 50), ("single_bank", 30, 1, 8),
                                         ("dense_o64", 64, 3, 12)])
 def test_inference_random_states(name, o, m, n):

@@ -13,11 +13,11 @@ import paper_2009_04861_b200 as T  # noqa: E402
 from paper_2009_04861_b200._capi import lib  # noqa: E402
 
 
-def fmnist(r_class, r_sub, amp, q, qt):
+def fmnist(r_class, r_sub, amp, mix, q, qt):
     tx, ty = np.zeros((q, 2352), np.uint8), np.zeros(q, np.int32)
     vx, vy = np.zeros((qt, 2352), np.uint8), np.zeros(qt, np.int32)
-    assert lib().tmg_synth_fmnist(2352, 784, 10, r_class, r_sub, amp, q, qt, tx.ctypes.data, ty.ctypes.data,
-                                  vx.ctypes.data, vy.ctypes.data) == 0
+    assert lib().tmg_synth_fmnist(2352, 784, 10, r_class, r_sub, amp, mix, q, qt, tx.ctypes.data,
+                                  ty.ctypes.data, vx.ctypes.data, vy.ctypes.data) == 0
     return tx, ty, vx, vy
 
 
@@ -41,8 +41,9 @@ def trial(data, m, n, T_, s, epochs=2):
     return accs
 
 
-for rc, rs, amp in [(0.10, 0.15, 40), (0.05, 0.2, 90), (0.04, 0.25, 120), (0.03, 0.3, 140)]:
-    print(json.dumps({"fmnist": [rc, rs, amp], "acc": trial(fmnist(rc, rs, amp, 10000, 2000), 10, 2000, 100, 15.0)}),
-          flush=True)
-for ps, cr in [(0.04, 0.5), (0.02, 0.7), (0.015, 0.8)]:
+for rc, rs, amp, mix in [(0.10, 0.15, 60, 0.8), (0.10, 0.15, 60, 0.9), (0.10, 0.15, 90, 0.95),
+                         (0.05, 0.15, 60, 0.9)]:
+    print(json.dumps({"fmnist": [rc, rs, amp, mix],
+                      "acc": trial(fmnist(rc, rs, amp, mix, 10000, 2000), 10, 2000, 100, 15.0)}), flush=True)
+for ps, cr in [(0.10, 0.3), (0.15, 0.3), (0.08, 0.2), (0.2, 0.4)]:
     print(json.dumps({"imdb": [ps, cr], "acc": trial(imdb(ps, cr, 5000, 2000), 2, 2000, 100, 15.0)}), flush=True)
