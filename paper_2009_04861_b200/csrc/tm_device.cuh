@@ -178,35 +178,27 @@ __device__ __forceinline__ void bernoulli_words(const uint32_t (&need)[K], const
       }
     }
   }
-  int cnt = 0;
+  // Phase 2: every round resolves the lowest undecided literal of EVERY word
+  // slot at once (one private random word per slot, ceil(K/4) Philox blocks
+  // per round); rounds repeat while any lane of the warp has one left
+  // (~1.3 rounds on average at MNIST shape).
+  uint32_t left = 0;
 #pragma unroll
-  for (int k = 0; k < K; ++k) cnt += __popc(und[k]);
-  for (int blk = 2; __any_sync(kFull, cnt > 0); ++blk) {
-    const U4 r = gen(K, blk);
+  for (int k = 0; k < K; ++k) left |= und[k];
+  for (int round = 0; __any_sync(kFull, left != 0); ++round) {
+    U4 r[(K + 3) / 4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t word = i == 0 ? r.x : (i == 1 ? r.y : (i == 2 ? r.z : r.w));
-      // lowest undecided literal of the lane (none: bit = 0, a no-op)
-      uint32_t bit = 0, s = 0;
-      int k = -1;
+    for (int b = 0; b < (K + 3) / 4; ++b) r[b] = gen(K, 2 + round * ((K + 3) / 4) + b);
+    left = 0;
 #pragma unroll
-      for (int kk = K - 1; kk >= 0; --kk)
-        if (und[kk]) k = kk;
-#pragma unroll
-      for (int kk = 0; kk < K; ++kk)
-        if (kk == k) {
-          bit = und[kk] & (0u - und[kk]);
-          s = sel[kk];
-        }
-      const uint32_t rest = (SEL && (s & bit)) ? th.hi_rest : th.lo_rest;
-      const uint32_t take = ((word >> 8) < rest) ? bit : 0u;
-#pragma unroll
-      for (int kk = 0; kk < K; ++kk)
-        if (kk == k) {
-          und[kk] ^= bit;
-          less[kk] |= take;
-        }
-      cnt -= bit ? 1 : 0;
+    for (int k = 0; k < K; ++k) {
+      const U4& rb = r[k / 4];
+      const uint32_t word = (k & 3) == 0 ? rb.x : ((k & 3) == 1 ? rb.y : ((k & 3) == 2 ? rb.z : rb.w));
+      const uint32_t bit = und[k] & (0u - und[k]);  // lowest undecided literal (0: none)
+      const uint32_t rest = (SEL && (sel[k] & bit)) ? th.hi_rest : th.lo_rest;
+      less[k] |= ((word >> 8) < rest) ? bit : 0u;
+      und[k] ^= bit;
+      left |= und[k];
     }
   }
 }

@@ -49,8 +49,10 @@ struct Clause {
         for (int b = 0; b < B; ++b) base[(b * 2 + part) * Wp + p * 32 + lane] = s[part][p].p[b];
   }
 
+  bool nonempty = false;  // include count > 0, refreshed by every eval_train
+
   // Train-mode evaluation (core.hpp:208-219): empty clause -> 1.
-  __device__ __forceinline__ int eval_train(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) const {
+  __device__ __forceinline__ int eval_train(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) {
     uint32_t viol = 0, any = 0;
 #pragma unroll
     for (int p = 0; p < NW; ++p) {
@@ -59,8 +61,25 @@ struct Clause {
       any |= ix | in;
     }
     const unsigned vb = __ballot_sync(kFull, viol != 0);
-    const unsigned ab = __ballot_sync(kFull, any != 0);
-    return ab == 0 ? 1 : (vb == 0 ? 1 : 0);
+    nonempty = __any_sync(kFull, any != 0);
+    return !nonempty ? 1 : (vb == 0 ? 1 : 0);
+  }
+
+  // Same, reusing the include-set emptiness of the last eval_train (valid
+  // while the automata have not moved since).
+  __device__ __forceinline__ int eval_cached(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) const {
+    uint32_t viol = 0;
+#pragma unroll
+    for (int p = 0; p < NW; ++p) viol |= (s[0][p].p[B - 1] & ~x[p]) | (s[1][p].p[B - 1] & ~n[p]);
+    const unsigned vb = __ballot_sync(kFull, viol != 0);
+    return !nonempty ? 1 : (vb == 0 ? 1 : 0);
+  }
+
+  __device__ __forceinline__ void refresh_nonempty() {
+    uint32_t any = 0;
+#pragma unroll
+    for (int p = 0; p < NW; ++p) any |= s[0][p].p[B - 1] | s[1][p].p[B - 1];
+    nonempty = __any_sync(kFull, any != 0);
   }
 
   __device__ __forceinline__ int include_count() const {
@@ -183,6 +202,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   Clause<NW, B> cl;
   uint32_t* st = P.state + static_cast<size_t>(lc) * B * 2 * P.Wp;
   cl.load(st, P.Wp, lane, P.o);
+  cl.refresh_nonempty();
   uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
   // Per-clause starting position in the epoch order (trainer.cpp:41-44, 222-223).
   const int64_t offset = static_cast<int64_t>(splitmix_dev(static_cast<uint64_t>(g) + 1) %
@@ -221,37 +241,44 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
     if (!gm) continue;
     events += __popc(gm);
 
-    // ---- gated steps in order; the next step's literal words and previous-
-    // output word are prefetched while the current one is processed.
+    // ---- gated steps in order; the next step's literal words are prefetched
+    // while the current one is processed. The previous-output word is loaded
+    // at the start of a step and only consumed after the feedback.
+    const int iq = static_cast<int>(i);  // q < 2^31
     int sl = __ffs(gm) - 1;
     gm &= gm - 1;
-    int64_t is = __shfl_sync(kFull, i, sl);
+    int is = __shfl_sync(kFull, iq, sl);
     int tg = __shfl_sync(kFull, target, sl);
     uint32_t x[NW], n[NW];
+    {
+      const uint32_t* xr = P.xplane + static_cast<size_t>(is) * P.Wp + lane;
+      const uint32_t* nr = P.nplane + static_cast<size_t>(is) * P.Wp + lane;
 #pragma unroll
-    for (int p = 0; p < NW; ++p) {
-      x[p] = __ldg(P.xplane + is * P.Wp + p * 32 + lane);
-      n[p] = __ldg(P.nplane + is * P.Wp + p * 32 + lane);
+      for (int p = 0; p < NW; ++p) {
+        x[p] = __ldg(xr + p * 32);
+        n[p] = __ldg(nr + p * 32);
+      }
     }
-    uint32_t pword = lane == 0 ? prev_row[is >> 5] : 0u;
     while (true) {
+      uint32_t pword = 0;
+      if (lane == 0) pword = prev_row[is >> 5];
       const bool more = gm != 0;
-      int64_t is2 = 0;
-      int tg2 = 0;
-      uint32_t x2[NW], n2[NW], pword2 = 0;
+      int is2 = 0, tg2 = 0;
+      uint32_t x2[NW], n2[NW];
       if (more) {
         const int sl2 = __ffs(gm) - 1;
         gm &= gm - 1;
-        is2 = __shfl_sync(kFull, i, sl2);
+        is2 = __shfl_sync(kFull, iq, sl2);
         tg2 = __shfl_sync(kFull, target, sl2);
+        const uint32_t* xr = P.xplane + static_cast<size_t>(is2) * P.Wp + lane;
+        const uint32_t* nr = P.nplane + static_cast<size_t>(is2) * P.Wp + lane;
 #pragma unroll
         for (int p = 0; p < NW; ++p) {
-          x2[p] = __ldg(P.xplane + is2 * P.Wp + p * 32 + lane);
-          n2[p] = __ldg(P.nplane + is2 * P.Wp + p * 32 + lane);
+          x2[p] = __ldg(xr + p * 32);
+          n2[p] = __ldg(nr + p * 32);
         }
-        if (lane == 0) pword2 = prev_row[is2 >> 5];
       }
-      const int before = cl.eval_train(x, n);
+      const int before = cl.eval_cached(x, n);
       int after = before;
       if (tg == 0) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
@@ -263,14 +290,13 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       if (lane == 0) {
         const uint32_t bit = 1u << (is & 31);
         if (((pword & bit) != 0) != (after != 0)) {
-          pword ^= bit;
-          prev_row[is >> 5] = pword;
+          prev_row[is >> 5] = pword ^ bit;
           int delta = after ? 1 : -1;
           if (!positive) delta = -delta;
-          atomicAdd(&P.tallies[is * P.m + c], delta);
-          if (P.tally_delta) atomicAdd(&P.tally_delta[is * P.m + c], delta);
+          const size_t ti = static_cast<size_t>(is) * P.m + c;
+          atomicAdd(&P.tallies[ti], delta);
+          if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
         }
-        if (more && (is2 >> 5) == (is >> 5)) pword2 = pword;  // same bitmap word: forward
       }
       if (!more) break;
       is = is2;
@@ -280,7 +306,6 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
         x[p] = x2[p];
         n[p] = n2[p];
       }
-      pword = pword2;
     }
   }
   cl.store(st, P.Wp, lane);
