@@ -92,6 +92,22 @@ def test_model_file_parser_matches_reference_text():
         model_io.parse(text.replace("end\n", "fin\n"))
 
 
+def test_bench_csv_schema_matches_reference():
+    """f4: the reference's CSV columns and %.9g formatting (bench.cpp:120-142)."""
+    from paper_2009_04861_b200.bench_sweep import (BenchRecord, median_epoch_seconds, read_bench_csv,
+                                                   write_bench_csv)
+    recs = [BenchRecord("par", 64, 2000, 0, 0.1234567891234, "accuracy", 0.9375),
+            BenchRecord("par", 64, 2000, 1, 0.2, "accuracy", 1.0),
+            BenchRecord("par", 64, 2000, 2, 0.05, "accuracy", 0.5)]
+    text = write_bench_csv(recs)
+    assert text.splitlines()[0] == "mode,workers,clauses,epoch,seconds,metric_name,metric_value"
+    assert text.splitlines()[1] == "par,64,2000,0,0.123456789,accuracy,0.9375"
+    assert median_epoch_seconds(recs, "par", 2000) == pytest.approx(0.1234567891234)
+    assert [r.epoch for r in read_bench_csv(text)] == [0, 1, 2]
+    with pytest.raises(ValueError):
+        median_epoch_seconds(recs, "seq", 2000)
+
+
 def test_shard_ranges_even_aligned_and_cover():
     from paper_2009_04861_b200.distributed import shard_range, window_bounds
     for n in [2, 20, 2000, 2002, 7000]:

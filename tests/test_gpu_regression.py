@@ -69,6 +69,21 @@ def test_regression_async_learns():
     assert mae < 2.5, mae  # reference W=1, 3 epochs: 2.12; a constant predictor: ~1.9-2.5
 
 
+def test_bench_sweep_csv_gpu():
+    """f4: the reference's clause sweep (bench.cpp:45-118) with GPU rows."""
+    from paper_2009_04861_b200 import bench_sweep as BS
+    from paper_2009_04861_b200 import synth
+    d = synth.make("xor", 2000, 500, 7, 0.1)
+    opts = BS.BenchOptions(clause_counts=[10, 20], modes=["seq", "par"], warmup_epochs=1, measured_epochs=2)
+    recs = BS.bench_sweep(d.train_x, d.train_y, d.test_x, d.test_y,
+                          T.TMConfig(margin=15, specificity=3.9, seed=1), opts)
+    assert len(recs) == 2 * 2 * 2
+    assert all(r.metric_name == "accuracy" and 0.4 <= r.metric_value <= 1.0 and r.seconds > 0 for r in recs)
+    text = BS.write_bench_csv(recs)
+    assert len(text.splitlines()) == 9
+    assert BS.median_epoch_seconds(recs, "par", 20) > 0
+
+
 def test_model_files_roundtrip_and_match_reference():
     """tmmodel v1: GPU-trained (sync mirror) machine == reference bytes; load back."""
     d = ("epoch_par_w1", "xor12")
