@@ -243,19 +243,25 @@ def run_ours(args):
     # ---- e2e: host buffers through the C ABI, copies inside the timed region
     host_bits = torch.from_numpy(d.train_x).pin_memory().numpy()
     host_lab = torch.from_numpy(d.train_y).pin_memory().numpy()
-    e2e_ms = []
-    for _ in range(args.steps):
+    e2e_ms, e2e_phases = [], []
+    for it in range(args.warmup + args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
         p2 = T.ExamplePool(O_FEAT, host_bits, host_lab, M_CLS, device=local)
+        t1 = time.perf_counter()
         ev, _, _ = one_epoch(p2)
         _ = [int(v) for v in ev]  # per-class report read back to the host
+        t2 = time.perf_counter()
         del p2
         torch.cuda.synchronize()
         barrier()
-        e2e_ms.append(max_over_ranks((time.perf_counter() - t0) * 1e3))
+        t3 = time.perf_counter()
+        dt = max_over_ranks((t3 - t0) * 1e3)
+        if it >= args.warmup:  # the same W untimed warm-up steps as the resident arm
+            e2e_ms.append(dt)
+            e2e_phases.append(((t1 - t0) * 1e3, (t2 - t1) * 1e3, (t3 - t2) * 1e3))
 
     if rank != 0:
         if world > 1:
@@ -296,6 +302,9 @@ def run_ours(args):
                                            f"LOP3-only {lop3_peak / 1e12:.2f} Tops/s",
                             "ops_model": "SURVEY.md 8(d): gate 18, eval 2*ceil(2o/32), TypeI 2o*18, TypeII 2o*3"}
     line["e2e"] = {"value": e2e_val, "unit": UNIT, "ms_per_step": statistics.mean(e2e_ms),
+                   "ms_all": [round(v, 3) for v in e2e_ms],
+                   "phases_ms": {k: round(statistics.mean(ph[n] for ph in e2e_phases), 3)
+                                 for n, k in enumerate(("pool_h2d_pack", "epoch_and_report", "pool_free"))},
                    "h2d_bytes_per_step": int(host_bits.nbytes + host_lab.nbytes + 4 * Q_TRAIN),
                    "d2h_bytes_per_step": int(8 * M_CLS * 2)}
     # ---- CPU reference beside it (rank 0, N=1 only)

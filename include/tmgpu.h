@@ -101,6 +101,14 @@ int tmg_machine_stream(tmg_machine* tm, void** stream);
  * entries, reference order) the +1 (inc) and -1 (dec) transitions. */
 int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
                              int32_t clause_output, uint32_t trials, uint64_t* inc, uint64_t* dec);
+/* One asynchronous Type I feedback (the epoch kernel's type_i_async: Philox
+ * key of `epoch`, counters (global clause g = bank*clauses + j, example)) applied
+ * in place to clause j of `bank` on one literal row (reference layout) with the
+ * given clause output. Deterministic; register-resident shapes only
+ * (feature_count <= 4096). Replaces one draw-for-draw call of
+ * detail::type_i_with_output (feedback.cpp:32-70) under the async RNG. */
+int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
+                           int32_t clause_output, uint32_t example, int32_t epoch);
 /* Integer-pipe roofline probe: LOP3-only and LOP3+IMAD thread-ops per second. */
 int tmg_bench_int_peak(int32_t device, double* lop3_ops_per_s, double* mixed_ops_per_s);
 

@@ -87,6 +87,10 @@ def lib():
                                                        C.c_double, C.c_int, C.c_uint64, C.c_int32, C.c_int32]
         L.orc_train_epoch_regress_parallel.restype = C.c_uint64
         L.orc_predict_scaled.argtypes = [C.POINTER(_Machine), P, C.c_int64, C.c_int32, P]
+        L.orc_philox4x32.argtypes = [P, C.c_uint32, C.c_uint32, C.c_int, P]
+        L.orc_async_key.argtypes = [C.c_uint64, C.c_int32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        L.orc_async_type_i.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32,
+                                       C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int32, C.c_int32]
         _lib = L
     return _lib
 
@@ -280,3 +284,29 @@ def refresh_tallies(tm: Machine, pool: Pool):
     if tm._s.q_bound != pool.q:
         tm.bind(pool.q)
     lib().orc_refresh_tallies(tm._sync(), pool._sync())
+
+
+def philox4x32(ctr, key0: int, key1: int, rounds: int = 7) -> np.ndarray:
+    """Philox4x32-R block (tm_oracle_async.c), the async engine's generator."""
+    c = np.ascontiguousarray(ctr, np.uint32)
+    out = np.zeros(4, np.uint32)
+    lib().orc_philox4x32(_ptr(c), key0, key1, rounds, _ptr(out))
+    return out
+
+
+def async_key(seed: int, epoch: int):
+    """Philox key (key0, key1) of an async epoch."""
+    k0, k1 = C.c_uint32(0), C.c_uint32(0)
+    lib().orc_async_key(seed, epoch, C.byref(k0), C.byref(k1))
+    return int(k0.value), int(k1.value)
+
+
+def async_type_i(counters_row: np.ndarray, lits_row: np.ndarray, o: int, N: int, out: int, s: float,
+                 boost: bool, g: int, i: int, seed: int, epoch: int, nw: int, rounds: int = 7) -> np.ndarray:
+    """One async-engine Type I feedback on one clause's 2o counters (copy)."""
+    row = np.ascontiguousarray(counters_row, np.uint16).copy()
+    lits = np.ascontiguousarray(lits_row, np.uint64)
+    k0, k1 = async_key(seed, epoch)
+    lib().orc_async_type_i(_ptr(row), _ptr(lits), o, N, int(out), float(s), int(bool(boost)), g, i, k0, k1,
+                           nw, rounds)
+    return row

@@ -83,4 +83,12 @@ uint64_t orc_train_epoch_regress_parallel(orc_machine* tm, orc_pool* pool, int32
                                           uint64_t seed, int32_t workers, int32_t epoch);
 void orc_predict_scaled(const orc_machine* tm, const uint64_t* lits, int64_t q, int32_t T, int32_t* out);
 
+/* tm_oracle_async.c: the async engine's Philox Type I draw, restated. */
+void orc_philox4x32(const uint32_t ctr[4], uint32_t k0, uint32_t k1, int rounds, uint32_t out[4]);
+void orc_async_key(uint64_t seed, int32_t epoch, uint32_t* key0, uint32_t* key1);
+uint32_t orc_prob_threshold(double p);
+void orc_async_type_i(uint16_t* counters, const uint64_t* lits, int32_t o, int32_t N, int32_t out, double s,
+                      int32_t boost, uint32_t g, uint32_t i, uint32_t key0, uint32_t key1, int32_t nw,
+                      int32_t rounds);
+
 #endif

@@ -3,6 +3,7 @@
 // the epoch orchestration (permutation, Philox keys, thresholds) and the
 // conversions between the reference's host layouts and the device layouts.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -69,6 +70,21 @@ struct DeviceGuard {
   }
 };
 
+// Keeps the current device's default memory pool from returning freed memory
+// to the driver at every synchronisation (once per device).
+void pool_init() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  static std::atomic<bool> done[64];
+  if (done[dev].load(std::memory_order_acquire)) return;
+  cudaMemPool_t mp;
+  if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev].store(true, std::memory_order_release);
+}
+
 template <typename T>
 struct DevBuf {
   T* ptr = nullptr;
@@ -77,13 +93,25 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
+  // Device memory comes from the device's stream-ordered pool, which keeps
+  // freed blocks mapped (release threshold raised in pool_init): creating and
+  // dropping example pools per call stays cheap. alloc/release keep
+  // cudaMalloc/cudaFree's synchronous semantics.
   void alloc(size_t n) {
     release();
-    if (n) CK(cudaMalloc(&ptr, n * sizeof(T)));
+    if (n) {
+      pool_init();
+      CK(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), cudaStreamPerThread));
+      CK(cudaStreamSynchronize(cudaStreamPerThread));
+    }
     count = n;
   }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr) {
+      cudaDeviceSynchronize();
+      cudaFreeAsync(ptr, cudaStreamPerThread);
+      cudaStreamSynchronize(cudaStreamPerThread);
+    }
     ptr = nullptr;
     count = 0;
   }
@@ -999,6 +1027,41 @@ TMG_API int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, c
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(inc, dinc.ptr, dinc.bytes(), cudaMemcpyDeviceToHost, tm->stream));
     CK(cudaMemcpyAsync(dec, ddec.ptr, ddec.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
+                                   int32_t clause_output, uint32_t example, int32_t epoch) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
+    if (!literals) fail(TMG_EINVAL, "null literal row");
+    DeviceGuard dg(tm->device);
+    const int W64 = (2 * tm->o + 63) / 64;
+    DevBuf<uint64_t> dl;
+    DevBuf<uint32_t> xs, ns;
+    dl.alloc(W64);
+    xs.alloc(tm->Wp);
+    ns.alloc(tm->Wp);
+    CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    epoch_keys(tm, epoch);
+    tmg_pool fake;
+    fake.o = tm->o;
+    fake.m = tm->m;
+    fake.q = 1;
+    tmg::TrainParams p = make_params(tm, &fake);
+    p.xplane = xs.ptr;
+    p.nplane = ns.ptr;
+    const size_t lc = static_cast<size_t>(bank) * tm->n_loc + (j - tm->j_begin);
+    const uint32_t g = static_cast<uint32_t>(bank) * tm->n + j;
+    if (!tmg::type_i_async_once_launch(p, tm->state.ptr + lc * tm->B * 2 * tm->Wp, g, example,
+                                       clause_output ? 1 : 0, tm->B, tm->NW, tm->stream))
+      fail(TMG_EINVAL, "async Type I probe not instantiated for this shape");
+    CK(cudaGetLastError());
+    tm->entries_dirty = true;
+    rebuild_entries(tm);
     CK(cudaStreamSynchronize(tm->stream));
   });
 }

@@ -134,6 +134,36 @@ __device__ __forceinline__ void step_down(Planes<B>& s, uint32_t dec, uint32_t l
   sub_one<B>(s, dec & ~eq_const<B>(s, lo));
 }
 
+// The same two steps when N = 2^(B-1), i.e. lo = 0 and hi = 2^B - 1: the
+// borrow (carry) chain is formed first; what leaves the top plane is exactly
+// the set of lanes already at lo (hi), which are then left untouched. One
+// LOP3 per plane for the chain and one for the flip, no separate compare.
+template <int B>
+__device__ __forceinline__ void sub_one_sat0(Planes<B>& s, uint32_t dec) {
+  uint32_t chain[B];
+  uint32_t t = dec;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    chain[b] = t;
+    t &= ~s.p[b];
+  }
+#pragma unroll
+  for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
+}
+
+template <int B>
+__device__ __forceinline__ void add_one_sat1(Planes<B>& s, uint32_t inc) {
+  uint32_t chain[B];
+  uint32_t t = inc;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    chain[b] = t;
+    t &= s.p[b];
+  }
+#pragma unroll
+  for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
+}
+
 // Warp-cooperative exact Bernoulli masks for one Type I event: every lane
 // owns K words of literals; bit b of word k is wanted with probability
 // P / 2^32 where P = P_high if bit b of sel[k] else P_low (SEL=false: always

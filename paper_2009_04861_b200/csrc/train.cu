@@ -18,11 +18,21 @@
 #include "kernels.h"
 #include "tm_device.cuh"
 
+#ifndef TMG_ASYNC_P2
+#define TMG_ASYNC_P2 1  // fused saturation when N = 2^(B-1)
+#endif
+#ifndef TMG_ASYNC_UNROLL_NW
+#define TMG_ASYNC_UNROLL_NW 1  // widest rows (words per lane) that get the 2x unrolled step loop
+#endif
+#ifndef TMG_ASYNC_V5
+#define TMG_ASYNC_V5 1  // window-deferred record + 2x unrolled step loop
+#endif
+
 namespace tmg {
 
 namespace {
 
-template <int NW, int B>
+template <int NW, int B, bool P2 = false>  // P2: N = 2^(B-1) (lo = 0, hi = all ones)
 struct Clause {
   Planes<B> s[2][NW];  // [part][pass]
   uint32_t valid[NW];  // literal bits that exist (f < o)
@@ -121,7 +131,14 @@ struct Clause {
       const uint32_t incl = w.p[B - 1];
       const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid[p];
       const uint32_t dec = ~lit & bern & ~incl & valid[p];
-      step<B>(w, inc, dec, lo, hi);
+      if (P2) {  // inc and dec lanes are disjoint
+        add_one_sat1<B>(w, inc);
+        sub_one_sat0<B>(w, dec);
+      } else {
+        step<B>(w, inc, dec, lo, hi);
+      }
+    } else if (P2) {
+      sub_one_sat0<B>(w, bern & valid[p]);
     } else {
       step_down<B>(w, bern & valid[p], lo);
     }
@@ -153,8 +170,8 @@ __device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row,
 // Type I (feedback.cpp:32-70) on every word of the clause with the exact
 // warp-cooperative Bernoulli sampler; counters keyed (clause g, example i,
 // literal word, block) so the draws do not depend on scheduling.
-template <int NW, int B>
-__device__ __forceinline__ void type_i_async(Clause<NW, B>& cl, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
+template <int NW, int B, bool P2>
+__device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
                                              int before, const TrainParams& P, uint32_t g, uint32_t i,
                                              int lane) {
   constexpr int K = 2 * NW;
@@ -179,15 +196,20 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B>& cl, const uint32_t (
   }
 }
 
-template <int NW, int B>
+// Resident CTAs (4 warps each) per SM for one instantiation: as many as the
+// register file allows for the clause planes (2*NW*B registers), the literal
+// double buffer and the sampler's working set without spilling. NW=1, B=8
+// (MNIST) gets 8 CTAs = 32 warps at 64 registers, the fastest in the r1m sweep.
 #ifndef TMG_ASYNC_MINB
-#define TMG_ASYNC_MINB 5  // 5 CTAs (20 warps) per SM: fastest in the round-1 sweep
-#endif
-#if TMG_ASYNC_MINB > 0
-#define TMG_ASYNC_BOUNDS __launch_bounds__(128, TMG_ASYNC_MINB)
+constexpr int async_regs(int NW, int B) { return 2 * NW * B + 40 + 8 * NW + (B == 8 ? 0 : (B == 4 ? 16 : 24)); }
+constexpr int async_min_blocks(int NW, int B) {
+  return 65536 / (128 * async_regs(NW, B)) < 1 ? 1 : 65536 / (128 * async_regs(NW, B));
+}
+#define TMG_ASYNC_BOUNDS __launch_bounds__(128, async_min_blocks(NW, B))
 #else
-#define TMG_ASYNC_BOUNDS __launch_bounds__(128)
+#define TMG_ASYNC_BOUNDS __launch_bounds__(128, TMG_ASYNC_MINB)
 #endif
+template <int NW, int B, bool P2>
 __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -199,7 +221,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   const int64_t q = P.q;
   const int T = P.margin;
 
-  Clause<NW, B> cl;
+  Clause<NW, B, P2> cl;
   uint32_t* st = P.state + static_cast<size_t>(lc) * B * 2 * P.Wp;
   cl.load(st, P.Wp, lane, P.o);
   cl.refresh_nonempty();
@@ -241,6 +263,74 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
     if (!gm) continue;
     events += __popc(gm);
 
+#if TMG_ASYNC_V5
+    // ---- gated steps in order. Each lane owns the bookkeeping of its own
+    // step: it fetched the previous-output bit of its example above and
+    // publishes the new output after the window (record_output_and_tally,
+    // pool.cpp:93-106). Deferring the publish to the end of the 32 steps is a
+    // legal interleaving: a clause visits each example once per pass, so no
+    // step of this window reads a tally this window writes; other clauses'
+    // reads were never ordered with respect to it. The step loop is unrolled
+    // twice so the next step's literal words load into the idle buffer.
+    uint32_t prevbit = 0;
+    if (gated) prevbit = (__ldcg(prev_row + (i >> 5)) >> (i & 31)) & 1u;
+    const int code = target ? ~static_cast<int>(i) : static_cast<int>(i);  // q < 2^31: sign = Type I
+    unsigned outs = 0;  // bit l: output after the step lane l drew
+    uint32_t xa[NW], na[NW], xb[NW], nb[NW];
+    auto fetch = [&](uint32_t (&xs)[NW], uint32_t (&ns)[NW], int& cd, int& sl) {
+      sl = __ffs(gm) - 1;
+      gm &= gm - 1;
+      cd = __shfl_sync(kFull, code, sl);
+      const size_t row = static_cast<size_t>(cd < 0 ? ~cd : cd) * P.Wp + lane;
+#pragma unroll
+      for (int p = 0; p < NW; ++p) {
+        xs[p] = __ldg(P.xplane + row + p * 32);
+        ns[p] = __ldg(P.nplane + row + p * 32);
+      }
+    };
+    auto run = [&](const uint32_t (&xs)[NW], const uint32_t (&ns)[NW], int cd, int sl) {
+      const int before = cl.eval_cached(xs, ns);
+      int after = before;
+      if (cd >= 0) {
+        if (before && cl.type_ii(xs, ns)) after = cl.eval_train(xs, ns);
+      } else {
+        ++events_type1;
+        type_i_async<NW, B, P2>(cl, xs, ns, before, P, g, static_cast<uint32_t>(~cd), lane);
+        after = cl.eval_train(xs, ns);
+      }
+      outs |= static_cast<unsigned>(after) << sl;
+    };
+    int cda, sla, cdb, slb;
+    if (NW <= TMG_ASYNC_UNROLL_NW) {
+      // Two copies of the step body, no register moves between buffers.
+      fetch(xa, na, cda, sla);
+      while (true) {
+        const bool more_b = gm != 0;
+        if (more_b) fetch(xb, nb, cdb, slb);
+        run(xa, na, cda, sla);
+        if (!more_b) break;
+        const bool more_a = gm != 0;
+        if (more_a) fetch(xa, na, cda, sla);
+        run(xb, nb, cdb, slb);
+        if (!more_a) break;
+      }
+    } else {
+      // Wide rows: one copy of the (large) step body keeps the kernel inside
+      // the instruction cache; the row of the step is loaded at its start.
+      while (gm) {
+        fetch(xa, na, cda, sla);
+        run(xa, na, cda, sla);
+      }
+    }
+    if (gated && ((outs >> lane) & 1u) != prevbit) {
+      atomicXor(prev_row + (i >> 5), 1u << (i & 31));
+      int delta = prevbit ? -1 : 1;
+      if (!positive) delta = -delta;
+      const size_t ti = static_cast<size_t>(i) * P.m + c;
+      atomicAdd(&P.tallies[ti], delta);
+      if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
+    }
+#else
     // ---- gated steps in order; the next step's literal words are prefetched
     // while the current one is processed. The previous-output word is loaded
     // at the start of a step and only consumed after the feedback.
@@ -284,7 +374,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
       } else {
         ++events_type1;
-        type_i_async<NW, B>(cl, x, n, before, P, g, static_cast<uint32_t>(is), lane);
+        type_i_async<NW, B, P2>(cl, x, n, before, P, g, static_cast<uint32_t>(is), lane);
         after = cl.eval_train(x, n);
       }
       if (lane == 0) {
@@ -307,6 +397,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
         n[p] = n2[p];
       }
     }
+#endif
   }
   cl.store(st, P.Wp, lane);
   const int cnt = cl.include_count();
@@ -472,7 +563,7 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
     Clause<NW, B> cl, c0;
     cl.load(state0, P.Wp, lane, P.o);
     c0 = cl;
-    type_i_async<NW, B>(cl, x, n, out, P, 0u, trial, lane);
+    type_i_async<NW, B, false>(cl, x, n, out, P, 0u, trial, lane);
 #pragma unroll
     for (int p = 0; p < NW; ++p)
 #pragma unroll
@@ -499,6 +590,26 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
   }
 }
 
+// One asynchronous Type I feedback (type_i_async, exactly as the epoch kernel
+// applies it) on the clause planes at `state`, literal row 0 of P, Philox
+// counters (clause g, example i): the deterministic unit the async sampler's
+// bit-exact parity test checks against oracle/tm_oracle.c:tm_async_type_i.
+template <int NW, int B, bool P2>
+__global__ void __launch_bounds__(32) type_i_async_once_kernel(TrainParams P, uint32_t* state, uint32_t g,
+                                                               uint32_t i, int out) {
+  const int lane = threadIdx.x;
+  Clause<NW, B, P2> cl;
+  cl.load(state, P.Wp, lane, P.o);
+  uint32_t x[NW], n[NW];
+#pragma unroll
+  for (int p = 0; p < NW; ++p) {
+    x[p] = P.xplane[p * 32 + lane];
+    n[p] = P.nplane[p * 32 + lane];
+  }
+  type_i_async<NW, B, P2>(cl, x, n, out, P, g, i, lane);
+  cl.store(state, P.Wp, lane);
+}
+
 template <int NW, int B>
 void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
   const int clauses = p.m * p.n_loc;
@@ -506,7 +617,10 @@ void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
   const int grid = (clauses + warps_per_block - 1) / warps_per_block;
   if (blocks) *blocks = grid;
   count_launch();
-  train_async_kernel<NW, B><<<grid, 32 * warps_per_block, 0, s>>>(p);
+  if (TMG_ASYNC_P2 && p.lo == 0 && p.hi == (1u << B) - 1u)
+    train_async_kernel<NW, B, true><<<grid, 32 * warps_per_block, 0, s>>>(p);
+  else
+    train_async_kernel<NW, B, false><<<grid, 32 * warps_per_block, 0, s>>>(p);
 }
 
 template <int NW, int B>
@@ -558,6 +672,23 @@ bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out
   if (NW == 1 && B == 8) return go(feedback_rates_kernel<1, 8>);
   if (NW == 1 && B == 15) return go(feedback_rates_kernel<1, 15>);
   if (NW == 3 && B == 8) return go(feedback_rates_kernel<3, 8>);
+  return false;
+}
+
+bool type_i_async_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, uint32_t i, int out, int B, int NW,
+                              cudaStream_t s) {
+  const bool p2 = TMG_ASYNC_P2 && p.lo == 0 && p.hi == (1u << B) - 1u;
+  auto go = [&](auto kern) {
+    count_launch();
+    kern<<<1, 32, 0, s>>>(p, state, g, i, out);
+    return true;
+  };
+#define TMG_ONCE(nw, b)                                                            \
+  if (NW == nw && B == b)                                                          \
+    return p2 ? go(type_i_async_once_kernel<nw, b, true>) : go(type_i_async_once_kernel<nw, b, false>);
+  TMG_ONCE(1, 4) TMG_ONCE(1, 8) TMG_ONCE(1, 15) TMG_ONCE(2, 4) TMG_ONCE(2, 8) TMG_ONCE(2, 15)
+  TMG_ONCE(3, 4) TMG_ONCE(3, 8) TMG_ONCE(3, 15) TMG_ONCE(4, 4) TMG_ONCE(4, 8) TMG_ONCE(4, 15)
+#undef TMG_ONCE
   return false;
 }
 

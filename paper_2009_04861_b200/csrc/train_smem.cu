@@ -104,19 +104,25 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
       gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
     }
     unsigned gm = __ballot_sync(kFull, gated);
+    if (!gm) continue;
     events += __popc(gm);
+    // Lane-owned bookkeeping, published after the window (see train.cu).
+    uint32_t prevbit = 0;
+    if (gated) prevbit = (__ldcg(prev_row + (i >> 5)) >> (i & 31)) & 1u;
+    const int code = target ? ~static_cast<int>(i) : static_cast<int>(i);
+    unsigned outs = 0;
     while (gm) {
       const int sl = __ffs(gm) - 1;
       gm &= gm - 1;
-      const int64_t is = __shfl_sync(kFull, i, sl);
-      const int tg = __shfl_sync(kFull, target, sl);
+      const int cd = __shfl_sync(kFull, code, sl);
+      const int64_t is = cd < 0 ? ~cd : cd;
+      const int tg = cd < 0;
       uint32_t x[NW], n[NW];
 #pragma unroll
       for (int p = 0; p < NW; ++p) {
         x[p] = __ldg(P.xplane + is * Wp + p * 32 + lane);
         n[p] = __ldg(P.nplane + is * Wp + p * 32 + lane);
       }
-      const uint32_t pword = lane == 0 ? prev_row[is >> 5] : 0u;
       const int before = eval_train_smem<NW, B>(S, x, n, lane);
       int after = before;
       if (tg == 0) {  // Type II (feedback.cpp:72-83)
@@ -177,16 +183,15 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
         __syncwarp();
         after = eval_train_smem<NW, B>(S, x, n, lane);
       }
-      if (lane == 0) {
-        const uint32_t bit = 1u << (is & 31);
-        if (((pword & bit) != 0) != (after != 0)) {
-          prev_row[is >> 5] = pword ^ bit;
-          int delta = after ? 1 : -1;
-          if (!positive) delta = -delta;
-          atomicAdd(&P.tallies[is * P.m + c], delta);
-          if (P.tally_delta) atomicAdd(&P.tally_delta[is * P.m + c], delta);
-        }
-      }
+      outs |= static_cast<unsigned>(after) << sl;
+    }
+    if (gated && ((outs >> lane) & 1u) != prevbit) {
+      atomicXor(prev_row + (i >> 5), 1u << (i & 31));
+      int delta = prevbit ? -1 : 1;
+      if (!positive) delta = -delta;
+      const size_t ti = static_cast<size_t>(i) * P.m + c;
+      atomicAdd(&P.tallies[ti], delta);
+      if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
     }
   }
   __syncwarp();

@@ -443,6 +443,14 @@ def feedback_rates(bank: ClassBank, j: int, literals, clause_output: int, trials
     return inc, dec
 
 
+def type_i_async(bank: ClassBank, j: int, literals, clause_output: int, example: int, epoch: int):
+    """One asynchronous Type I feedback on clause j (the epoch kernel's Philox
+    sampler, counters (clause, example), key of `epoch`), applied in place."""
+    lits = _lits2d(bank._tm, literals)[:1].copy()
+    check(lib().tmg_debug_type_i_async(bank._tm.handle, bank._c, j, _ptr(lits), int(clause_output),
+                                       int(example) & 0xFFFFFFFF, int(epoch)))
+
+
 def evaluate_clause(bank: ClassBank, j: int, literals, mode: int) -> int:
     """evaluate_clause (core.hpp:208-219) on the GPU."""
     lits = _lits2d(bank._tm, literals)[:1].copy()

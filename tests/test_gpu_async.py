@@ -61,6 +61,30 @@ def test_async_epoch_invariants_mnist_shape():
     assert np.array_equal(T.predict_all(tm, test), ref.predict(lits))
 
 
+@pytest.mark.parametrize("kind,q,clauses,T_,s_", [("fmnist", 800, 40, 100, 15.0), ("imdb", 600, 24, 100, 15.0)])
+def test_async_epoch_invariants_wide_rows(kind, q, clauses, T_, s_):
+    """Register kernel at 3 words per lane (FMNIST shape) and the shared-memory
+    clause kernel (IMDb shape, 10 words per lane): tally invariant after every
+    epoch, counters in range, exact refresh and inference vs the oracle."""
+    d = synth.make(kind, q, 64, 7)
+    tm = T.MultiClassTM(T.TMConfig(clauses=clauses, margin=T_, specificity=s_, seed=5), d.features, d.classes)
+    pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes)
+    for e in range(2):
+        rep = T.train_epoch_parallel(tm, pool, 1, e)
+        assert 0 < sum(rep.type_i_events) < rep.total_feedback_events()
+        _check_tally_invariant(tm, pool, d.classes, q)
+    ref = O.Machine(d.features, d.classes, clauses, 128)
+    ref.set_counters(np.stack([tm.banks[c].counters() for c in range(d.classes)]))
+    assert ref.counters.min() >= 1 and ref.counters.max() <= 256
+    T.refresh_tallies(pool, tm)
+    rpool = O.Pool(d.train_x, d.train_y, d.classes)
+    O.refresh_tallies(ref, rpool)
+    assert np.array_equal(pool.tallies(), rpool.tallies)
+    test = T.ExamplePool(d.features, d.test_x, d.test_y, d.classes)
+    lits = O.pack_literals(d.test_x)
+    assert np.array_equal(T.class_sums(tm, test), ref.class_sums(lits))
+
+
 def test_async_window_accounting():
     """Windows of a pass compose to the full pass (multi-GPU building block)."""
     d = synth.make("xor", 1000, 10, 5, 0.1)
@@ -117,6 +141,44 @@ def test_type_i_table1_conformance(o, N, s, boost, out):
     sel = exp_dec > 0
     if sel.sum() > 20:
         assert abs(dec[sel].mean() - p_lo) < 0.003
+
+
+@pytest.mark.parametrize("o,N,s,boost", [(784, 128, 10.0, False), (784, 128, 10.0, True), (784, 100, 10.0, False),
+                                         (12, 128, 3.9, False), (40, 5, 2.0, True), (2352, 128, 15.0, False),
+                                         (1500, 300, 7.5, False), (2000, 128, 1.0, False)])
+def test_async_type_i_bit_exact(o, N, s, boost):
+    """The asynchronous Type I draw (Philox counters (clause, example) under the
+    epoch key, exact bit-serial Bernoulli, saturating steps) reproduced
+    counter-for-counter by its C restatement (oracle/tm_oracle_async.c), for
+    both clause outputs, on near-saturated and mid-range automata."""
+    from paper_2009_04861_b200.tsetlin import type_i_async
+    rng = np.random.default_rng(o * 7 + N)
+    n, m = 4, 2
+    tm = T.MultiClassTM(T.TMConfig(clauses=n, state_depth=N, specificity=s, boost_true_positive=boost, seed=77),
+                        o, m)
+    nw = tm.info().words_per_lane
+    L = 2 * o
+    for c in range(m):
+        cs = rng.integers(1, 2 * N + 1, size=(n, L))
+        ends = rng.random((n, L))
+        cs[ends < 0.15] = 1
+        cs[ends > 0.9] = 2 * N
+        tm.banks[c].set_counters(cs.astype(np.uint16))
+    for trial in range(12):
+        c, j = int(rng.integers(m)), int(rng.integers(n))
+        x = (rng.random(o) < 0.5).astype(np.uint8)
+        lits = O.pack_literals(x)[0]
+        out = int(trial % 2)
+        example, epoch = int(rng.integers(0, 1 << 31)), int(rng.integers(0, 50))
+        before = tm.banks[c].counters()
+        g = c * n + j
+        expect = O.async_type_i(before[j], lits, o, N, out, s, boost, g, example, 77, epoch, nw)
+        type_i_async(tm.banks[c], j, lits, out, example, epoch)
+        after = tm.banks[c].counters()
+        assert np.array_equal(after[j], expect), (trial, np.flatnonzero(after[j] != expect)[:10])
+        others = [k for k in range(n) if k != j]
+        assert np.array_equal(after[others], before[others])
+        assert (after[j] != before[j]).any() or s == 1.0
 
 
 def _ref_acc():

@@ -151,3 +151,28 @@ def test_inference_random_states(name, o, m, n):
     O.refresh_tallies(tm, pool)
     assert np.array_equal(pool.tallies, load("inference", f"{name}_tallies.npy"))
     assert np.array_equal(tm.prev, load("inference", f"{name}_prev.npy"))
+
+
+def test_philox_known_answers():
+    """The async engine's generator, restated in oracle/tm_oracle_async.c, on
+    the Random123 published known-answer vectors (kat_vectors, philox4x32 R=10)."""
+    assert list(O.philox4x32([0, 0, 0, 0], 0, 0, 10)) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    ff = 0xFFFFFFFF
+    assert list(O.philox4x32([ff] * 4, ff, ff, 10)) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    pi = [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344]
+    assert list(O.philox4x32(pi, 0xA4093822, 0x299F31D0, 10)) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_async_type_i_restatement_rates():
+    """The restated async draw feeds back at p_low = 1/s with clause output 0
+    (Table 1): pooled over many examples, within binomial noise."""
+    o, N, s = 64, 128, 10.0
+    counters = np.full(2 * o, 100, np.uint16)
+    lits = O.pack_literals(np.zeros(o, np.uint8))[0]
+    moved = 0
+    trials = 400
+    for i in range(trials):
+        after = O.async_type_i(counters, lits, o, N, 0, s, False, 5, i, 1, 0, 1)
+        moved += int((after != counters).sum())
+    rate = moved / (trials * 2 * o)
+    assert abs(rate - 0.1) < 0.006, rate
