@@ -138,6 +138,7 @@ def run_reference(args):
                    "clauses_per_class": N_CLAUSES, "T": MARGIN, "s": SPEC, "state_bits": 8},
         "examples_per_s": q_use / t,
         "feedback_events_per_step": statistics.mean(r["feedback_events"] for r in rows),
+        "feedback_events_per_s": statistics.mean(r["feedback_events"] for r in rows) / t,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"fresh-model epoch 0 on the first {q_use} of {Q_TRAIN} training rows, "
                                    f"train_epoch_parallel(workers={cores})"},
@@ -282,6 +283,7 @@ def run_ours(args):
                    "l2": "flushed (256 MB write) between timed steps; working set (prev bits 150 MB) > L2"},
         "examples_per_s": Q_TRAIN / (ms * 1e-3),
         "feedback_events_per_step": statistics.mean(events),
+        "feedback_events_per_s": statistics.mean(events) / (ms * 1e-3),
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -290,13 +292,20 @@ def run_ours(args):
         ops = algorithmic_ops(M_CLS * N_CLAUSES * Q_TRAIN, int(statistics.mean(events)),
                               int(statistics.mean(type1)))
         k = statistics.mean(kern_s)
-        traffic = None
-        tpath = os.path.join(REPO, "profiles", "train_async_dram_bytes.json")
-        if os.path.exists(tpath):
-            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        traffic, hw = None, None
+        tpath = os.path.join(REPO, "profiles", "train_async_ncu.json")
+        if os.path.exists(tpath):  # the committed ncu --set full summary of this kernel
+            prof = json.load(open(tpath))
+            traffic = prof.get("dram_bytes_per_launch")
+            hw = {k: prof.get(k) for k in ("pipe_alu_pct", "pipe_fmaheavy_pct", "issue_active_pct", "ipc_active",
+                                           "duration_ms", "source")}
         line["roofline"] = {"bound": "int-alu", "achieved": ops / k / 1e12, "peak": mixed_peak / 1e12,
                             "unit": "Tops/s", "frac": ops / k / mixed_peak, "traffic": traffic,
-                            "kernel": "train_async_kernel<1,8>", "kernel_ms": k * 1e3,
+                            "frac_note": "algorithmic ops (SURVEY 8(d) model) / kernel time; >1 = the sampler "
+                                         "draws fewer random words than the model charges (effective). "
+                                         "Hardware view: ncu ALU-pipe utilisation in 'ncu'",
+                            "ncu": hw,
+                            "kernel": "train_async_kernel<1,8,P2>", "kernel_ms": k * 1e3,
                             "kernel_share_of_step": k * 1e3 / ms,
                             "peak_source": "measured on this GPU by tmg_bench_int_peak (LOP3+IMAD issue); "
                                            f"LOP3-only {lop3_peak / 1e12:.2f} Tops/s",
@@ -315,6 +324,7 @@ def run_ours(args):
         t = rows[0]["seconds"]
         line["cpu_baseline"] = {"value": evals(q_use, N_CLAUSES) / t, "unit": UNIT, "cores": cores,
                                 "kind": "reference", "examples_per_s": q_use / t,
+                                "feedback_events_per_s": rows[0]["feedback_events"] / t,
                                 "sample": f"fresh-model epoch 0 on the first {q_use} of {Q_TRAIN} rows, "
                                           f"reference train_epoch_parallel(workers={cores}), "
                                           f"{rows[0]['feedback_events']} feedback events"}

@@ -109,6 +109,9 @@ int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, const uin
  * detail::type_i_with_output (feedback.cpp:32-70) under the async RNG. */
 int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
                            int32_t clause_output, uint32_t example, int32_t epoch);
+/* Instrumentation counters of a TMG_STATS build (zeros otherwise): copies
+ * `count` (<= 256) of them to `out`, then zeroes them if `reset`. */
+int tmg_debug_counters(tmg_machine* tm, uint64_t* out, int32_t count, int32_t reset);
 /* Integer-pipe roofline probe: LOP3-only and LOP3+IMAD thread-ops per second. */
 int tmg_bench_int_peak(int32_t device, double* lop3_ops_per_s, double* mixed_ops_per_s);
 

@@ -164,6 +164,7 @@ struct tmg_machine {
   DevBuf<int32_t> inc_count, nentries, sums;
   DevBuf<tmg::EvalEntry> entries;
   DevBuf<unsigned long long> events;
+  DevBuf<unsigned long long> dbg;  // instrumentation counters (TMG_STATS builds)
   DevBuf<uint16_t> scratch16;
   bool entries_dirty = true;
   // current async epoch
@@ -260,6 +261,8 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->nentries.alloc(cl);
     tm->entries.alloc(cl * tm->Wx);
     tm->events.alloc(2 * static_cast<size_t>(m));  // all events, then Type I events
+    tm->dbg.alloc(tmg::kDebugCounters);
+    CK(cudaMemsetAsync(tm->dbg.ptr, 0, tm->dbg.bytes(), tm->stream));
     bind(tm, 0);
     reset_state(tm);
   } catch (...) {
@@ -315,11 +318,19 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   }
   p.bern.hi_rest = p.thr_high & 0x00FFFFFFu;
   p.bern.lo_rest = p.thr_low & 0x00FFFFFFu;
+  p.bern.one = 1u;
   p.key0 = tm->key0;
   p.key1 = tm->key1;
+  for (int r = 0; r < tmg::kMaxPhiloxRounds; ++r) {
+    p.rkey[0][r] = tm->key0 + static_cast<uint32_t>(r) * 0x9E3779B9u;
+    p.rkey[1][r] = tm->key1 + static_cast<uint32_t>(r) * 0xBB67AE85u;
+  }
   p.t_begin = 0;
   p.t_end = pool->q;
   p.events = tm->events.ptr;
+#ifdef TMG_STATS
+  p.dbg = tm->dbg.ptr;
+#endif
   return p;
 }
 
@@ -499,6 +510,7 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   tm->sums.release();
   tm->entries.release();
   tm->events.release();
+  tm->dbg.release();
   tm->scratch16.release();
   if (tm->ev0) cudaEventDestroy(tm->ev0);
   if (tm->ev1) cudaEventDestroy(tm->ev1);
@@ -1062,6 +1074,17 @@ TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, con
     CK(cudaGetLastError());
     tm->entries_dirty = true;
     rebuild_entries(tm);
+    CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_debug_counters(tmg_machine* tm, uint64_t* out, int32_t count, int32_t reset) {
+  return guarded([&] {
+    M(tm);
+    if (count < 0 || count > tmg::kDebugCounters) fail(TMG_EINVAL, "counter count out of range");
+    DeviceGuard dg(tm->device);
+    if (count) CK(cudaMemcpyAsync(out, tm->dbg.ptr, count * 8, cudaMemcpyDeviceToHost, tm->stream));
+    if (reset) CK(cudaMemsetAsync(tm->dbg.ptr, 0, tm->dbg.bytes(), tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
   });
 }

@@ -17,7 +17,10 @@ inline void count_launch() { __atomic_fetch_add(&g_launches, 1ULL, __ATOMIC_RELA
 struct BernThresholds {
   uint32_t hi_mask[8], lo_mask[8];
   uint32_t hi_rest, lo_rest;
+  uint32_t one;  // 1, opaque to the compiler (IMAD-as-add in the sampler)
 };
+
+constexpr int kMaxPhiloxRounds = 10;
 
 // Device view of one machine shard + pool, shared by all training kernels.
 struct TrainParams {
@@ -46,9 +49,15 @@ struct TrainParams {
   uint32_t thr_high, thr_low;  // async: P(u < p) thresholds as 32-bit fixed point
   BernThresholds bern;         // the same, split for the sampler
   uint32_t key0, key1;         // async: Philox key for (seed, epoch)
+  // The same key's round schedule (key0 + r*0x9E3779B9, key1 + r*0xBB67AE85),
+  // precomputed so the rounds read it from the constant bank, not registers.
+  uint32_t rkey[2][kMaxPhiloxRounds];
   int64_t t_begin, t_end;      // async: window of each clause's pass
   unsigned long long* events;  // [2m]: feedback events per class, then Type I events per class
+  unsigned long long* dbg;     // [kDebugCounters] instrumentation (TMG_STATS builds), else null
 };
+
+constexpr int kDebugCounters = 256;
 
 struct MirrorJob {
   int32_t c, j;  // class, global clause index

@@ -31,6 +31,11 @@ constexpr unsigned kFull = 0xffffffffu;
 #define TMG_PHILOX_ROUNDS 7
 #endif
 
+// Phase-1 "less" accumulation as IMAD (FMA pipe) instead of LOP3 (ALU pipe).
+#ifndef TMG_SAMPLER_IMAD
+#define TMG_SAMPLER_IMAD 1
+#endif
+
 // ---------------------------------------------------------------- Philox ---
 // Keyed per (seed, epoch); counters carry (clause, example, literal word,
 // draw block).
@@ -48,6 +53,22 @@ __device__ __forceinline__ U4 philox4x32(U4 c, uint32_t k0, uint32_t k1) {
     c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// The same block with the key schedule read from `rk` (TrainParams::rkey,
+// kernel-parameter space): the per-round XOR takes its key straight from the
+// constant bank instead of holding 2 x rounds key registers live.
+__device__ __forceinline__ U4 philox4x32(U4 c, const uint32_t (&rk)[2][kMaxPhiloxRounds]) {
+  static_assert(TMG_PHILOX_ROUNDS <= kMaxPhiloxRounds, "round schedule too short");
+#pragma unroll
+  for (int r = 0; r < TMG_PHILOX_ROUNDS; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x;
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = U4{hi1 ^ c.y ^ rk[0][r], lo1, hi0 ^ c.w ^ rk[1][r], lo0};
   }
   return c;
 }
@@ -73,6 +94,13 @@ struct Xoshiro {
     return static_cast<double>(next() >> 11) * 0x1.0p-53;
   }
 };
+
+// a * b + c on the FMA pipe (IMAD), for ALU-pipe relief.
+__device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
 
 // ---------------------------------------------------------- bit-sliced ops ---
 // Per-lane view of one clause part (x or !x) word: B planes.
@@ -203,7 +231,14 @@ __device__ __forceinline__ void bernoulli_words(const uint32_t (&need)[K], const
       for (int k = 0; k < K; ++k) {
         const uint32_t rb = i == 0 ? r[k].x : (i == 1 ? r[k].y : (i == 2 ? r[k].z : r[k].w));
         const uint32_t pk = SEL ? ((sel[k] & ph) | (~sel[k] & pl)) : pl;
+#if TMG_SAMPLER_IMAD
+        // The literals decided "less" this round are disjoint from `less`, so
+        // the OR is an add; as an IMAD with the opaque unit th.one it issues
+        // on the FMA pipe and leaves the (binding) ALU pipe two LOP3 a round.
+        less[k] = mad_u32(und[k] & ~rb & pk, th.one, less[k]);
+#else
         less[k] |= und[k] & ~rb & pk;
+#endif
         und[k] &= ~(rb ^ pk);
       }
     }

@@ -185,8 +185,34 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32
   auto gen = [&](int slot, int blk) {
     const uint32_t wid = slot < K ? static_cast<uint32_t>(((slot >> 1) * 32 + lane) * 2 + (slot & 1))
                                   : (0xFFFF0000u | static_cast<uint32_t>(lane));
-    return philox4x32(U4{g, i, wid, static_cast<uint32_t>(blk)}, P.key0, P.key1);
+    return philox4x32(U4{g, i, wid, static_cast<uint32_t>(blk)}, P.rkey);
   };
+#ifdef TMG_STATS
+  if (P.dbg) {
+    // Draws whose outcome cannot move the automaton (a step into the
+    // saturated end it already sits at): histogram of the warp maximum per
+    // lane and the warp total, per clause output (tools/draw_stats.py).
+    int cnt = 0;
+#pragma unroll
+    for (int p = 0; p < NW; ++p)
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const Planes<B>& w = cl.s[part][p];
+        const uint32_t lit = part ? n[p] : x[p];
+        const uint32_t at_lo = eq_const<B>(w, P.lo), at_hi = eq_const<B>(w, P.hi), incl = w.p[B - 1];
+        const uint32_t rel = before ? ((lit & ~at_hi) | (~lit & ~incl & ~at_lo)) : ~at_lo;
+        cnt += __popc(rel & cl.valid[p]);
+      }
+    const int mx = __reduce_max_sync(kFull, cnt), sum = __reduce_add_sync(kFull, cnt);
+    if (lane == 0) {
+      unsigned long long* d = P.dbg + (before ? 128 : 0);
+      atomicAdd(d + min(mx, 63), 1ULL);
+      atomicAdd(d + 64, 1ULL);
+      atomicAdd(d + 65, static_cast<unsigned long long>(sum));
+      atomicAdd(d + 66, static_cast<unsigned long long>(mx));
+    }
+  }
+#endif
   if (before) bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
   else bernoulli_words<K, false>(need, sel, P.bern, bern, gen);
 #pragma unroll
@@ -255,7 +281,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
         e = y ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
         target = (y == 1) == positive ? 1 : 0;
       }
-      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
+      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.rkey);
       // u < e / 2T  <=>  r * 2T < e * 2^32  (exact integer gate, feedback.cpp:24-28)
       gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
     }

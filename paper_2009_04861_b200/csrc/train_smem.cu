@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
         e = y ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
         target = (y == 1) == positive ? 1 : 0;
       }
-      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.key0, P.key1);
+      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.rkey);
       gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
     }
     unsigned gm = __ballot_sync(kFull, gated);
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
           auto gen = [&](int slot, int blk) {
             const uint32_t wid = slot < 2 ? static_cast<uint32_t>(w * 2 + slot)
                                           : (0xFFFF0000u | static_cast<uint32_t>(p * 32 + lane));
-            return philox4x32(U4{g, i32, wid, static_cast<uint32_t>(blk)}, P.key0, P.key1);
+            return philox4x32(U4{g, i32, wid, static_cast<uint32_t>(blk)}, P.rkey);
           };
           if (before) bernoulli_words<2, true>(need, sel, P.bern, bern, gen);
           else bernoulli_words<2, false>(need, sel, P.bern, bern, gen);
