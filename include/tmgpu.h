@@ -112,6 +112,10 @@ int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, const uint6
 /* Instrumentation counters of a TMG_STATS build (zeros otherwise): copies
  * `count` (<= 256) of them to `out`, then zeroes them if `reset`. */
 int tmg_debug_counters(tmg_machine* tm, uint64_t* out, int32_t count, int32_t reset);
+/* The async engine's alias table for the clause-output-0 Type I draw: 256
+ * entries (threshold24 << 8 | alias) of the law of 8 independent literals
+ * firing with probability threshold / 2^32 (host-side, no GPU needed). */
+int tmg_alias8_table(uint32_t threshold, uint32_t* out);
 /* Integer-pipe roofline probe: LOP3-only and LOP3+IMAD thread-ops per second. */
 int tmg_bench_int_peak(int32_t device, double* lop3_ops_per_s, double* mixed_ops_per_s);
 

@@ -90,7 +90,9 @@ def lib():
         L.orc_philox4x32.argtypes = [P, C.c_uint32, C.c_uint32, C.c_int, P]
         L.orc_async_key.argtypes = [C.c_uint64, C.c_int32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
         L.orc_async_type_i.argtypes = [P, P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_int32,
-                                       C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int32, C.c_int32]
+                                       C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int32, C.c_int32, P]
+        L.orc_prob_threshold.argtypes = [C.c_double]
+        L.orc_prob_threshold.restype = C.c_uint32
         _lib = L
     return _lib
 
@@ -301,12 +303,35 @@ def async_key(seed: int, epoch: int):
     return int(k0.value), int(k1.value)
 
 
+def prob_threshold(p: float) -> int:
+    """P(u < p) as a 32-bit fixed-point threshold (the async engine's)."""
+    return int(lib().orc_prob_threshold(p))
+
+
 def async_type_i(counters_row: np.ndarray, lits_row: np.ndarray, o: int, N: int, out: int, s: float,
-                 boost: bool, g: int, i: int, seed: int, epoch: int, nw: int, rounds: int = 7) -> np.ndarray:
-    """One async-engine Type I feedback on one clause's 2o counters (copy)."""
+                 boost: bool, g: int, i: int, seed: int, epoch: int, nw: int, rounds: int = 7,
+                 alias8=None) -> np.ndarray:
+    """One async-engine Type I feedback on one clause's 2o counters (copy).
+    alias8: the engine's 256-entry table for clause output 0 (None: bit-serial)."""
     row = np.ascontiguousarray(counters_row, np.uint16).copy()
     lits = np.ascontiguousarray(lits_row, np.uint64)
     k0, k1 = async_key(seed, epoch)
+    tab = None if alias8 is None else np.ascontiguousarray(alias8, np.uint32)
     lib().orc_async_type_i(_ptr(row), _ptr(lits), o, N, int(out), float(s), int(bool(boost)), g, i, k0, k1,
-                           nw, rounds)
+                           nw, rounds, None if tab is None else _ptr(tab))
     return row
+
+
+def alias8_law(table: np.ndarray) -> np.ndarray:
+    """Pattern law (256 probabilities) implied by an alias table as the
+    engine samples it: column u & 0xFF, own pattern iff (u|0xFF) < entry."""
+    law = np.zeros(256)
+    for col in range(256):
+        e = int(table[col])
+        if (e & 0xFF) == col and (e >> 8) == 0:
+            law[col] += 1.0 / 256
+            continue
+        t = (e >> 8) / 2.0 ** 24
+        law[col] += t / 256
+        law[e & 0xFF] += (1.0 - t) / 256
+    return law

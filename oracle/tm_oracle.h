@@ -89,6 +89,6 @@ void orc_async_key(uint64_t seed, int32_t epoch, uint32_t* key0, uint32_t* key1)
 uint32_t orc_prob_threshold(double p);
 void orc_async_type_i(uint16_t* counters, const uint64_t* lits, int32_t o, int32_t N, int32_t out, double s,
                       int32_t boost, uint32_t g, uint32_t i, uint32_t key0, uint32_t key1, int32_t nw,
-                      int32_t rounds);
+                      int32_t rounds, const uint32_t* alias8);
 
 #endif

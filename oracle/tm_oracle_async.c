@@ -26,6 +26,8 @@
  *   out=1, lit=1: +1 w.p. p_high (always if boost and included)
  *   out=1, lit=0: +1 if included / -1 if excluded, w.p. p_low
  *   out=0       : -1 w.p. p_low
+ * With out=0 and an alias table the engine draws whole 8-literal patterns
+ * instead (see orc_async_type_i below and tm_device.cuh alias_words).
  */
 #include <math.h>
 #include <stdint.h>
@@ -72,8 +74,63 @@ static int lit_bit(const uint64_t* w, int k) { return (int)((w[k >> 6] >> (k & 6
 
 void orc_async_type_i(uint16_t* counters, const uint64_t* lits, int32_t o, int32_t N, int32_t out, double s,
                       int32_t boost, uint32_t g, uint32_t i, uint32_t key0, uint32_t key1, int32_t nw,
-                      int32_t rounds) {
+                      int32_t rounds, const uint32_t* alias8) {
   const int L = 2 * o;
+  const uint32_t p_high0 = orc_prob_threshold((s - 1.0) / s), p_low0 = orc_prob_threshold(1.0 / s);
+  const int alias_sel = (uint64_t)p_high0 + p_low0 == ((uint64_t)1 << 32);
+  if (out && alias8 && alias_sel) {
+    /* Clause output 1 with p_high = 1 - p_low exactly: the same alias
+     * patterns, negated on the true literals (tm_device.cuh / train.cu). */
+    for (int part = 0; part < 2; ++part)
+      for (int wi = 0; wi * 32 < o; ++wi) {
+        const uint32_t ctr[4] = {g, i, (uint32_t)(2 * wi + part), 0u};
+        uint32_t blk[4];
+        orc_philox4x32(ctr, key0, key1, rounds, blk);
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t u = blk[j], e = alias8[u & 0xFFu];
+          const uint32_t pattern = ((u | 0xFFu) < e ? u : e) & 0xFFu;
+          for (int b = 0; b < 8; ++b) {
+            const int f = wi * 32 + j * 8 + b;
+            if (f >= o) continue;
+            const int k = part * o + f, lit = lit_bit(lits, k);
+            const int fire = (int)((pattern >> b) & 1u) ^ lit;
+            const int included = counters[k] > N;
+            int v = counters[k];
+            if (lit) {
+              if (fire || (boost && included)) v += 1;
+            } else if (fire) {
+              v += included ? 1 : -1;
+            }
+            if (v < 1) v = 1;
+            if (v > 2 * N) v = 2 * N;
+            counters[k] = (uint16_t)v;
+          }
+        }
+      }
+    return;
+  }
+  if (!out && alias8) {
+    /* Clause output 0: each aligned 8-literal group of word slot (wi, part)
+     * draws its pattern with byte j's uniform u = word j of Philox(g, i,
+     * 2*wi + part, 0) from the alias table (tm_device.cuh alias_words). */
+    for (int part = 0; part < 2; ++part)
+      for (int wi = 0; wi * 32 < o; ++wi) {
+        const uint32_t ctr[4] = {g, i, (uint32_t)(2 * wi + part), 0u};
+        uint32_t blk[4];
+        orc_philox4x32(ctr, key0, key1, rounds, blk);
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t u = blk[j], e = alias8[u & 0xFFu];
+          const uint32_t pattern = ((u | 0xFFu) < e ? u : e) & 0xFFu;
+          for (int b = 0; b < 8; ++b) {
+            const int f = wi * 32 + j * 8 + b;
+            if (f >= o || !((pattern >> b) & 1u)) continue;
+            const int k = part * o + f;
+            if (counters[k] > 1) counters[k] -= 1; /* -1 w.p. p_low, saturating at 1 */
+          }
+        }
+      }
+    return;
+  }
   const uint32_t p_high = orc_prob_threshold((s - 1.0) / s), p_low = orc_prob_threshold(1.0 / s);
   const int K = 2 * nw, nb = (K + 3) / 4;
   uint8_t* bern = (uint8_t*)malloc((size_t)L);

@@ -140,6 +140,53 @@ uint32_t prob_threshold(double p) {  // P(u < p) as 32-bit fixed point
   return static_cast<uint32_t>(std::llround(v));
 }
 
+// Walker/Vose alias table of the law of an 8-literal Type I pattern when
+// every literal fires independently with probability p = P / 2^32 (the
+// clause-output-0 draw of the async sampler, tm_device.cuh alias_words).
+// Built exactly in integer units of 2^-32: each pattern's mass is its
+// product-law probability rounded by largest remainders (error < 2^-32,
+// total exactly 1), 256 columns of 2^24 units, so the sampled law equals
+// the rounded masses exactly. Entry = threshold24 << 8 | alias; a column
+// whose own pattern always wins is stored as (0 << 8 | itself).
+void build_alias8(uint32_t P, uint32_t out[256]) {
+  const double p = std::ldexp(static_cast<double>(P), -32);
+  int64_t mass[256];
+  double frac[256];
+  int64_t total = 0;
+  for (int i = 0; i < 256; ++i) {
+    const int k = __builtin_popcount(static_cast<unsigned>(i));
+    const double units = std::ldexp(std::pow(p, k) * std::pow(1.0 - p, 8 - k), 32);
+    mass[i] = static_cast<int64_t>(std::floor(units));
+    frac[i] = units - static_cast<double>(mass[i]);
+    total += mass[i];
+  }
+  int order[256];
+  for (int i = 0; i < 256; ++i) order[i] = i;
+  std::stable_sort(order, order + 256, [&](int a, int b) { return frac[a] > frac[b]; });
+  for (int r = 0; total < (int64_t(1) << 32); ++r, ++total) ++mass[order[r % 256]];
+  for (int r = 255; total > (int64_t(1) << 32); --r, --total)  // (float slack only)
+    if (mass[order[r]] > 0) --mass[order[r]];
+  constexpr int64_t kCol = int64_t(1) << 24;
+  int alias[256];
+  int64_t thr[256];
+  int small[256], large[256], ns = 0, nl = 0;
+  for (int i = 0; i < 256; ++i) {
+    alias[i] = i;
+    thr[i] = kCol;
+    (mass[i] < kCol ? small[ns++] : large[nl++]) = i;
+  }
+  while (ns > 0 && nl > 0) {
+    const int a = small[--ns], b = large[--nl];
+    thr[a] = mass[a];
+    alias[a] = b;
+    mass[b] -= kCol - mass[a];
+    (mass[b] < kCol ? small[ns++] : large[nl++]) = b;
+  }
+  for (int i = 0; i < 256; ++i)
+    out[i] = (alias[i] == i || thr[i] >= kCol) ? static_cast<uint32_t>(i)
+                                               : (static_cast<uint32_t>(thr[i]) << 8) | static_cast<uint32_t>(alias[i]);
+}
+
 }  // namespace
 
 struct tmg_pool {
@@ -165,6 +212,7 @@ struct tmg_machine {
   DevBuf<tmg::EvalEntry> entries;
   DevBuf<unsigned long long> events;
   DevBuf<unsigned long long> dbg;  // instrumentation counters (TMG_STATS builds)
+  DevBuf<uint32_t> alias8;         // alias table of the clause-output-0 Type I draw
   DevBuf<uint16_t> scratch16;
   bool entries_dirty = true;
   // current async epoch
@@ -263,6 +311,12 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->events.alloc(2 * static_cast<size_t>(m));  // all events, then Type I events
     tm->dbg.alloc(tmg::kDebugCounters);
     CK(cudaMemsetAsync(tm->dbg.ptr, 0, tm->dbg.bytes(), tm->stream));
+    {
+      uint32_t tab[256];
+      build_alias8(prob_threshold(1.0 / cfg->specificity), tab);
+      tm->alias8.alloc(256);
+      CK(cudaMemcpy(tm->alias8.ptr, tab, sizeof tab, cudaMemcpyHostToDevice));
+    }
     bind(tm, 0);
     reset_state(tm);
   } catch (...) {
@@ -328,6 +382,8 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   p.t_begin = 0;
   p.t_end = pool->q;
   p.events = tm->events.ptr;
+  p.alias8 = tm->alias8.ptr;
+  p.alias_sel = (static_cast<uint64_t>(p.thr_high) + p.thr_low == (uint64_t(1) << 32)) ? 1 : 0;
 #ifdef TMG_STATS
   p.dbg = tm->dbg.ptr;
 #endif
@@ -511,6 +567,7 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   tm->entries.release();
   tm->events.release();
   tm->dbg.release();
+  tm->alias8.release();
   tm->scratch16.release();
   if (tm->ev0) cudaEventDestroy(tm->ev0);
   if (tm->ev1) cudaEventDestroy(tm->ev1);
@@ -1086,6 +1143,13 @@ TMG_API int tmg_debug_counters(tmg_machine* tm, uint64_t* out, int32_t count, in
     if (count) CK(cudaMemcpyAsync(out, tm->dbg.ptr, count * 8, cudaMemcpyDeviceToHost, tm->stream));
     if (reset) CK(cudaMemsetAsync(tm->dbg.ptr, 0, tm->dbg.bytes(), tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
+  });
+}
+
+TMG_API int tmg_alias8_table(uint32_t threshold, uint32_t* out) {
+  return guarded([&] {
+    if (!out) fail(TMG_EINVAL, "null output");
+    build_alias8(threshold, out);
   });
 }
 

@@ -48,6 +48,8 @@ struct TrainParams {
   int32_t all_positive;
   uint32_t thr_high, thr_low;  // async: P(u < p) thresholds as 32-bit fixed point
   BernThresholds bern;         // the same, split for the sampler
+  const uint32_t* alias8;      // [256] alias table of Bernoulli(thr_low/2^32)^8 (threshold<<8 | alias)
+  int32_t alias_sel;           // thr_high + thr_low == 2^32: clause-output-1 draws use the table too
   uint32_t key0, key1;         // async: Philox key for (seed, epoch)
   // The same key's round schedule (key0 + r*0x9E3779B9, key1 + r*0xBB67AE85),
   // precomputed so the rounds read it from the constant bank, not registers.

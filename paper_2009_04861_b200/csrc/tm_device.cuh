@@ -192,6 +192,37 @@ __device__ __forceinline__ void add_one_sat1(Planes<B>& s, uint32_t inc) {
   for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
 }
 
+// Alias-table sampler for the Type I draws of a clause with output 0, where
+// every literal independently takes its step with the same p = P_low / 2^32
+// (feedback.cpp:66-68). Each aligned group of 8 literals draws its whole
+// 8-bit pattern from the product law Bernoulli(p)^8 with one 32-bit uniform
+// u and Walker's alias method: column = u & 0xFF, and the column's own
+// pattern wins iff (u >> 8) < its 24-bit threshold, else its alias
+// (entry = threshold << 8 | alias; (u | 0xFF) < entry is that test).
+// Pattern probabilities are within 2^-32 of the product law (masses rounded
+// to 2^-32 units, engine.cu build_alias8), each literal's within 2^-25 of p. One Philox block = the 32 literals of a word slot;
+// `tab` holds kAliasCopies interleaved copies of the 256 entries so the 32
+// lanes' random lookups hit at most two shared-memory wavefronts.
+constexpr int kAliasCopies = 16;
+
+template <int K, typename Gen>
+__device__ __forceinline__ void alias_words(const uint32_t (&need)[K], const uint32_t* tab, uint32_t laneoff,
+                                            uint32_t (&bern)[K], Gen&& gen) {
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const U4 r = gen(k, 0);
+    uint32_t b[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t u = j == 0 ? r.x : (j == 1 ? r.y : (j == 2 ? r.z : r.w));
+      const uint32_t e = tab[((u & 0xFFu) * kAliasCopies) | laneoff];
+      b[j] = (u | 0xFFu) < e ? u : e;  // low byte: the drawn pattern
+    }
+    const uint32_t lo = __byte_perm(b[0], b[1], 0x0040), hi = __byte_perm(b[2], b[3], 0x0040);
+    bern[k] = __byte_perm(lo, hi, 0x5410) & need[k];
+  }
+}
+
 // Warp-cooperative exact Bernoulli masks for one Type I event: every lane
 // owns K words of literals; bit b of word k is wanted with probability
 // P / 2^32 where P = P_high if bit b of sel[k] else P_low (SEL=false: always

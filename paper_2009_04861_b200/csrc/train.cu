@@ -24,6 +24,9 @@
 #ifndef TMG_ASYNC_UNROLL_NW
 #define TMG_ASYNC_UNROLL_NW 1  // widest rows (words per lane) that get the 2x unrolled step loop
 #endif
+#ifndef TMG_ALIAS
+#define TMG_ALIAS 1  // alias-table sampler for clause-output-0 Type I draws
+#endif
 #ifndef TMG_ASYNC_V5
 #define TMG_ASYNC_V5 1  // window-deferred record + 2x unrolled step loop
 #endif
@@ -173,7 +176,7 @@ __device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row,
 template <int NW, int B, bool P2>
 __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
                                              int before, const TrainParams& P, uint32_t g, uint32_t i,
-                                             int lane) {
+                                             int lane, const uint32_t* atab) {
   constexpr int K = 2 * NW;
   uint32_t need[K], sel[K], bern[K];
 #pragma unroll
@@ -213,13 +216,37 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32
     }
   }
 #endif
+#if TMG_ALIAS
+  if (before && !P.alias_sel) {
+    bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
+  } else {
+    alias_words<K>(need, atab, static_cast<uint32_t>(lane) & (kAliasCopies - 1), bern, gen);
+    // Clause output 1: a true literal fires w.p. p_high = 1 - p_low, a false
+    // one w.p. p_low, so one Bernoulli(p_low) bit serves either, negated on
+    // the true literals (independence across literals is untouched).
+    if (before) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) bern[k] = (bern[k] ^ sel[k]) & need[k];
+    }
+  }
+#else
   if (before) bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
   else bernoulli_words<K, false>(need, sel, P.bern, bern, gen);
+#endif
 #pragma unroll
   for (int p = 0; p < NW; ++p) {
     cl.type_i_word(0, p, x[p], before, P.boost, bern[2 * p], P.lo, P.hi);
     cl.type_i_word(1, p, n[p], before, P.boost, bern[2 * p + 1], P.lo, P.hi);
   }
+}
+
+// Copies the machine's alias table (P.alias8, 256 entries) into kAliasCopies
+// interleaved shared-memory copies; every thread of the CTA takes part.
+__device__ __forceinline__ void load_alias(const TrainParams& P, uint32_t* tab) {
+#if TMG_ALIAS
+  for (int k = threadIdx.x; k < 256 * kAliasCopies; k += blockDim.x) tab[k] = __ldg(P.alias8 + k / kAliasCopies);
+  __syncthreads();
+#endif
 }
 
 // Resident CTAs (4 warps each) per SM for one instantiation: as many as the
@@ -237,6 +264,8 @@ constexpr int async_min_blocks(int NW, int B) {
 #endif
 template <int NW, int B, bool P2>
 __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
+  __shared__ uint32_t atab[TMG_ALIAS ? 256 * kAliasCopies : 1];
+  load_alias(P, atab);
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= P.m * P.n_loc) return;
@@ -321,7 +350,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
         if (before && cl.type_ii(xs, ns)) after = cl.eval_train(xs, ns);
       } else {
         ++events_type1;
-        type_i_async<NW, B, P2>(cl, xs, ns, before, P, g, static_cast<uint32_t>(~cd), lane);
+        type_i_async<NW, B, P2>(cl, xs, ns, before, P, g, static_cast<uint32_t>(~cd), lane, atab);
         after = cl.eval_train(xs, ns);
       }
       outs |= static_cast<unsigned>(after) << sl;
@@ -400,7 +429,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
       } else {
         ++events_type1;
-        type_i_async<NW, B, P2>(cl, x, n, before, P, g, static_cast<uint32_t>(is), lane);
+        type_i_async<NW, B, P2>(cl, x, n, before, P, g, static_cast<uint32_t>(is), lane, atab);
         after = cl.eval_train(x, n);
       }
       if (lane == 0) {
@@ -576,6 +605,8 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
                                                              int out, uint32_t trials,
                                                              unsigned long long* inc_cnt,
                                                              unsigned long long* dec_cnt) {
+  __shared__ uint32_t atab[TMG_ALIAS ? 256 * kAliasCopies : 1];
+  load_alias(P, atab);
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -589,7 +620,7 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
     Clause<NW, B> cl, c0;
     cl.load(state0, P.Wp, lane, P.o);
     c0 = cl;
-    type_i_async<NW, B, false>(cl, x, n, out, P, 0u, trial, lane);
+    type_i_async<NW, B, false>(cl, x, n, out, P, 0u, trial, lane, atab);
 #pragma unroll
     for (int p = 0; p < NW; ++p)
 #pragma unroll
@@ -623,6 +654,8 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
 template <int NW, int B, bool P2>
 __global__ void __launch_bounds__(32) type_i_async_once_kernel(TrainParams P, uint32_t* state, uint32_t g,
                                                                uint32_t i, int out) {
+  __shared__ uint32_t atab[TMG_ALIAS ? 256 * kAliasCopies : 1];
+  load_alias(P, atab);
   const int lane = threadIdx.x;
   Clause<NW, B, P2> cl;
   cl.load(state, P.Wp, lane, P.o);
@@ -632,7 +665,7 @@ __global__ void __launch_bounds__(32) type_i_async_once_kernel(TrainParams P, ui
     x[p] = P.xplane[p * 32 + lane];
     n[p] = P.nplane[p * 32 + lane];
   }
-  type_i_async<NW, B, P2>(cl, x, n, out, P, g, i, lane);
+  type_i_async<NW, B, P2>(cl, x, n, out, P, g, i, lane, atab);
   cl.store(state, P.Wp, lane);
 }
 

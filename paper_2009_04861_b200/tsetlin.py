@@ -451,6 +451,14 @@ def type_i_async(bank: ClassBank, j: int, literals, clause_output: int, example:
                                        int(example) & 0xFFFFFFFF, int(epoch)))
 
 
+def alias8_table(threshold: int) -> np.ndarray:
+    """The engine's 256-entry alias table for clause-output-0 Type I draws at
+    feed-back probability threshold / 2^32 (host computation)."""
+    out = np.zeros(256, np.uint32)
+    check(lib().tmg_alias8_table(int(threshold) & 0xFFFFFFFF, _ptr(out)))
+    return out
+
+
 def evaluate_clause(bank: ClassBank, j: int, literals, mode: int) -> int:
     """evaluate_clause (core.hpp:208-219) on the GPU."""
     lits = _lits2d(bank._tm, literals)[:1].copy()

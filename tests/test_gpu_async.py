@@ -151,8 +151,9 @@ def test_async_type_i_bit_exact(o, N, s, boost):
     epoch key, exact bit-serial Bernoulli, saturating steps) reproduced
     counter-for-counter by its C restatement (oracle/tm_oracle_async.c), for
     both clause outputs, on near-saturated and mid-range automata."""
-    from paper_2009_04861_b200.tsetlin import type_i_async
+    from paper_2009_04861_b200.tsetlin import alias8_table, type_i_async
     rng = np.random.default_rng(o * 7 + N)
+    table = alias8_table(O.prob_threshold(1.0 / s))
     n, m = 4, 2
     tm = T.MultiClassTM(T.TMConfig(clauses=n, state_depth=N, specificity=s, boost_true_positive=boost, seed=77),
                         o, m)
@@ -172,7 +173,7 @@ def test_async_type_i_bit_exact(o, N, s, boost):
         example, epoch = int(rng.integers(0, 1 << 31)), int(rng.integers(0, 50))
         before = tm.banks[c].counters()
         g = c * n + j
-        expect = O.async_type_i(before[j], lits, o, N, out, s, boost, g, example, 77, epoch, nw)
+        expect = O.async_type_i(before[j], lits, o, N, out, s, boost, g, example, 77, epoch, nw, alias8=table)
         type_i_async(tm.banks[c], j, lits, out, example, epoch)
         after = tm.banks[c].counters()
         assert np.array_equal(after[j], expect), (trial, np.flatnonzero(after[j] != expect)[:10])
