@@ -104,8 +104,8 @@ int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, const uin
 /* One asynchronous Type I feedback (the epoch kernel's type_i_async: Philox
  * key of `epoch`, counters (global clause g = bank*clauses + j, example)) applied
  * in place to clause j of `bank` on one literal row (reference layout) with the
- * given clause output. Deterministic; register-resident shapes only
- * (feature_count <= 4096). Replaces one draw-for-draw call of
+ * given clause output. Deterministic; register-resident shapes (feature_count
+ * <= 4096) and the shared-memory path of wider rows. Replaces one call of
  * detail::type_i_with_output (feedback.cpp:32-70) under the async RNG. */
 int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
                            int32_t clause_output, uint32_t example, int32_t epoch);

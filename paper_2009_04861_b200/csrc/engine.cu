@@ -1125,8 +1125,13 @@ TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, con
     p.nplane = ns.ptr;
     const size_t lc = static_cast<size_t>(bank) * tm->n_loc + (j - tm->j_begin);
     const uint32_t g = static_cast<uint32_t>(bank) * tm->n + j;
-    if (!tmg::type_i_async_once_launch(p, tm->state.ptr + lc * tm->B * 2 * tm->Wp, g, example,
-                                       clause_output ? 1 : 0, tm->B, tm->NW, tm->stream))
+    uint32_t* st = tm->state.ptr + lc * tm->B * 2 * tm->Wp;
+    const bool ok = tm->NW <= 4
+                        ? tmg::type_i_async_once_launch(p, st, g, example, clause_output ? 1 : 0, tm->B, tm->NW,
+                                                        tm->stream)
+                        : tmg::type_i_smem_once_launch(p, st, g, example, clause_output ? 1 : 0, tm->B, tm->NW,
+                                                       tm->stream);
+    if (!ok)
       fail(TMG_EINVAL, "async Type I probe not instantiated for this shape");
     CK(cudaGetLastError());
     tm->entries_dirty = true;

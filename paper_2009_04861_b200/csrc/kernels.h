@@ -112,6 +112,8 @@ bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s
 bool train_mirror_launch(const TrainParams& p, const MirrorParams& mp, int B, int NW, cudaStream_t s);
 bool type_i_async_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, uint32_t i, int out, int B, int NW,
                               cudaStream_t s);
+bool type_i_smem_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, uint32_t i, int out, int B, int NW,
+                             cudaStream_t s);
 bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out, uint32_t trials, int B, int NW,
                            unsigned long long* inc, unsigned long long* dec, cudaStream_t s);
 void build_entries_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, EvalEntry* e,

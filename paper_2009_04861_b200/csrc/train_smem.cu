@@ -55,9 +55,69 @@ __device__ __forceinline__ uint32_t valid_of(int w, int o) {
   return first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
 }
 
-template <int NW, int B>
+// Type I (feedback.cpp:32-70) on a shared-memory clause, one word pair per
+// lane at a time, with the register kernel's draws (train.cu type_i_async):
+// alias patterns from Philox counters (clause, example, 2*word + part, 0),
+// or the bit-serial sampler when p_high != 1 - p_low.
+template <int NW, int B, bool P2>
+__device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
+                                            int before, const TrainParams& P, uint32_t g, uint32_t i32, int lane,
+                                            const uint32_t* atab) {
+#pragma unroll 1
+  for (int p = 0; p < NW; ++p) {
+    const int w = p * 32 + lane;
+    const uint32_t vm = valid_of(w, P.o);
+    const uint32_t need[2] = {vm, vm};
+    const uint32_t sel[2] = {x[p], n[p]};
+    uint32_t bern[2];
+    auto gen = [&](int slot, int blk) {
+      const uint32_t wid = slot < 2 ? static_cast<uint32_t>(w * 2 + slot)
+                                    : (0xFFFF0000u | static_cast<uint32_t>(p * 32 + lane));
+      return philox4x32(U4{g, i32, wid, static_cast<uint32_t>(blk)}, P.rkey);
+    };
+    if (before && !P.alias_sel) {
+      bernoulli_words<2, true>(need, sel, P.bern, bern, gen);
+    } else {
+      alias_words<2>(need, atab, static_cast<uint32_t>(lane) & (kAliasCopies - 1), bern, gen);
+      if (before) {
+        bern[0] = (bern[0] ^ sel[0]) & need[0];
+        bern[1] = (bern[1] ^ sel[1]) & need[1];
+      }
+    }
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+      Planes<B> pl;
+      S.get(part, w, pl);
+      const uint32_t lit = sel[part];
+      if (before) {
+        const uint32_t incl = pl.p[B - 1];
+        const uint32_t inc = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part] & incl)) & vm;
+        const uint32_t dec = ~lit & bern[part] & ~incl & vm;
+        if (P2) {
+          add_one_sat1<B>(pl, inc);
+          sub_one_sat0<B>(pl, dec);
+        } else {
+          step<B>(pl, inc, dec, P.lo, P.hi);
+        }
+      } else if (P2) {
+        sub_one_sat0<B>(pl, bern[part] & vm);
+      } else {
+        step_down<B>(pl, bern[part] & vm, P.lo);
+      }
+      S.put(part, w, pl);
+    }
+  }
+  __syncwarp();
+}
+
+template <int NW, int B, bool P2>
 __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(TrainParams P) {
   extern __shared__ uint32_t smem[];
+  const int Wp = P.Wp;
+  const size_t words = static_cast<size_t>(B) * 2 * Wp;
+  uint32_t* atab = smem + kSmemWarps * words;  // alias table copies after the clause planes
+  for (int k = threadIdx.x; k < 256 * kAliasCopies; k += blockDim.x) atab[k] = __ldg(P.alias8 + k / kAliasCopies);
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int lc = blockIdx.x * kSmemWarps + wib;
@@ -68,8 +128,6 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
   const bool positive = P.all_positive || (j & 1) == 0;
   const int64_t q = P.q;
   const int T = P.margin;
-  const int Wp = P.Wp;
-  const size_t words = static_cast<size_t>(B) * 2 * Wp;
   SmemPlanes<B> S{smem + wib * words, Wp};
   uint32_t* st = P.state + static_cast<size_t>(lc) * words;
   for (size_t k = lane; k < words; k += 32) S.s[k] = st[k];
@@ -149,37 +207,7 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
         }
       } else {  // Type I (feedback.cpp:32-70), one word pair at a time
         ++events_type1;
-        const uint32_t i32 = static_cast<uint32_t>(is);
-#pragma unroll 1
-        for (int p = 0; p < NW; ++p) {
-          const int w = p * 32 + lane;
-          const uint32_t vm = valid_of(w, P.o);
-          const uint32_t need[2] = {vm, vm};
-          const uint32_t sel[2] = {x[p], n[p]};
-          uint32_t bern[2];
-          auto gen = [&](int slot, int blk) {
-            const uint32_t wid = slot < 2 ? static_cast<uint32_t>(w * 2 + slot)
-                                          : (0xFFFF0000u | static_cast<uint32_t>(p * 32 + lane));
-            return philox4x32(U4{g, i32, wid, static_cast<uint32_t>(blk)}, P.rkey);
-          };
-          if (before) bernoulli_words<2, true>(need, sel, P.bern, bern, gen);
-          else bernoulli_words<2, false>(need, sel, P.bern, bern, gen);
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {
-            Planes<B> pl;
-            S.get(part, w, pl);
-            const uint32_t lit = sel[part];
-            if (before) {
-              const uint32_t incl = pl.p[B - 1];
-              const uint32_t inc = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part] & incl)) & vm;
-              const uint32_t dec = ~lit & bern[part] & ~incl & vm;
-              step<B>(pl, inc, dec, P.lo, P.hi);
-            } else {
-              step_down<B>(pl, bern[part] & vm, P.lo);
-            }
-            S.put(part, w, pl);
-          }
-        }
+        type_i_smem<NW, B, P2>(S, x, n, before, P, g, static_cast<uint32_t>(is), lane, atab);
         __syncwarp();
         after = eval_train_smem<NW, B>(S, x, n, lane);
       }
@@ -209,21 +237,69 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
   }
 }
 
+template <int NW, int B, bool P2>
+void launch_smem_p2(const TrainParams& p, cudaStream_t s, int grid, size_t shm) {
+  if (shm > 48 * 1024)
+    cudaFuncSetAttribute(train_async_smem_kernel<NW, B, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(shm));
+  count_launch();
+  train_async_smem_kernel<NW, B, P2><<<grid, 32 * kSmemWarps, shm, s>>>(p);
+}
+
 template <int NW, int B>
 bool launch_smem(const TrainParams& p, cudaStream_t s, int* blocks) {
   const int clauses = p.m * p.n_loc;
   const int grid = (clauses + kSmemWarps - 1) / kSmemWarps;
-  const size_t shm = sizeof(uint32_t) * kSmemWarps * B * 2 * p.Wp;
-  if (shm > 48 * 1024)
-    cudaFuncSetAttribute(train_async_smem_kernel<NW, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(shm));
+  const size_t shm = sizeof(uint32_t) * (kSmemWarps * B * 2 * p.Wp + 256 * kAliasCopies);
   if (blocks) *blocks = grid;
-  count_launch();
-  train_async_smem_kernel<NW, B><<<grid, 32 * kSmemWarps, shm, s>>>(p);
+  if (p.lo == 0 && p.hi == (1u << B) - 1u) launch_smem_p2<NW, B, true>(p, s, grid, shm);
+  else launch_smem_p2<NW, B, false>(p, s, grid, shm);
   return true;
 }
 
+// One Type I feedback of the shared-memory path on the clause planes at
+// `state` (global), literal row 0 of P: the wide-row counterpart of
+// train.cu type_i_async_once_kernel for the async sampler's parity test.
+template <int NW, int B, bool P2>
+__global__ void __launch_bounds__(32) type_i_smem_once_kernel(TrainParams P, uint32_t* state, uint32_t g,
+                                                              uint32_t i, int out) {
+  extern __shared__ uint32_t smem[];
+  const int lane = threadIdx.x;
+  const size_t words = static_cast<size_t>(B) * 2 * P.Wp;
+  uint32_t* atab = smem + words;
+  for (int k = lane; k < 256 * kAliasCopies; k += 32) atab[k] = __ldg(P.alias8 + k / kAliasCopies);
+  for (size_t k = lane; k < words; k += 32) smem[k] = state[k];
+  __syncwarp();
+  SmemPlanes<B> S{smem, P.Wp};
+  uint32_t x[NW], n[NW];
+#pragma unroll
+  for (int p = 0; p < NW; ++p) {
+    x[p] = P.xplane[p * 32 + lane];
+    n[p] = P.nplane[p * 32 + lane];
+  }
+  type_i_smem<NW, B, P2>(S, x, n, out, P, g, i, lane, atab);
+  for (size_t k = lane; k < words; k += 32) state[k] = smem[k];
+}
+
 }  // namespace
+
+bool type_i_smem_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, uint32_t i, int out, int B, int NW,
+                             cudaStream_t s) {
+  const bool p2 = p.lo == 0 && p.hi == (1u << B) - 1u;
+  const size_t shm = sizeof(uint32_t) * (static_cast<size_t>(B) * 2 * p.Wp + 256 * kAliasCopies);
+  auto go = [&](auto kern) {
+    if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
+    count_launch();
+    kern<<<1, 32, shm, s>>>(p, state, g, i, out);
+    return true;
+  };
+#define TMG_SONCE(nw, b)                                                           \
+  if (NW == nw && B == b)                                                          \
+    return p2 ? go(type_i_smem_once_kernel<nw, b, true>) : go(type_i_smem_once_kernel<nw, b, false>);
+  TMG_SONCE(8, 4) TMG_SONCE(8, 8) TMG_SONCE(8, 15) TMG_SONCE(10, 4) TMG_SONCE(10, 8) TMG_SONCE(10, 15)
+#undef TMG_SONCE
+  return false;
+}
 
 bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
   if (NW == 8 && B == 8) return launch_smem<8, 8>(p, s, blocks);

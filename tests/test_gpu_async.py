@@ -145,12 +145,16 @@ def test_type_i_table1_conformance(o, N, s, boost, out):
 
 @pytest.mark.parametrize("o,N,s,boost", [(784, 128, 10.0, False), (784, 128, 10.0, True), (784, 100, 10.0, False),
                                          (12, 128, 3.9, False), (40, 5, 2.0, True), (2352, 128, 15.0, False),
-                                         (1500, 300, 7.5, False), (2000, 128, 1.0, False)])
+                                         (1500, 300, 7.5, False), (2000, 128, 1.0, False),
+                                         (5000, 128, 15.0, False), (10000, 128, 15.0, True),
+                                         (9000, 100, 25.0, False)])
 def test_async_type_i_bit_exact(o, N, s, boost):
     """The asynchronous Type I draw (Philox counters (clause, example) under the
-    epoch key, exact bit-serial Bernoulli, saturating steps) reproduced
-    counter-for-counter by its C restatement (oracle/tm_oracle_async.c), for
-    both clause outputs, on near-saturated and mid-range automata."""
+    epoch key; alias-table patterns, or the exact bit-serial sampler when
+    p_high != 1 - p_low; saturating steps) reproduced counter-for-counter by
+    its C restatement (oracle/tm_oracle_async.c), for both clause outputs, on
+    near-saturated and mid-range automata, register-resident and
+    shared-memory (wide-row) clause paths."""
     from paper_2009_04861_b200.tsetlin import alias8_table, type_i_async
     rng = np.random.default_rng(o * 7 + N)
     table = alias8_table(O.prob_threshold(1.0 / s))
