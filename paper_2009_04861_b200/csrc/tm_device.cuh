@@ -95,6 +95,13 @@ struct Xoshiro {
   }
 };
 
+// %laneid (one S2R when rematerialised, no mask).
+__device__ __forceinline__ uint32_t lane_id() {
+  uint32_t l;
+  asm("mov.u32 %0, %%laneid;" : "=r"(l));
+  return l;
+}
+
 // a * b + c on the FMA pipe (IMAD), for ALU-pipe relief.
 __device__ __forceinline__ uint32_t mad_u32(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -208,6 +215,9 @@ constexpr int kAliasCopies = 16;
 template <int K, typename Gen>
 __device__ __forceinline__ void alias_words(const uint32_t (&need)[K], const uint32_t* tab, uint32_t laneoff,
                                             uint32_t (&bern)[K], Gen&& gen) {
+  // Shared-space byte address of this lane's copy of column 0; column c is
+  // 4 * kAliasCopies * c further (one IMAD per lookup, on the FMA pipe).
+  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 4u * laneoff;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const U4 r = gen(k, 0);
@@ -215,7 +225,8 @@ __device__ __forceinline__ void alias_words(const uint32_t (&need)[K], const uin
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t u = j == 0 ? r.x : (j == 1 ? r.y : (j == 2 ? r.z : r.w));
-      const uint32_t e = tab[((u & 0xFFu) * kAliasCopies) | laneoff];
+      uint32_t e;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(mad_u32(u & 0xFFu, 4u * kAliasCopies, base)));
       b[j] = (u | 0xFFu) < e ? u : e;  // low byte: the drawn pattern
     }
     const uint32_t lo = __byte_perm(b[0], b[1], 0x0040), hi = __byte_perm(b[2], b[3], 0x0040);

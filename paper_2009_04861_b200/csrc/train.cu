@@ -27,9 +27,6 @@
 #ifndef TMG_ALIAS
 #define TMG_ALIAS 1  // alias-table sampler for clause-output-0 Type I draws
 #endif
-#ifndef TMG_ASYNC_V5
-#define TMG_ASYNC_V5 1  // window-deferred record + 2x unrolled step loop
-#endif
 
 namespace tmg {
 
@@ -155,7 +152,7 @@ __device__ __forceinline__ uint64_t splitmix_dev(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-// Publishes the post-feedback output (pool.cpp:93-106): lane 0 only.
+// Publishes the post-feedback output (pool.cpp:93-106); one lane.
 __device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row, int64_t i, int c,
                                        bool positive, uint32_t pword, int after) {
   const uint32_t bit = 1u << (i & 31);
@@ -266,7 +263,7 @@ template <int NW, int B, bool P2>
 __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   __shared__ uint32_t atab[TMG_ALIAS ? 256 * kAliasCopies : 1];
   load_alias(P, atab);
-  const int lane = threadIdx.x & 31;
+  const int lane = static_cast<int>(lane_id());
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= P.m * P.n_loc) return;
   const int c = lc / P.n_loc;
@@ -318,7 +315,6 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
     if (!gm) continue;
     events += __popc(gm);
 
-#if TMG_ASYNC_V5
     // ---- gated steps in order. Each lane owns the bookkeeping of its own
     // step: it fetched the previous-output bit of its example above and
     // publishes the new output after the window (record_output_and_tally,
@@ -332,10 +328,12 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
     const int code = target ? ~static_cast<int>(i) : static_cast<int>(i);  // q < 2^31: sign = Type I
     unsigned outs = 0;  // bit l: output after the step lane l drew
     uint32_t xa[NW], na[NW], xb[NW], nb[NW];
-    auto fetch = [&](uint32_t (&xs)[NW], uint32_t (&ns)[NW], int& cd, int& sl) {
-      sl = __ffs(gm) - 1;
-      gm &= gm - 1;
-      cd = __shfl_sync(kFull, code, sl);
+    events_type1 += __popc(__ballot_sync(kFull, gated && target));
+    auto fetch = [&](uint32_t (&xs)[NW], uint32_t (&ns)[NW], int& cd, uint32_t& sl) {
+      const int l = __ffs(gm) - 1;
+      sl = gm & (0u - gm);  // this step's lane bit
+      gm ^= sl;
+      cd = __shfl_sync(kFull, code, l);
       const size_t row = static_cast<size_t>(cd < 0 ? ~cd : cd) * P.Wp + lane;
 #pragma unroll
       for (int p = 0; p < NW; ++p) {
@@ -343,19 +341,19 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
         ns[p] = __ldg(P.nplane + row + p * 32);
       }
     };
-    auto run = [&](const uint32_t (&xs)[NW], const uint32_t (&ns)[NW], int cd, int sl) {
+    auto run = [&](const uint32_t (&xs)[NW], const uint32_t (&ns)[NW], int cd, uint32_t sl) {
       const int before = cl.eval_cached(xs, ns);
       int after = before;
       if (cd >= 0) {
         if (before && cl.type_ii(xs, ns)) after = cl.eval_train(xs, ns);
       } else {
-        ++events_type1;
         type_i_async<NW, B, P2>(cl, xs, ns, before, P, g, static_cast<uint32_t>(~cd), lane, atab);
         after = cl.eval_train(xs, ns);
       }
-      outs |= static_cast<unsigned>(after) << sl;
+      outs = mad_u32(sl, static_cast<uint32_t>(after), outs);  // disjoint bits: OR as an FMA-pipe add
     };
-    int cda, sla, cdb, slb;
+    int cda, cdb;
+    uint32_t sla, slb;
     if (NW <= TMG_ASYNC_UNROLL_NW) {
       // Two copies of the step body, no register moves between buffers.
       fetch(xa, na, cda, sla);
@@ -385,74 +383,6 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       atomicAdd(&P.tallies[ti], delta);
       if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
     }
-#else
-    // ---- gated steps in order; the next step's literal words are prefetched
-    // while the current one is processed. The previous-output word is loaded
-    // at the start of a step and only consumed after the feedback.
-    const int iq = static_cast<int>(i);  // q < 2^31
-    int sl = __ffs(gm) - 1;
-    gm &= gm - 1;
-    int is = __shfl_sync(kFull, iq, sl);
-    int tg = __shfl_sync(kFull, target, sl);
-    uint32_t x[NW], n[NW];
-    {
-      const uint32_t* xr = P.xplane + static_cast<size_t>(is) * P.Wp + lane;
-      const uint32_t* nr = P.nplane + static_cast<size_t>(is) * P.Wp + lane;
-#pragma unroll
-      for (int p = 0; p < NW; ++p) {
-        x[p] = __ldg(xr + p * 32);
-        n[p] = __ldg(nr + p * 32);
-      }
-    }
-    while (true) {
-      uint32_t pword = 0;
-      if (lane == 0) pword = prev_row[is >> 5];
-      const bool more = gm != 0;
-      int is2 = 0, tg2 = 0;
-      uint32_t x2[NW], n2[NW];
-      if (more) {
-        const int sl2 = __ffs(gm) - 1;
-        gm &= gm - 1;
-        is2 = __shfl_sync(kFull, iq, sl2);
-        tg2 = __shfl_sync(kFull, target, sl2);
-        const uint32_t* xr = P.xplane + static_cast<size_t>(is2) * P.Wp + lane;
-        const uint32_t* nr = P.nplane + static_cast<size_t>(is2) * P.Wp + lane;
-#pragma unroll
-        for (int p = 0; p < NW; ++p) {
-          x2[p] = __ldg(xr + p * 32);
-          n2[p] = __ldg(nr + p * 32);
-        }
-      }
-      const int before = cl.eval_cached(x, n);
-      int after = before;
-      if (tg == 0) {
-        if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
-      } else {
-        ++events_type1;
-        type_i_async<NW, B, P2>(cl, x, n, before, P, g, static_cast<uint32_t>(is), lane, atab);
-        after = cl.eval_train(x, n);
-      }
-      if (lane == 0) {
-        const uint32_t bit = 1u << (is & 31);
-        if (((pword & bit) != 0) != (after != 0)) {
-          prev_row[is >> 5] = pword ^ bit;
-          int delta = after ? 1 : -1;
-          if (!positive) delta = -delta;
-          const size_t ti = static_cast<size_t>(is) * P.m + c;
-          atomicAdd(&P.tallies[ti], delta);
-          if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
-        }
-      }
-      if (!more) break;
-      is = is2;
-      tg = tg2;
-#pragma unroll
-      for (int p = 0; p < NW; ++p) {
-        x[p] = x2[p];
-        n[p] = n2[p];
-      }
-    }
-#endif
   }
   cl.store(st, P.Wp, lane);
   const int cnt = cl.include_count();
