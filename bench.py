@@ -340,7 +340,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--windows", type=int, default=64, help="tally all-reduce windows per epoch (N>1)")
+    ap.add_argument("--windows", type=int, default=16, help="tally all-reduce windows per epoch (N>1; 16 costs ~2%% on one GPU, tools/window_cost.py)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -113,7 +113,10 @@ class ExamplePool:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().tmg_pool_destroy(h)
+            try:
+                lib().tmg_pool_destroy(h)
+            except Exception:  # interpreter teardown: the process frees the device anyway
+                pass
             self._h = None
 
     @property
@@ -275,7 +278,10 @@ class MultiClassTM:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().tmg_machine_destroy(h)
+            try:
+                lib().tmg_machine_destroy(h)
+            except Exception:  # interpreter teardown: the process frees the device anyway
+                pass
             self._h = None
 
     @property
@@ -516,7 +522,10 @@ class RegressionHead:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            lib().tmg_machine_destroy(h)
+            try:
+                lib().tmg_machine_destroy(h)
+            except Exception:  # interpreter teardown: the process frees the device anyway
+                pass
             self._h = None
 
     @property

@@ -85,6 +85,56 @@ def test_async_epoch_invariants_wide_rows(kind, q, clauses, T_, s_):
     assert np.array_equal(T.class_sums(tm, test), ref.class_sums(lits))
 
 
+def test_two_clause_shards_one_gpu():
+    """The multi-GPU window protocol (distributed.py) with two clause shards
+    on one GPU and the all-reduce done by hand: after every epoch both tally
+    replicas are equal and equal the signed sum of BOTH shards' clause
+    outputs; sharded class sums (partial sums added) equal the oracle's on
+    the combined state; accuracy is that of the unsharded machine."""
+    import torch
+    from paper_2009_04861_b200 import distributed as D
+    d = synth.make("mnist", 3000, 1000, 2009)
+    n, m, q = 200, 10, 3000
+    cfg = T.TMConfig(clauses=n, margin=50, specificity=10.0, seed=4)
+    engines = []
+    for r in range(2):
+        jb, je = D.shard_range(n, r, 2)
+        tm = T.MultiClassTM(cfg, 784, m, clause_range=(jb, je))
+        pool = T.ExamplePool(784, d.train_x, d.train_y, m)
+        engines.append(D.GpuShardEngine(tm, pool))
+    for e in range(2):
+        for eng in engines:
+            eng.begin(e)
+        for t0, t1 in D.window_bounds(q, 8):
+            for eng in engines:
+                eng.window(e, t0, t1)
+            torch.cuda.synchronize()
+            reduced = engines[0].delta().clone() + engines[1].delta().clone()
+            for eng in engines:
+                eng.apply(reduced)
+            torch.cuda.synchronize()
+        t0_, t1_ = engines[0].pool.tallies(), engines[1].pool.tallies()
+        assert np.array_equal(t0_, t1_)
+        for c in range(m):
+            bits = np.concatenate([_bits_of(eng.tm.banks[c].prev_outputs(), q) for eng in engines])
+            expect = bits[0::2].sum(0) - bits[1::2].sum(0)
+            assert np.array_equal(t0_[:, c], expect), (e, c)
+    test = T.ExamplePool(784, d.test_x, d.test_y, m)
+    sums = sum(T.class_sums(eng.tm, test) for eng in engines)
+    ref = O.Machine(784, m, n, 128)
+    full = np.concatenate([np.stack([eng.tm.banks[c].counters() for c in range(m)]) for eng in engines], axis=1)
+    ref.set_counters(full)
+    lits = O.pack_literals(d.test_x)
+    assert np.array_equal(sums, ref.class_sums(lits))
+    acc_sharded = float((sums.argmax(1) == d.test_y).mean())
+    single = T.MultiClassTM(cfg, 784, m)
+    spool = T.ExamplePool(784, d.train_x, d.train_y, m)
+    for e in range(2):
+        T.train_epoch_parallel(single, spool, 1, e)
+    acc_single = T.evaluate_accuracy(single, test)
+    assert acc_sharded > acc_single - 0.03, (acc_sharded, acc_single)
+
+
 def test_async_window_accounting():
     """Windows of a pass compose to the full pass (multi-GPU building block)."""
     d = synth.make("xor", 1000, 10, 5, 0.1)
