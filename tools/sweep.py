@@ -38,6 +38,18 @@ def run(kind, clauses_list, q, qt, T_, s, epochs=2):
 
 
 q = int(sys.argv[2]) if len(sys.argv) > 2 else 60000
+
+
+def warm_up():
+    """One throwaway epoch so module loading and clock ramp-up stay out of the
+    first sweep point."""
+    d = synth.make("mnist", 2000, 0, 1)
+    tm = T.MultiClassTM(T.TMConfig(clauses=100, margin=50, specificity=10.0, seed=1), 784, 10)
+    pool = T.ExamplePool(784, d.train_x, d.train_y, 10)
+    T.train_epoch_parallel(tm, pool, 1, 0)
+
+
+warm_up()
 if what in ("mnist", "all"):
     run("mnist", [20, 100, 200, 500, 1000, 2000, 5000, 7000, 10000], q, 10000, 50, 10.0)
 if what in ("fmnist", "all"):
