@@ -158,6 +158,55 @@ def algorithmic_ops(steps_per_epoch: int, events: int, type1: int) -> float:
     return 18.0 * steps_per_epoch + events * 2.0 * w32 + type1 * L * 18.0 + (events - type1) * L * 3.0
 
 
+def inference_line(args, tm, d, local, stream):
+    import numpy as np
+    import torch
+
+    import paper_2009_04861_b200 as T
+    from paper_2009_04861_b200 import _capi, model_io
+
+    tx = torch.from_numpy(d.test_x).to(f"cuda:{local}")
+    ty = torch.from_numpy(d.test_y).to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    test = T.ExamplePool.from_device(O_FEAT, tx.data_ptr(), ty.data_ptr(), Q_TEST, M_CLS, device=local,
+                                     labels_host=d.test_y)
+    sums = torch.zeros(Q_TEST * M_CLS, dtype=torch.int32, device=f"cuda:{local}")
+    ms = []
+    for r in range(args.warmup + args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _capi.check(_capi.lib().tmg_class_sums_device(tm.handle, test.handle, T.PREDICT, sums.data_ptr()))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if r >= args.warmup:
+            ms.append(e0.elapsed_time(e1))
+    t = statistics.mean(ms)
+    pred = T.predict_all(tm, test)
+    evals_per_s = M_CLS * N_CLAUSES * Q_TEST * 2 * O_FEAT / (t * 1e-3)
+    out = {"metric": "clause-literal evals/s (predict, class sums of the test rows)", "value": evals_per_s,
+           "unit": "clause-literal evals/s", "rows_per_s": Q_TEST / (t * 1e-3), "ms": t, "rows": Q_TEST,
+           "kernel": "eval_sums_kernel<0,128>", "model": "state after the last timed epoch",
+           "test_accuracy": float((pred == d.test_y).mean())}
+    if not args.no_cpu and os.path.exists(REF_DRIVER):
+        import tempfile
+        rows = 500
+        with tempfile.TemporaryDirectory() as tmp:
+            path = os.path.join(tmp, "bench.model")
+            model_io.save_model_file(path, tm)
+            r = json.loads(subprocess.run(
+                [REF_DRIVER, "predict", path, "--data", "mnist", "--q", str(Q_TRAIN), "--qtest", str(Q_TEST),
+                 "--qtest-use", str(rows), "--data-seed", str(DATA_SEED)],
+                check=True, capture_output=True, text=True).stdout)
+            same = bool(np.array_equal(np.load(path + ".ref_pred.npy"), pred[:rows]))
+        out["cpu_baseline"] = {"value": M_CLS * N_CLAUSES * rows * 2 * O_FEAT / r["seconds"],
+                               "unit": "clause-literal evals/s", "rows_per_s": r["rows_per_s"], "cores": 1,
+                               "kind": "reference",
+                               "sample": f"predict_all (single-threaded by construction, trainer.cpp:272-279) "
+                                         f"on the first {rows} test rows, same model file"}
+        out["predictions_identical"] = same
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -316,6 +365,12 @@ def run_ours(args):
                                  for n, k in enumerate(("pool_h2d_pack", "epoch_and_report", "pool_free"))},
                    "h2d_bytes_per_step": int(host_bits.nbytes + host_lab.nbytes + 4 * Q_TRAIN),
                    "d2h_bytes_per_step": int(8 * M_CLS * 2)}
+    # ---- inference on the state the last timed epoch left (class sums of the
+    # 10 000 test rows; K1 eval kernel, CUDA events on the engine stream),
+    # beside the reference's single-threaded predict_all on the SAME model
+    # file for a bounded row sample, predictions compared row for row.
+    if world == 1:
+        line["inference"] = inference_line(args, tm, d, local, stream)
     # ---- CPU reference beside it (rank 0, N=1 only)
     if world == 1 and not args.no_cpu and os.path.exists(REF_DRIVER):
         cores = os.cpu_count() or 1

@@ -8,7 +8,7 @@
 //   train  ...     time train_epoch_parallel / _sequential on synthetic data
 //                  (bench.py's cpu_baseline and --impl reference arm, and the
 //                  async-accuracy reference numbers in tests/golden/)
-//   predict ...    time predict_all
+//   predict <model> ...  time predict_all on a saved model (tools/eval_time.py)
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -602,6 +602,32 @@ int cmd_train(const Args& a) {
   return 0;
 }
 
+// predict <model.txt> [flags]: load a tmmodel v1 file (e.g. written by the
+// GPU engine) and time the reference's single-threaded predict_all on the
+// first --qtest-use rows of the synthetic test split; prints one JSON line and
+// saves the predictions next to the model (<model>.ref_pred.npy).
+int cmd_predict(const std::string& model_path, const Args& a) {
+  AnyModel any = load_model_file(model_path);
+  auto* tmp = std::get_if<MultiClassTM>(&any);
+  if (!tmp) throw std::invalid_argument("predict: not a classification model");
+  const MultiClassTM& tm = *tmp;
+  Split d = make_data(a.data, a.q, a.qt, a.data_seed, a.noise);  // the test split follows the train rows
+  const std::int64_t qtu = a.qt_use > 0 ? std::min(a.qt_use, a.qt) : a.qt;
+  auto vx = prefix(d.test_x, static_cast<std::size_t>(qtu), static_cast<std::size_t>(d.features));
+  auto vy = prefix(d.test_y, static_cast<std::size_t>(qtu), 1);
+  ExamplePool test(d.features, vx, vy, d.classes);
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::vector<std::int32_t> pred = predict_all(tm, test);
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  npyio::save(model_path + ".ref_pred.npy", pred);
+  std::int64_t hits = 0;
+  for (std::int64_t i = 0; i < qtu; ++i) hits += pred[static_cast<std::size_t>(i)] == vy[static_cast<std::size_t>(i)];
+  std::printf("{\"rows\": %lld, \"seconds\": %.6f, \"rows_per_s\": %.3f, \"accuracy\": %.6f, \"threads\": 1}\n",
+              static_cast<long long>(qtu), secs, static_cast<double>(qtu) / secs,
+              static_cast<double>(hits) / static_cast<double>(std::max<std::int64_t>(qtu, 1)));
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -626,6 +652,7 @@ int main(int argc, char** argv) {
       return 0;
     }
     if (cmd == "train") return cmd_train(parse(argc, argv, 2));
+    if (cmd == "predict" && argc > 2) return cmd_predict(argv[2], parse(argc, argv, 3));
     std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
     return 2;
   } catch (const std::exception& ex) {
