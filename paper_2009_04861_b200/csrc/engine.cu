@@ -198,7 +198,9 @@ struct tmg_pool {
   int o = 0, m = 0, Wp = 0;
   int64_t q = 0;
   cudaStream_t stream = nullptr;
-  DevBuf<uint32_t> xplane, nplane;
+  DevBuf<uint32_t> rows;  // [q][2][Wp]: x-plane words, then !x-plane words
+  uint32_t* xplane() const { return rows.ptr; }
+  uint32_t* nplane() const { return rows.ptr + Wp; }
   DevBuf<int32_t> labels, tallies, delta, order;
   std::vector<int32_t> host_labels;
 };
@@ -356,8 +358,8 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   p.Wq = tm->Wq;
   p.lo = (1u << (tm->B - 1)) - static_cast<uint32_t>(tm->N);
   p.hi = (1u << (tm->B - 1)) + static_cast<uint32_t>(tm->N) - 1u;
-  p.xplane = pool->xplane.ptr;
-  p.nplane = pool->nplane.ptr;
+  p.xplane = pool->xplane();
+  p.nplane = pool->nplane();
   p.labels = pool->labels.ptr;
   p.tallies = pool->tallies.ptr;
   p.tally_delta = nullptr;
@@ -473,8 +475,7 @@ tmg_pool* create_pool_common(int device, int o, int64_t q, int m) {
 
 void finish_pool(tmg_pool* pool, const uint8_t* d_bits, const int32_t* d_labels) {
   const size_t rows = static_cast<size_t>(pool->q);
-  pool->xplane.alloc(rows * pool->Wp);
-  pool->nplane.alloc(rows * pool->Wp);
+  pool->rows.alloc(rows * 2 * pool->Wp);
   pool->labels.alloc(rows);
   pool->tallies.alloc(rows * pool->m);
   pool->delta.alloc(rows * pool->m);
@@ -483,7 +484,7 @@ void finish_pool(tmg_pool* pool, const uint8_t* d_bits, const int32_t* d_labels)
   DevBuf<int> err;
   err.alloc(2);
   CK(cudaMemsetAsync(err.ptr, 0, 8, pool->stream));
-  tmg::pack_planes_launch(d_bits, pool->xplane.ptr, pool->nplane.ptr, pool->q, pool->o, pool->Wp, err.ptr,
+  tmg::pack_planes_launch(d_bits, pool->xplane(), pool->nplane(), pool->q, pool->o, pool->Wp, err.ptr,
                           pool->stream);
   CK(cudaGetLastError());
   if (pool->m > 1) tmg::check_labels_launch(d_labels, pool->q, pool->m, err.ptr, pool->stream);
@@ -777,8 +778,7 @@ TMG_API int tmg_pool_destroy(tmg_pool* pool) {
   cudaGetDevice(&prev);
   cudaSetDevice(pool->device);
   if (pool->stream) cudaStreamSynchronize(pool->stream);
-  pool->xplane.release();
-  pool->nplane.release();
+  pool->rows.release();
   pool->labels.release();
   pool->tallies.release();
   pool->delta.release();
@@ -801,17 +801,18 @@ TMG_API int tmg_pool_get_literals(const tmg_pool* pool, uint64_t* out) {
     if (!pool) fail(TMG_EINVAL, "null pool handle");
     DeviceGuard dg(pool->device);
     const size_t rows = static_cast<size_t>(pool->q);
-    std::vector<uint32_t> xs(rows * pool->Wp), ns(rows * pool->Wp);
-    CK(cudaMemcpyAsync(xs.data(), pool->xplane.ptr, xs.size() * 4, cudaMemcpyDeviceToHost, pool->stream));
-    CK(cudaMemcpyAsync(ns.data(), pool->nplane.ptr, ns.size() * 4, cudaMemcpyDeviceToHost, pool->stream));
+    std::vector<uint32_t> rw(rows * 2 * pool->Wp);
+    CK(cudaMemcpyAsync(rw.data(), pool->xplane(), rw.size() * 4, cudaMemcpyDeviceToHost, pool->stream));
     CK(cudaStreamSynchronize(pool->stream));
     const int o = pool->o, W64 = (2 * o + 63) / 64;
     for (size_t i = 0; i < rows; ++i) {
       uint64_t* row = out + i * W64;
       std::fill(row, row + W64, 0);
+      const uint32_t* xs = rw.data() + i * 2 * pool->Wp;
+      const uint32_t* ns = xs + pool->Wp;
       for (int f = 0; f < o; ++f) {
-        if ((xs[i * pool->Wp + (f >> 5)] >> (f & 31)) & 1u) row[f >> 6] |= 1ULL << (f & 63);
-        if ((ns[i * pool->Wp + (f >> 5)] >> (f & 31)) & 1u) row[(o + f) >> 6] |= 1ULL << ((o + f) & 63);
+        if ((xs[f >> 5] >> (f & 31)) & 1u) row[f >> 6] |= 1ULL << (f & 63);
+        if ((ns[f >> 5] >> (f & 31)) & 1u) row[(o + f) >> 6] |= 1ULL << ((o + f) & 63);
       }
     }
   });
@@ -1074,15 +1075,14 @@ TMG_API int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, c
     DeviceGuard dg(tm->device);
     const int W64 = (2 * tm->o + 63) / 64;
     DevBuf<uint64_t> dl;
-    DevBuf<uint32_t> xs, ns;
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
     DevBuf<unsigned long long> dinc, ddec;
     dl.alloc(W64);
-    xs.alloc(tm->Wp);
-    ns.alloc(tm->Wp);
+    xs.alloc(2 * tm->Wp);
     dinc.alloc(2 * static_cast<size_t>(tm->o));
     ddec.alloc(2 * static_cast<size_t>(tm->o));
     CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
-    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, xs.ptr + tm->Wp, 1, tm->o, tm->Wp, tm->stream);
     CK(cudaMemsetAsync(dinc.ptr, 0, dinc.bytes(), tm->stream));
     CK(cudaMemsetAsync(ddec.ptr, 0, ddec.bytes(), tm->stream));
     epoch_keys(tm, 0);
@@ -1094,7 +1094,7 @@ TMG_API int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, c
     fake.q = 1;
     p = make_params(tm, &fake);
     p.xplane = xs.ptr;
-    p.nplane = ns.ptr;
+    p.nplane = xs.ptr + tm->Wp;
     const size_t lc = static_cast<size_t>(bank) * tm->n_loc + (j - tm->j_begin);
     if (!tmg::feedback_rates_launch(p, tm->state.ptr + lc * tm->B * 2 * tm->Wp, clause_output ? 1 : 0, trials,
                                     tm->B, tm->NW, dinc.ptr, ddec.ptr, tm->stream))
@@ -1115,12 +1115,11 @@ TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, con
     DeviceGuard dg(tm->device);
     const int W64 = (2 * tm->o + 63) / 64;
     DevBuf<uint64_t> dl;
-    DevBuf<uint32_t> xs, ns;
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
     dl.alloc(W64);
-    xs.alloc(tm->Wp);
-    ns.alloc(tm->Wp);
+    xs.alloc(2 * tm->Wp);
     CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
-    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, xs.ptr + tm->Wp, 1, tm->o, tm->Wp, tm->stream);
     epoch_keys(tm, epoch);
     tmg_pool fake;
     fake.o = tm->o;
@@ -1128,7 +1127,7 @@ TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, con
     fake.q = 1;
     tmg::TrainParams p = make_params(tm, &fake);
     p.xplane = xs.ptr;
-    p.nplane = ns.ptr;
+    p.nplane = xs.ptr + tm->Wp;
     const size_t lc = static_cast<size_t>(bank) * tm->n_loc + (j - tm->j_begin);
     const uint32_t g = static_cast<uint32_t>(bank) * tm->n + j;
     uint32_t* st = tm->state.ptr + lc * tm->B * 2 * tm->Wp;
@@ -1242,12 +1241,11 @@ TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_
     DeviceGuard dg(tm->device);
     const int W64 = (2 * tm->o + 63) / 64;
     DevBuf<uint64_t> dl;
-    DevBuf<uint32_t> xs, ns;
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
     dl.alloc(W64);
-    xs.alloc(tm->Wp);
-    ns.alloc(tm->Wp);
+    xs.alloc(2 * tm->Wp);
     CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
-    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, xs.ptr + tm->Wp, 1, tm->o, tm->Wp, tm->stream);
     tmg::MirrorJob jb{};
     jb.c = bank;
     jb.j = j;
@@ -1275,7 +1273,7 @@ TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_
     p.lo = (1u << (tm->B - 1)) - static_cast<uint32_t>(tm->N);
     p.hi = (1u << (tm->B - 1)) + static_cast<uint32_t>(tm->N) - 1u;
     p.xplane = xs.ptr;
-    p.nplane = ns.ptr;
+    p.nplane = xs.ptr + tm->Wp;
     p.q = 1;
     p.margin = 1;
     p.boost = boost ? 1 : 0;
@@ -1303,16 +1301,15 @@ TMG_API int tmg_evaluate_clause(tmg_machine* tm, int32_t bank, int32_t j, const 
     DeviceGuard dg(tm->device);
     const int W64 = (2 * tm->o + 63) / 64;
     DevBuf<uint64_t> dl;
-    DevBuf<uint32_t> xs, ns;
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
     DevBuf<int32_t> dout;
     dl.alloc(W64);
-    xs.alloc(tm->Wp);
-    ns.alloc(tm->Wp);
+    xs.alloc(2 * tm->Wp);
     dout.alloc(1);
     CK(cudaMemcpyAsync(dl.ptr, literals, W64 * 8, cudaMemcpyHostToDevice, tm->stream));
-    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, 1, tm->o, tm->Wp, tm->stream);
+    tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, xs.ptr + tm->Wp, 1, tm->o, tm->Wp, tm->stream);
     const int lc = bank * tm->n_loc + (j - tm->j_begin);
-    tmg::eval_one_launch(tm->state.ptr, lc, tm->B, tm->Wp, xs.ptr, ns.ptr, mode == TMG_EVAL_TRAIN ? 1 : 0,
+    tmg::eval_one_launch(tm->state.ptr, lc, tm->B, tm->Wp, xs.ptr, xs.ptr + tm->Wp, mode == TMG_EVAL_TRAIN ? 1 : 0,
                          dout.ptr, tm->stream);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, dout.ptr, 4, cudaMemcpyDeviceToHost, tm->stream));
@@ -1327,7 +1324,7 @@ TMG_API int tmg_refresh_tallies(tmg_machine* tm, tmg_pool* pool) {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
     if (tm->q_bound != pool->q) bind(tm, pool->q);  // pool.cpp:113
-    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, true, pool->tallies.ptr, tm->prev.ptr);
+    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, true, pool->tallies.ptr, tm->prev.ptr);
     CK(cudaStreamSynchronize(tm->stream));
   });
 }
@@ -1336,7 +1333,7 @@ TMG_API int tmg_class_sums_device(tmg_machine* tm, const tmg_pool* pool, int32_t
   return guarded([&] {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
-    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, mode == TMG_EVAL_TRAIN, d_sums, nullptr);
+    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, mode == TMG_EVAL_TRAIN, d_sums, nullptr);
     CK(cudaStreamSynchronize(tm->stream));
   });
 }
@@ -1346,7 +1343,7 @@ TMG_API int tmg_class_sums(tmg_machine* tm, const tmg_pool* pool, int32_t mode, 
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
     ensure_sums(tm, pool->q);
-    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, mode == TMG_EVAL_TRAIN, tm->sums.ptr,
+    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, mode == TMG_EVAL_TRAIN, tm->sums.ptr,
                       nullptr);
     CK(cudaMemcpyAsync(out, tm->sums.ptr, static_cast<size_t>(pool->q) * tm->m * 4, cudaMemcpyDeviceToHost,
                        tm->stream));
@@ -1360,7 +1357,7 @@ TMG_API int tmg_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
     DeviceGuard dg(tm->device);
     if (tm->n_loc != tm->n) fail(TMG_EINVAL, "predict on a clause shard: reduce class sums across shards first");
     ensure_sums(tm, pool->q + (pool->q + tm->m - 1) / tm->m + 1);
-    class_sums_device(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, false, tm->sums.ptr, nullptr);
+    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, false, tm->sums.ptr, nullptr);
     int32_t* pred = tm->sums.ptr + static_cast<size_t>(pool->q) * tm->m;
     tmg::argmax_launch(tm->sums.ptr, pred, pool->q, tm->m, tm->stream);
     CK(cudaGetLastError());
@@ -1370,15 +1367,13 @@ TMG_API int tmg_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
 }
 
 namespace {
-void literals_to_planes(tmg_machine* tm, const uint64_t* lits, int64_t q, DevBuf<uint32_t>& xs,
-                        DevBuf<uint32_t>& ns) {
+void literals_to_planes(tmg_machine* tm, const uint64_t* lits, int64_t q, DevBuf<uint32_t>& xs) {
   const int W64 = (2 * tm->o + 63) / 64;
   DevBuf<uint64_t> dl;
   dl.alloc(static_cast<size_t>(q) * W64);
-  xs.alloc(static_cast<size_t>(q) * tm->Wp);
-  ns.alloc(static_cast<size_t>(q) * tm->Wp);
+  xs.alloc(static_cast<size_t>(q) * 2 * tm->Wp);
   CK(cudaMemcpyAsync(dl.ptr, lits, dl.bytes(), cudaMemcpyHostToDevice, tm->stream));
-  tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, ns.ptr, q, tm->o, tm->Wp, tm->stream);
+  tmg::unpack_ref_literals_launch(dl.ptr, xs.ptr, xs.ptr + tm->Wp, q, tm->o, tm->Wp, tm->stream);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(tm->stream));
 }
@@ -1389,10 +1384,10 @@ TMG_API int tmg_class_sums_literals(tmg_machine* tm, const uint64_t* lits, int64
     M(tm);
     if (q <= 0) return;
     DeviceGuard dg(tm->device);
-    DevBuf<uint32_t> xs, ns;
-    literals_to_planes(tm, lits, q, xs, ns);
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
+    literals_to_planes(tm, lits, q, xs);
     ensure_sums(tm, q);
-    class_sums_device(tm, xs.ptr, ns.ptr, q, mode == TMG_EVAL_TRAIN, tm->sums.ptr, nullptr);
+    class_sums_device(tm, xs.ptr, xs.ptr + tm->Wp, q, mode == TMG_EVAL_TRAIN, tm->sums.ptr, nullptr);
     CK(cudaMemcpyAsync(out, tm->sums.ptr, static_cast<size_t>(q) * tm->m * 4, cudaMemcpyDeviceToHost, tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
   });
@@ -1404,10 +1399,10 @@ TMG_API int tmg_predict_literals(tmg_machine* tm, const uint64_t* lits, int64_t 
     if (q <= 0) return;
     if (tm->n_loc != tm->n) fail(TMG_EINVAL, "predict on a clause shard: reduce class sums across shards first");
     DeviceGuard dg(tm->device);
-    DevBuf<uint32_t> xs, ns;
-    literals_to_planes(tm, lits, q, xs, ns);
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
+    literals_to_planes(tm, lits, q, xs);
     ensure_sums(tm, q + (q + tm->m - 1) / tm->m + 1);
-    class_sums_device(tm, xs.ptr, ns.ptr, q, false, tm->sums.ptr, nullptr);
+    class_sums_device(tm, xs.ptr, xs.ptr + tm->Wp, q, false, tm->sums.ptr, nullptr);
     int32_t* pred = tm->sums.ptr + static_cast<size_t>(q) * tm->m;
     tmg::argmax_launch(tm->sums.ptr, pred, q, tm->m, tm->stream);
     CK(cudaGetLastError());
@@ -1441,7 +1436,7 @@ TMG_API int tmg_regress_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* 
   return guarded([&] {
     if (!M(tm) || !pool || tm->o != pool->o) fail(TMG_EINVAL, "head/pool feature count mismatch");
     DeviceGuard dg(tm->device);
-    regress_predict_planes(tm, pool->xplane.ptr, pool->nplane.ptr, pool->q, out);
+    regress_predict_planes(tm, pool->xplane(), pool->nplane(), pool->q, out);
   });
 }
 
@@ -1450,9 +1445,9 @@ TMG_API int tmg_regress_predict_literals(tmg_machine* tm, const uint64_t* lits, 
     M(tm);
     if (q <= 0) return;
     DeviceGuard dg(tm->device);
-    DevBuf<uint32_t> xs, ns;
-    literals_to_planes(tm, lits, q, xs, ns);
-    regress_predict_planes(tm, xs.ptr, ns.ptr, q, out);
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
+    literals_to_planes(tm, lits, q, xs);
+    regress_predict_planes(tm, xs.ptr, xs.ptr + tm->Wp, q, out);
   });
 }
 
@@ -1464,8 +1459,8 @@ TMG_API int tmg_update_regress(tmg_machine* tm, const uint64_t* literals, int32_
     if (!M(tm)->all_positive) fail(TMG_EINVAL, "not a regression machine");
     if (tm->n_loc != tm->n) fail(TMG_EINVAL, "needs the full (unsharded) machine");
     DeviceGuard dg(tm->device);
-    DevBuf<uint32_t> xs, ns;
-    literals_to_planes(tm, literals, 1, xs, ns);
+    DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
+    literals_to_planes(tm, literals, 1, xs);
     DevBuf<int32_t> lab, ord;
     DevBuf<uint64_t> drng;
     lab.alloc(1);
@@ -1484,7 +1479,7 @@ TMG_API int tmg_update_regress(tmg_machine* tm, const uint64_t* literals, int32_
     tmg::TrainParams p = make_params(tm, &fake);
     tm->regress_mode = false;
     p.xplane = xs.ptr;
-    p.nplane = ns.ptr;
+    p.nplane = xs.ptr + tm->Wp;
     p.labels = lab.ptr;
     p.order = ord.ptr;
     tmg::SeqParams sp{};

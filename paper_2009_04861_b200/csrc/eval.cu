@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
     const int64_t ie = i0 + e;
     uint32_t xv = 0, nv = 0;
     if (ie < P.q) {
-      xv = __ldg(P.xplane + ie * P.Wp + w);
-      nv = __ldg(P.nplane + ie * P.Wp + w);
+      xv = __ldg(P.xplane + ie * 2 * P.Wp + w);
+      nv = __ldg(P.nplane + ie * 2 * P.Wp + w);
     }
     tile[w * kTS + e] = xv;
     tile[(P.Wx + w) * kTS + e] = nv;
@@ -172,8 +172,8 @@ __global__ void pack_planes_kernel(const uint8_t* __restrict__ bits, uint32_t* _
   const unsigned xs = __ballot_sync(kFull, valid && b);
   const unsigned ns = __ballot_sync(kFull, valid && !b);
   if (lane == 0) {
-    xplane[i * Wp + w] = xs;
-    nplane[i * Wp + w] = ns;
+    xplane[i * 2 * Wp + w] = xs;
+    nplane[i * 2 * Wp + w] = ns;
   }
 }
 
@@ -206,8 +206,8 @@ __global__ void unpack_ref_kernel(const uint64_t* __restrict__ lits, uint32_t* _
   };
   const int f0 = w * 32;
   uint32_t vmask = f0 >= o ? 0u : (o - f0 >= 32 ? kFull : ((1u << (o - f0)) - 1u));
-  xplane[idx] = f0 < o ? (bits_at(f0) & vmask) : 0u;
-  nplane[idx] = f0 < o ? (bits_at(o + f0) & vmask) : 0u;
+  xplane[i * 2 * Wp + w] = f0 < o ? (bits_at(f0) & vmask) : 0u;
+  nplane[i * 2 * Wp + w] = f0 < o ? (bits_at(o + f0) & vmask) : 0u;
 }
 
 // classify (trainer.cpp:244-260): strict '>' keeps the lowest class on ties;

@@ -31,8 +31,10 @@ struct TrainParams {
   int32_t n, n_loc, j_begin, m, o, Wp, Wq;
   uint32_t lo, hi;  // plane value range of counters [1, 2N]
   // Pool.
-  const uint32_t* xplane;  // [q][Wp] literals k < o
-  const uint32_t* nplane;  // [q][Wp] literals k >= o
+  // Literal rows: [q][2][Wp] words, x-plane then !x-plane (tm_device.cuh);
+  // nplane == xplane + Wp, row stride 2 * Wp.
+  const uint32_t* xplane;  // literals k < o
+  const uint32_t* nplane;  // literals k >= o
   const int32_t* labels;   // [q]
   int32_t* tallies;        // [q][m]
   int32_t* tally_delta;    // [q][m] or null: deltas also published here (multi-GPU)

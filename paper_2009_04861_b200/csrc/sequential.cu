@@ -83,8 +83,8 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
     }
     __syncthreads();
     const int neg = neg_s;
-    const uint32_t* xr = P.xplane + i * Wp;
-    const uint32_t* nr = P.nplane + i * Wp;
+    const uint32_t* xr = P.xplane + i * 2 * Wp;
+    const uint32_t* nr = P.nplane + i * 2 * Wp;
     for (int feed = 0; feed < (P.regress ? 1 : 2); ++feed) {
       const int c = P.regress ? 0 : (feed == 0 ? y : neg);
       const int target = feed == 0 ? 1 : 0;

@@ -334,11 +334,13 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       sl = gm & (0u - gm);  // this step's lane bit
       gm ^= sl;
       cd = __shfl_sync(kFull, code, l);
-      const size_t row = static_cast<size_t>(cd < 0 ? ~cd : cd) * P.Wp + lane;
+      // Literal rows are [x words | !x words] (2 * Wp words, nplane = xplane
+      // + Wp): one address, both planes at compile-time offsets.
+      const uint32_t* rp = P.xplane + static_cast<size_t>(cd < 0 ? ~cd : cd) * (64 * NW) + lane;
 #pragma unroll
       for (int p = 0; p < NW; ++p) {
-        xs[p] = __ldg(P.xplane + row + p * 32);
-        ns[p] = __ldg(P.nplane + row + p * 32);
+        xs[p] = __ldg(rp + p * 32);
+        ns[p] = __ldg(rp + 32 * NW + p * 32);
       }
     };
     auto run = [&](const uint32_t (&xs)[NW], const uint32_t (&ns)[NW], int cd, uint32_t sl) {
@@ -460,8 +462,8 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
       uint32_t x[NW], n[NW];
 #pragma unroll
       for (int p = 0; p < NW; ++p) {
-        x[p] = P.xplane[i * P.Wp + p * 32 + lane];
-        n[p] = P.nplane[i * P.Wp + p * 32 + lane];
+        x[p] = P.xplane[i * 2 * P.Wp + p * 32 + lane];
+        n[p] = P.nplane[i * 2 * P.Wp + p * 32 + lane];
       }
       const bool type2 = forced ? job.forced == 2 : target == 0;
       const int evald = cl.eval_train(x, n);

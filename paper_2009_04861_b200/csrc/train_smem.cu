@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
       uint32_t x[NW], n[NW];
 #pragma unroll
       for (int p = 0; p < NW; ++p) {
-        x[p] = __ldg(P.xplane + is * Wp + p * 32 + lane);
-        n[p] = __ldg(P.nplane + is * Wp + p * 32 + lane);
+        x[p] = __ldg(P.xplane + is * 2 * Wp + p * 32 + lane);
+        n[p] = __ldg(P.nplane + is * 2 * Wp + p * 32 + lane);
       }
       const int before = eval_train_smem<NW, B>(S, x, n, lane);
       int after = before;
