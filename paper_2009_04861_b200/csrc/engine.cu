@@ -6,6 +6,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -124,10 +125,10 @@ struct DevBuf {
 
 // Supported words-per-lane instantiations of the training kernels.
 int round_nw(int nw) {
-  static const int kNW[] = {1, 2, 3, 4, 8, 10};
+  static const int kNW[] = {1, 2, 3, 4, 6, 8, 10, 12, 16};
   for (int v : kNW)
     if (nw <= v) return v;
-  fail(TMG_EINVAL, "feature count too large for the register-resident clause kernels (max 10240)");
+  fail(TMG_EINVAL, "feature count too large for the register-resident clause kernels (max 16384)");
 }
 
 int planes_for(int N) {
@@ -412,7 +413,9 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
   if (with_delta) p.tally_delta = pool->delta.ptr;
   int blocks = 0;
   // Register-resident clauses up to 4 words per lane per part (o <= 4096);
-  // wider rows keep the automata in shared memory.
+  // wider rows keep the automata in shared memory. (A variant splitting each
+  // wide clause over 2-4 warps with register-resident slices measured 3-11 %
+  // slower at IMDb shape, round 1, and was dropped.)
   const bool ok = tm->NW <= 4 ? tmg::train_async_launch(p, tm->B, tm->NW, tm->stream, &blocks)
                               : tmg::train_async_smem_launch(p, tm->B, tm->NW, tm->stream, &blocks);
   if (!ok) fail(TMG_ERUNTIME, "no async kernel instantiation for this shape");
@@ -1131,11 +1134,9 @@ TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, con
     const size_t lc = static_cast<size_t>(bank) * tm->n_loc + (j - tm->j_begin);
     const uint32_t g = static_cast<uint32_t>(bank) * tm->n + j;
     uint32_t* st = tm->state.ptr + lc * tm->B * 2 * tm->Wp;
-    const bool ok = tm->NW <= 4
-                        ? tmg::type_i_async_once_launch(p, st, g, example, clause_output ? 1 : 0, tm->B, tm->NW,
-                                                        tm->stream)
-                        : tmg::type_i_smem_once_launch(p, st, g, example, clause_output ? 1 : 0, tm->B, tm->NW,
-                                                       tm->stream);
+    const int out = clause_output ? 1 : 0;
+    const bool ok = tm->NW <= 4 ? tmg::type_i_async_once_launch(p, st, g, example, out, tm->B, tm->NW, tm->stream)
+                                : tmg::type_i_smem_once_launch(p, st, g, example, out, tm->B, tm->NW, tm->stream);
     if (!ok)
       fail(TMG_EINVAL, "async Type I probe not instantiated for this shape");
     CK(cudaGetLastError());

@@ -15,236 +15,13 @@
 //                  reference xoshiro streams, bit-exact (sync mirror mode).
 #include <cstdio>
 
+#include "clause.cuh"
 #include "kernels.h"
 #include "tm_device.cuh"
-
-#ifndef TMG_ASYNC_P2
-#define TMG_ASYNC_P2 1  // fused saturation when N = 2^(B-1)
-#endif
-#ifndef TMG_ASYNC_UNROLL_NW
-#define TMG_ASYNC_UNROLL_NW 1  // widest rows (words per lane) that get the 2x unrolled step loop
-#endif
-#ifndef TMG_ALIAS
-#define TMG_ALIAS 1  // alias-table sampler for clause-output-0 Type I draws
-#endif
 
 namespace tmg {
 
 namespace {
-
-template <int NW, int B, bool P2 = false>  // P2: N = 2^(B-1) (lo = 0, hi = all ones)
-struct Clause {
-  Planes<B> s[2][NW];  // [part][pass]
-  uint32_t valid[NW];  // literal bits that exist (f < o)
-
-  __device__ __forceinline__ void load(const uint32_t* base, int Wp, int lane, int o) {
-#pragma unroll
-    for (int p = 0; p < NW; ++p) {
-      const int wi = p * 32 + lane;
-      const int first = wi * 32;
-      valid[p] = first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
-#pragma unroll
-      for (int part = 0; part < 2; ++part)
-#pragma unroll
-        for (int b = 0; b < B; ++b) s[part][p].p[b] = base[(b * 2 + part) * Wp + wi];
-    }
-  }
-
-  __device__ __forceinline__ void store(uint32_t* base, int Wp, int lane) const {
-#pragma unroll
-    for (int p = 0; p < NW; ++p)
-#pragma unroll
-      for (int part = 0; part < 2; ++part)
-#pragma unroll
-        for (int b = 0; b < B; ++b) base[(b * 2 + part) * Wp + p * 32 + lane] = s[part][p].p[b];
-  }
-
-  bool nonempty = false;  // include count > 0, refreshed by every eval_train
-
-  // Train-mode evaluation (core.hpp:208-219): empty clause -> 1.
-  __device__ __forceinline__ int eval_train(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) {
-    uint32_t viol = 0, any = 0;
-#pragma unroll
-    for (int p = 0; p < NW; ++p) {
-      const uint32_t ix = s[0][p].p[B - 1], in = s[1][p].p[B - 1];
-      viol |= (ix & ~x[p]) | (in & ~n[p]);
-      any |= ix | in;
-    }
-    const unsigned vb = __ballot_sync(kFull, viol != 0);
-    nonempty = __any_sync(kFull, any != 0);
-    return !nonempty ? 1 : (vb == 0 ? 1 : 0);
-  }
-
-  // Same, reusing the include-set emptiness of the last eval_train (valid
-  // while the automata have not moved since).
-  __device__ __forceinline__ int eval_cached(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) const {
-    uint32_t viol = 0;
-#pragma unroll
-    for (int p = 0; p < NW; ++p) viol |= (s[0][p].p[B - 1] & ~x[p]) | (s[1][p].p[B - 1] & ~n[p]);
-    const unsigned vb = __ballot_sync(kFull, viol != 0);
-    return !nonempty ? 1 : (vb == 0 ? 1 : 0);
-  }
-
-  __device__ __forceinline__ void refresh_nonempty() {
-    uint32_t any = 0;
-#pragma unroll
-    for (int p = 0; p < NW; ++p) any |= s[0][p].p[B - 1] | s[1][p].p[B - 1];
-    nonempty = __any_sync(kFull, any != 0);
-  }
-
-  __device__ __forceinline__ int include_count() const {
-    int cnt = 0;
-#pragma unroll
-    for (int p = 0; p < NW; ++p) cnt += __popc(s[0][p].p[B - 1]) + __popc(s[1][p].p[B - 1]);
-#pragma unroll
-    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
-    return cnt;
-  }
-
-  // Type II (feedback.cpp:72-83): with output 1, every excluded automaton of
-  // a false literal takes a Penalty (+1). Excluded states sit below the top
-  // plane, so no saturation is possible. Returns whether anything moved.
-  __device__ __forceinline__ bool type_ii(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) {
-    uint32_t moved = 0;
-#pragma unroll
-    for (int p = 0; p < NW; ++p) {
-#pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        const uint32_t lit = part ? n[p] : x[p];
-        const uint32_t inc = ~lit & ~s[part][p].p[B - 1] & valid[p];
-        add_one<B>(s[part][p], inc);
-        moved |= inc;
-      }
-    }
-    return __any_sync(kFull, moved != 0);
-  }
-
-  // Type I (feedback.cpp:32-70) given per-word Bernoulli masks:
-  //   out=1, lit=1 : +1 w.p. (s-1)/s  (always if boost and included)
-  //   out=1, lit=0 : Reward w.p. 1/s  (-1 if excluded; +1 if included, which
-  //                  only a caller-forced output can reach, feedback.cpp:55-57)
-  //   out=0        : -1 w.p. 1/s       (Penalty on Include, Reward on Exclude)
-  __device__ __forceinline__ void type_i_word(int part, int p, uint32_t lit, int out, int boost,
-                                              uint32_t bern, uint32_t lo, uint32_t hi) {
-    Planes<B>& w = s[part][p];
-    if (out) {
-      const uint32_t incl = w.p[B - 1];
-      const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid[p];
-      const uint32_t dec = ~lit & bern & ~incl & valid[p];
-      if (P2) {  // inc and dec lanes are disjoint
-        add_one_sat1<B>(w, inc);
-        sub_one_sat0<B>(w, dec);
-      } else {
-        step<B>(w, inc, dec, lo, hi);
-      }
-    } else if (P2) {
-      sub_one_sat0<B>(w, bern & valid[p]);
-    } else {
-      step_down<B>(w, bern & valid[p], lo);
-    }
-  }
-};
-
-__device__ __forceinline__ uint64_t splitmix_dev(uint64_t x) {
-  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  return z ^ (z >> 31);
-}
-
-// Publishes the post-feedback output (pool.cpp:93-106); one lane.
-__device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row, int64_t i, int c,
-                                       bool positive, uint32_t pword, int after) {
-  const uint32_t bit = 1u << (i & 31);
-  const int before = (pword & bit) ? 1 : 0;
-  if (before == after) return;
-  prev_row[i >> 5] = pword ^ bit;
-  int delta = after ? 1 : -1;
-  if (!positive) delta = -delta;
-  atomicAdd(&P.tallies[i * P.m + c], delta);
-  if (P.tally_delta) atomicAdd(&P.tally_delta[i * P.m + c], delta);
-}
-
-// --------------------------------------------------------------- async ---
-
-// Type I (feedback.cpp:32-70) on every word of the clause with the exact
-// warp-cooperative Bernoulli sampler; counters keyed (clause g, example i,
-// literal word, block) so the draws do not depend on scheduling.
-template <int NW, int B, bool P2>
-__device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
-                                             int before, const TrainParams& P, uint32_t g, uint32_t i,
-                                             int lane, const uint32_t* atab) {
-  constexpr int K = 2 * NW;
-  uint32_t need[K], sel[K], bern[K];
-#pragma unroll
-  for (int p = 0; p < NW; ++p) {
-    need[2 * p] = need[2 * p + 1] = cl.valid[p];
-    sel[2 * p] = x[p];
-    sel[2 * p + 1] = n[p];
-  }
-  auto gen = [&](int slot, int blk) {
-    const uint32_t wid = slot < K ? static_cast<uint32_t>(((slot >> 1) * 32 + lane) * 2 + (slot & 1))
-                                  : (0xFFFF0000u | static_cast<uint32_t>(lane));
-    return philox4x32(U4{g, i, wid, static_cast<uint32_t>(blk)}, P.rkey);
-  };
-#ifdef TMG_STATS
-  if (P.dbg) {
-    // Draws whose outcome cannot move the automaton (a step into the
-    // saturated end it already sits at): histogram of the warp maximum per
-    // lane and the warp total, per clause output (tools/draw_stats.py).
-    int cnt = 0;
-#pragma unroll
-    for (int p = 0; p < NW; ++p)
-#pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        const Planes<B>& w = cl.s[part][p];
-        const uint32_t lit = part ? n[p] : x[p];
-        const uint32_t at_lo = eq_const<B>(w, P.lo), at_hi = eq_const<B>(w, P.hi), incl = w.p[B - 1];
-        const uint32_t rel = before ? ((lit & ~at_hi) | (~lit & ~incl & ~at_lo)) : ~at_lo;
-        cnt += __popc(rel & cl.valid[p]);
-      }
-    const int mx = __reduce_max_sync(kFull, cnt), sum = __reduce_add_sync(kFull, cnt);
-    if (lane == 0) {
-      unsigned long long* d = P.dbg + (before ? 128 : 0);
-      atomicAdd(d + min(mx, 63), 1ULL);
-      atomicAdd(d + 64, 1ULL);
-      atomicAdd(d + 65, static_cast<unsigned long long>(sum));
-      atomicAdd(d + 66, static_cast<unsigned long long>(mx));
-    }
-  }
-#endif
-#if TMG_ALIAS
-  if (before && !P.alias_sel) {
-    bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
-  } else {
-    alias_words<K>(need, atab, static_cast<uint32_t>(lane) & (kAliasCopies - 1), bern, gen);
-    // Clause output 1: a true literal fires w.p. p_high = 1 - p_low, a false
-    // one w.p. p_low, so one Bernoulli(p_low) bit serves either, negated on
-    // the true literals (independence across literals is untouched).
-    if (before) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) bern[k] = (bern[k] ^ sel[k]) & need[k];
-    }
-  }
-#else
-  if (before) bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
-  else bernoulli_words<K, false>(need, sel, P.bern, bern, gen);
-#endif
-#pragma unroll
-  for (int p = 0; p < NW; ++p) {
-    cl.type_i_word(0, p, x[p], before, P.boost, bern[2 * p], P.lo, P.hi);
-    cl.type_i_word(1, p, n[p], before, P.boost, bern[2 * p + 1], P.lo, P.hi);
-  }
-}
-
-// Copies the machine's alias table (P.alias8, 256 entries) into kAliasCopies
-// interleaved shared-memory copies; every thread of the CTA takes part.
-__device__ __forceinline__ void load_alias(const TrainParams& P, uint32_t* tab) {
-#if TMG_ALIAS
-  for (int k = threadIdx.x; k < 256 * kAliasCopies; k += blockDim.x) tab[k] = __ldg(P.alias8 + k / kAliasCopies);
-  __syncthreads();
-#endif
-}
 
 // Resident CTAs (4 warps each) per SM for one instantiation: as many as the
 // register file allows for the clause planes (2*NW*B registers), the literal
@@ -270,17 +47,13 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
   const bool positive = P.all_positive || (j & 1) == 0;
-  const int64_t q = P.q;
-  const int T = P.margin;
 
   Clause<NW, B, P2> cl;
   uint32_t* st = P.state + static_cast<size_t>(lc) * B * 2 * P.Wp;
   cl.load(st, P.Wp, lane, P.o);
   cl.refresh_nonempty();
   uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
-  // Per-clause starting position in the epoch order (trainer.cpp:41-44, 222-223).
-  const int64_t offset = static_cast<int64_t>(splitmix_dev(static_cast<uint64_t>(g) + 1) %
-                                              static_cast<uint64_t>(q));
+  const int64_t offset = clause_offset_dev(g, P.q);
   unsigned long long events = 0, events_type1 = 0;
 
   for (int64_t t0 = P.t_begin; t0 < P.t_end; t0 += 32) {
@@ -289,28 +62,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
     const int64_t t = t0 + lane;
     int64_t i = 0;
     int target = 0;  // 1: the step would take Type I feedback, 0: Type II
-    bool gated = false;
-    if (t < P.t_end) {
-      int64_t pos = offset + t;
-      if (pos >= q) pos -= q;
-      i = P.order ? __ldg(P.order + pos) : pos;
-      const int label = __ldg(P.labels + i);
-      int v = __ldcg(P.tallies + i * P.m + c);  // relaxed, L2-coherent read
-      int64_t e;
-      if (P.regress) {  // regression.cpp:46-67, 204-206
-        v = v < 0 ? 0 : (v > T ? T : v);
-        e = label > v ? static_cast<int64_t>(label) - v : static_cast<int64_t>(v) - label;
-        target = v < label ? 1 : 0;
-      } else {  // trainer.cpp:118-126
-        const int y = label == c ? 1 : 0;
-        v = v < -T ? -T : (v > T ? T : v);
-        e = y ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
-        target = (y == 1) == positive ? 1 : 0;
-      }
-      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.rkey);
-      // u < e / 2T  <=>  r * 2T < e * 2^32  (exact integer gate, feedback.cpp:24-28)
-      gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
-    }
+    const bool gated = t < P.t_end && gate_step(P, c, positive, g, offset, t, i, target);
     unsigned gm = __ballot_sync(kFull, gated);
     if (!gm) continue;
     events += __popc(gm);
@@ -643,8 +395,11 @@ bool dispatch_mirror(const TrainParams& p, const MirrorParams& mp, int NW, cudaS
     case 2: launch_mirror<2, B>(p, mp, s); return true;
     case 3: launch_mirror<3, B>(p, mp, s); return true;
     case 4: launch_mirror<4, B>(p, mp, s); return true;
+    case 6: launch_mirror<6, B>(p, mp, s); return true;
     case 8: launch_mirror<8, B>(p, mp, s); return true;
     case 10: launch_mirror<10, B>(p, mp, s); return true;
+    case 12: launch_mirror<12, B>(p, mp, s); return true;
+    case 16: launch_mirror<16, B>(p, mp, s); return true;
     default: return false;
   }
 }

@@ -7,10 +7,15 @@
 #include "kernels.h"
 #include "tm_device.cuh"
 
+#ifndef TMG_SMEM_UNROLL
+#define TMG_SMEM_UNROLL 2  // word pairs of a Type I feedback processed together (ILP at low occupancy)
+#endif
+
 namespace tmg {
 
 namespace {
 
+constexpr int kSmemUnroll = TMG_SMEM_UNROLL;
 constexpr int kSmemWarps = 2;  // clauses (warps) per CTA
 
 __device__ __forceinline__ uint64_t splitmix_dev2(uint64_t x) {
@@ -63,7 +68,7 @@ template <int NW, int B, bool P2>
 __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
                                             int before, const TrainParams& P, uint32_t g, uint32_t i32, int lane,
                                             const uint32_t* atab) {
-#pragma unroll 1
+#pragma unroll kSmemUnroll
   for (int p = 0; p < NW; ++p) {
     const int w = p * 32 + lane;
     const uint32_t vm = valid_of(w, P.o);
@@ -296,18 +301,22 @@ bool type_i_smem_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, 
 #define TMG_SONCE(nw, b)                                                           \
   if (NW == nw && B == b)                                                          \
     return p2 ? go(type_i_smem_once_kernel<nw, b, true>) : go(type_i_smem_once_kernel<nw, b, false>);
-  TMG_SONCE(8, 4) TMG_SONCE(8, 8) TMG_SONCE(8, 15) TMG_SONCE(10, 4) TMG_SONCE(10, 8) TMG_SONCE(10, 15)
+  TMG_SONCE(6, 4) TMG_SONCE(6, 8) TMG_SONCE(6, 15) TMG_SONCE(8, 4) TMG_SONCE(8, 8) TMG_SONCE(8, 15)
+  TMG_SONCE(10, 4) TMG_SONCE(10, 8) TMG_SONCE(10, 15) TMG_SONCE(12, 4) TMG_SONCE(12, 8) TMG_SONCE(12, 15)
+  TMG_SONCE(16, 4) TMG_SONCE(16, 8) TMG_SONCE(16, 15)
 #undef TMG_SONCE
   return false;
 }
 
 bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
-  if (NW == 8 && B == 8) return launch_smem<8, 8>(p, s, blocks);
-  if (NW == 10 && B == 8) return launch_smem<10, 8>(p, s, blocks);
-  if (NW == 8 && B == 15) return launch_smem<8, 15>(p, s, blocks);
-  if (NW == 10 && B == 15) return launch_smem<10, 15>(p, s, blocks);
-  if (NW == 8 && B == 4) return launch_smem<8, 4>(p, s, blocks);
-  if (NW == 10 && B == 4) return launch_smem<10, 4>(p, s, blocks);
+#define TMG_SMEM(nw_)                                        \
+  if (NW == nw_) {                                           \
+    if (B == 4) return launch_smem<nw_, 4>(p, s, blocks);    \
+    if (B == 8) return launch_smem<nw_, 8>(p, s, blocks);    \
+    if (B == 15) return launch_smem<nw_, 15>(p, s, blocks);  \
+  }
+  TMG_SMEM(6) TMG_SMEM(8) TMG_SMEM(10) TMG_SMEM(12) TMG_SMEM(16)
+#undef TMG_SMEM
   return false;
 }
 

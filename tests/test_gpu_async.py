@@ -135,6 +135,31 @@ def test_two_clause_shards_one_gpu():
     assert acc_sharded > acc_single - 0.03, (acc_sharded, acc_single)
 
 
+@pytest.mark.parametrize("o", [5000, 15000])
+def test_async_epoch_invariants_very_wide(o):
+    """6- and 16-word-per-lane shared-memory clause kernels on random
+    prototype data: tally invariant, counter range, exact refresh."""
+    rng = np.random.default_rng(o)
+    m, q, n = 3, 256, 8
+    protos = rng.random((m, o)) < 0.3
+    y = rng.integers(0, m, q).astype(np.int32)
+    x = (protos[y] ^ (rng.random((q, o)) < 0.1)).astype(np.uint8)
+    tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=10, specificity=5.0, seed=2), o, m)
+    pool = T.ExamplePool(o, x, y, m)
+    for e in range(2):
+        rep = T.train_epoch_parallel(tm, pool, 1, e)
+        assert rep.total_feedback_events() > 0
+        _check_tally_invariant(tm, pool, m, q)
+    cs = np.stack([tm.banks[c].counters() for c in range(m)])
+    assert cs.min() >= 1 and cs.max() <= 256
+    T.refresh_tallies(pool, tm)
+    ref = O.Machine(o, m, n, 128)
+    ref.set_counters(cs)
+    rpool = O.Pool(x, y, m)
+    O.refresh_tallies(ref, rpool)
+    assert np.array_equal(pool.tallies(), rpool.tallies)
+
+
 def test_async_window_accounting():
     """Windows of a pass compose to the full pass (multi-GPU building block)."""
     d = synth.make("xor", 1000, 10, 5, 0.1)
@@ -197,7 +222,7 @@ def test_type_i_table1_conformance(o, N, s, boost, out):
                                          (12, 128, 3.9, False), (40, 5, 2.0, True), (2352, 128, 15.0, False),
                                          (1500, 300, 7.5, False), (2000, 128, 1.0, False),
                                          (5000, 128, 15.0, False), (10000, 128, 15.0, True),
-                                         (9000, 100, 25.0, False)])
+                                         (9000, 100, 25.0, False), (15000, 128, 10.0, False)])
 def test_async_type_i_bit_exact(o, N, s, boost):
     """The asynchronous Type I draw (Philox counters (clause, example) under the
     epoch key; alias-table patterns, or the exact bit-serial sampler when
