@@ -160,6 +160,45 @@ def test_async_epoch_invariants_very_wide(o):
     assert np.array_equal(pool.tallies(), rpool.tallies)
 
 
+def test_async_gate_zero_at_margin():
+    """SPEC acceptance 2 on the asynchronous kernel: a step whose clamped
+    class sum already sits at the margin (v = T for the label class, v = -T
+    for the others) is never fed back (e = 0, feedback.cpp:24-28). Tallies
+    preset far beyond +-T stay clamped there whatever the clauses do, so the
+    whole epoch must report zero feedback events."""
+    d = synth.make("mnist", 1000, 16, 2009)
+    T_ = 20
+    tm = T.MultiClassTM(T.TMConfig(clauses=100, margin=T_, specificity=10.0, seed=8), 784, 10)
+    pool = T.ExamplePool(784, d.train_x, d.train_y, 10)
+    tal = np.full((1000, 10), -100000, np.int32)
+    tal[np.arange(1000), d.train_y] = 100000
+    pool.set_tallies(tal)
+    rep = T.train_epoch_parallel(tm, pool, 1, 0)
+    assert rep.total_feedback_events() == 0
+    # one notch inside the margin for the label class only: every example of
+    # class c gates its class-c clauses with probability 1/(2T) > 0
+    tal[np.arange(1000), d.train_y] = T_ - 1
+    pool.set_tallies(tal)
+    tm.reset()
+    rep = T.train_epoch_parallel(tm, pool, 1, 1)
+    assert 0 < rep.total_feedback_events() < 1000 * 100 // 4
+
+
+def test_async_contended_tallies_lose_no_update():
+    """SPEC acceptance 6 (lost-update freedom) at GPU scale: 4 examples, 2
+    classes x 2000 clauses, so every tally takes thousands of concurrent
+    atomic adds per epoch; the tally invariant must hold exactly."""
+    rng = np.random.default_rng(6)
+    x = (rng.random((4, 64)) < 0.5).astype(np.uint8)
+    y = np.array([0, 1, 0, 1], np.int32)
+    tm = T.MultiClassTM(T.TMConfig(clauses=2000, margin=1000, specificity=3.0, seed=6), 64, 2)
+    pool = T.ExamplePool(64, x, y, 2)
+    for e in range(3):
+        rep = T.train_epoch_parallel(tm, pool, 1, e)
+        assert rep.total_feedback_events() > 4000
+        _check_tally_invariant(tm, pool, 2, 4)
+
+
 def test_async_window_accounting():
     """Windows of a pass compose to the full pass (multi-GPU building block)."""
     d = synth.make("xor", 1000, 10, 5, 0.1)
