@@ -217,10 +217,15 @@ def run_ours(args):
     from paper_2009_04861_b200.tsetlin import int_peak, kernel_launches, machine_stream
 
     rank, world, local = dist_env()
+    if args.share_device:  # protocol test: every rank on cuda:0 (gloo; NCCL rejects duplicate GPUs)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(args.dist_backend)
 
     def barrier():
         if world > 1:
@@ -397,6 +402,9 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--windows", type=int, default=16, help="tally all-reduce windows per epoch (N>1; 16 costs ~2%% on one GPU, tools/window_cost.py)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (tests: gloo)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="run every rank on cuda:0 (one-GPU test of the N>1 protocol; not a measurement)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

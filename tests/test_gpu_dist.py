@@ -1,0 +1,102 @@
+"""The multi-GPU clause-sharding protocol through torch.distributed with the
+REAL GPU engine: two processes (gloo, both on cuda:0 because NCCL refuses
+duplicate GPUs and this box has one), GpuShardEngine + torch_allreduce over
+CUDA tensors, two epochs; then replicas equal, the tally invariant over both
+shards, and sharded class sums equal to the oracle's on the merged machine.
+Also runs bench.py's N>1 path the same way (the driver's torchrun launch)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+O_FEAT, M, N, Q = 784, 10, 60, 1500
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_04861_b200 as T
+    from paper_2009_04861_b200 import distributed as D
+    from paper_2009_04861_b200 import synth
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    d = synth.make("mnist", Q, 300, 2009)
+    jb, je = D.shard_range(N, rank, world)
+    tm = T.MultiClassTM(T.TMConfig(clauses=N, margin=20, specificity=10.0, seed=3), O_FEAT, M, clause_range=(jb, je))
+    pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M)
+    eng = D.GpuShardEngine(tm, pool)
+    for e in range(2):
+        D.train_epoch_windows(eng, e, windows=5, allreduce=D.torch_allreduce())
+    np.save(os.path.join(out_dir, f"tallies{rank}.npy"), pool.tallies())
+    np.save(os.path.join(out_dir, f"prev{rank}.npy"), np.stack([tm.banks[c].prev_outputs() for c in range(M)]))
+    np.save(os.path.join(out_dir, f"counters{rank}.npy"), np.stack([tm.banks[c].counters() for c in range(M)]))
+    test = T.ExamplePool(O_FEAT, d.test_x, d.test_y, M)
+    part = torch.from_numpy(T.class_sums(tm, test).astype(np.int64))
+    dist.all_reduce(part)
+    np.save(os.path.join(out_dir, f"sums{rank}.npy"), part.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _bits(prev, q):
+    b = np.unpackbits(prev.view(np.uint8), axis=-1, bitorder="little")
+    return b[..., :q].astype(np.int64)
+
+
+def test_gpu_shards_two_processes(tmp_path):
+    import torch.multiprocessing as mp
+
+    from paper_2009_04861_b200 import distributed as D
+    from paper_2009_04861_b200 import synth
+    world = 2
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    t0, t1 = np.load(tmp_path / "tallies0.npy"), np.load(tmp_path / "tallies1.npy")
+    assert np.array_equal(t0, t1), "replicas diverged after the final all-reduce"
+    expect = np.zeros((Q, M), np.int64)
+    for r in range(world):
+        jb, je = D.shard_range(N, r, world)
+        bits = _bits(np.load(tmp_path / f"prev{r}.npy"), Q)  # m x n_loc x q
+        for c in range(M):
+            for jl in range(je - jb):
+                j = jb + jl
+                expect[:, c] += bits[c, jl] if j % 2 == 0 else -bits[c, jl]
+    assert np.array_equal(t0, expect)
+    assert np.abs(t0).sum() > 0
+    counters = np.concatenate([np.load(tmp_path / f"counters{r}.npy") for r in range(world)], axis=1)
+    merged = O.Machine(O_FEAT, M, N, 128)
+    merged.set_counters(counters)
+    d = synth.make("mnist", Q, 300, 2009)
+    full = merged.class_sums(O.pack_literals(d.test_x))
+    assert np.array_equal(np.load(tmp_path / "sums0.npy"), full)
+    assert np.array_equal(np.load(tmp_path / "sums1.npy"), full)
+
+
+def test_bench_two_ranks_protocol():
+    """bench.py under torchrun with 2 ranks (gloo, shared device): one JSON
+    line from rank 0 with n_gpus = 2 and a positive value."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(REPO, "bench.py"),
+           "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-cpu", "--dist-backend", "gloo", "--share-device"]
+    out = subprocess.run(cmd, check=True, capture_output=True, text=True, timeout=900, cwd=REPO).stdout
+    lines = [json.loads(l) for l in out.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
+    assert lines[0]["config"]["clauses_per_class_total"] == 4000
