@@ -17,6 +17,10 @@
 #include "kernels.h"
 #include "tm_device.cuh"
 
+#ifndef TMG_EVAL_STAGE
+#define TMG_EVAL_STAGE 4  // (r1au: 4 -> 1.22 ms, 32 -> 1.48, unstaged 1.33) clauses whose include lists a CTA stages in shared memory at a time
+#endif
+
 namespace tmg {
 
 namespace {
@@ -59,7 +63,7 @@ __global__ void build_entries_kernel(const uint32_t* __restrict__ state, int cla
 template <bool TRAIN, int kTile>
 __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
   constexpr int kTS = kTile + 1;
-  extern __shared__ uint32_t tile[];  // [2][Wx][kTS]
+  extern __shared__ uint32_t tile[];  // [2][Wx][kTS], then P.stage staged clauses' entries
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTile;
@@ -85,31 +89,50 @@ __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
   const int jl1 = min(jl0 + P.chunk, P.n_loc);
   const uint32_t* xs = tile + tid;
   const uint32_t* ns = tile + P.Wx * kTS + tid;
+  // Clause include-word lists are staged P.stage clauses at a time (every
+  // warp copies whole lists, coalesced), so the evaluation loop reads them
+  // from shared memory instead of a dependent global load per clause.
+  uint4* sent = reinterpret_cast<uint4*>(tile + ((2 * P.Wx * kTS + 3) & ~3));
+  int* sne = reinterpret_cast<int*>(sent + static_cast<size_t>(P.stage) * P.Wx);
+  const int warp = tid >> 5, nwarps = kTile >> 5;
   int sum = 0;
-  for (int jl = jl0; jl < jl1; ++jl) {
-    const int lc = c * P.n_loc + jl;
-    const int ne = __ldg(P.nentries + lc);
-    int out;
-    if (ne == 0) {
-      out = TRAIN ? 1 : 0;  // empty-clause convention (core.hpp:211-213)
-    } else {
-      const EvalEntry* en = P.entries + static_cast<size_t>(lc) * P.Wx;
-      uint32_t viol = 0;
-      for (int k = 0; k < ne; k += 4) {
-        const int kend = min(k + 4, ne);
-        for (int kk = k; kk < kend; ++kk) {
-          const uint4 ent = __ldg(reinterpret_cast<const uint4*>(en + kk));
-          viol |= (ent.y & ~xs[ent.x * kTS]) | (ent.z & ~ns[ent.x * kTS]);
-        }
-        if (__all_sync(kFull, viol != 0 || !live)) break;
-      }
-      out = viol == 0 ? 1 : 0;
+  for (int jb = jl0; jb < jl1; jb += P.stage) {
+    const int nb = min(P.stage, jl1 - jb);
+    __syncthreads();  // the previous block's lists are consumed
+    for (int cs = warp; cs < nb; cs += nwarps) {
+      const int lc = c * P.n_loc + jb + cs;
+      const int ne = __ldg(P.nentries + lc);
+      const uint4* src = reinterpret_cast<const uint4*>(P.entries + static_cast<size_t>(lc) * P.Wx);
+      for (int k = lane; k < ne; k += 32) sent[cs * P.Wx + k] = __ldg(src + k);
+      if (lane == 0) sne[cs] = ne;
     }
-    const int j = P.j_begin + jl;
-    sum += (!P.all_positive && (j & 1)) ? -out : out;
-    if (TRAIN && P.prev != nullptr) {  // refresh_tallies also rewrites previous outputs
-      const unsigned bits = __ballot_sync(kFull, live && out);
-      if (lane == 0 && i < P.q) P.prev[static_cast<size_t>(lc) * P.Wq + (i >> 5)] = bits;
+    __syncthreads();
+    for (int cs = 0; cs < nb; ++cs) {
+      const int jl = jb + cs;
+      const int lc = c * P.n_loc + jl;
+      const int ne = sne[cs];
+      int out;
+      if (ne == 0) {
+        out = TRAIN ? 1 : 0;  // empty-clause convention (core.hpp:211-213)
+      } else {
+        const uint4* en = sent + cs * P.Wx;
+        uint32_t viol = 0;
+        for (int k = 0; k < ne; k += 4) {
+          const int kend = min(k + 4, ne);
+          for (int kk = k; kk < kend; ++kk) {
+            const uint4 ent = en[kk];
+            viol |= (ent.y & ~xs[ent.x * kTS]) | (ent.z & ~ns[ent.x * kTS]);
+          }
+          if (__all_sync(kFull, viol != 0 || !live)) break;
+        }
+        out = viol == 0 ? 1 : 0;
+      }
+      const int j = P.j_begin + jl;
+      sum += (!P.all_positive && (j & 1)) ? -out : out;
+      if (TRAIN && P.prev != nullptr) {  // refresh_tallies also rewrites previous outputs
+        const unsigned bits = __ballot_sync(kFull, live && out);
+        if (lane == 0 && i < P.q) P.prev[static_cast<size_t>(lc) * P.Wq + (i >> 5)] = bits;
+      }
     }
   }
   if (live) atomicAdd(P.sums + i * P.m + c, sum);
@@ -289,11 +312,15 @@ void eval_sums_launch(const EvalParams& p, bool train_mode, cudaStream_t s) {
   const int chunks = (p.n_loc + p.chunk - 1) / p.chunk;
   auto go = [&](auto kern, int tile) {
     dim3 grid(blocks_for(p.q, tile), p.m * chunks);
-    const size_t shm = sizeof(uint32_t) * 2 * p.Wx * (tile + 1);
+    EvalParams q = p;
+    // ~16 KB of staged include lists per CTA (at least one clause).
+    q.stage = std::max(1, std::min(TMG_EVAL_STAGE, static_cast<int>((16 * 1024) / (16 * std::max(1, p.Wx)))));
+    const size_t shm = sizeof(uint32_t) * ((2 * p.Wx * (tile + 1) + 3) & ~3) +
+                       sizeof(uint4) * static_cast<size_t>(q.stage) * p.Wx + sizeof(int) * q.stage;
     if (shm > 48 * 1024)
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
     count_launch();
-    kern<<<grid, tile, shm, s>>>(p);
+    kern<<<grid, tile, shm, s>>>(q);
   };
   const bool wide = sizeof(uint32_t) * 2 * p.Wx * 129 > 200 * 1024;
   if (train_mode) {

@@ -101,6 +101,7 @@ struct EvalParams {
   const int32_t* inc_count;  // [m*n_loc]
   uint32_t* prev;            // refresh mode: [m*n_loc][Wq]
   int32_t n_loc, j_begin, m, Wx, Wp, Wq, chunk;
+  int32_t stage;  // clauses whose include lists are staged in shared memory at a time (set at launch)
   int32_t all_positive;  // regression head: every clause votes +1
   const uint32_t* xplane;
   const uint32_t* nplane;

@@ -23,6 +23,12 @@ CASES = {
                            noise=0.4, data_seed=7, workers=1),
     "mnist_q6000": dict(data="mnist", q=6000, qtest=2000, clauses=2000, T=50, s=10.0, epochs=3,
                         noise=0.0, data_seed=2009),
+    # BASELINE.json configs[2] / [3] shapes at the full clause counts, on a
+    # training prefix the reference finishes in minutes.
+    "fmnist_q1000": dict(data="fmnist", q=1000, qtest=2000, clauses=8000, T=100, s=15.0, epochs=2,
+                         noise=0.0, data_seed=2352),
+    "imdb_q4000": dict(data="imdb", q=4000, qtest=2000, clauses=10000, T=100, s=15.0, epochs=2,
+                       noise=0.0, data_seed=10000),
 }
 
 

@@ -336,6 +336,30 @@ def test_async_accuracy_parity_xor(case, tol):
     assert gpu >= lo - tol
 
 
+@pytest.mark.parametrize("case,kind", [("fmnist_q1000", "fmnist"), ("imdb_q4000", "imdb")])
+def test_async_accuracy_parity_wide(case, kind):
+    """BASELINE.json configs[2]/[3] shapes (FMNIST 2352 bits x 8000 clauses,
+    IMDb 10 000 bits x 10 000 clauses, the shared-memory clause kernel) vs the
+    reference's parallel trainer on the same training prefix, 5 seeds."""
+    ref = _ref_acc().get(case)
+    if ref is None:
+        pytest.skip("accuracy_ref.json lacks " + case)
+    cfgd = ref["config"]
+    d = synth.make(kind, cfgd["q"], cfgd["qtest"], cfgd["data_seed"])
+    accs = []
+    for seed in range(1, 6):
+        tm = T.MultiClassTM(T.TMConfig(clauses=cfgd["clauses"], margin=cfgd["T"], specificity=cfgd["s"],
+                                       seed=seed), d.features, d.classes)
+        pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes)
+        test = T.ExamplePool(d.features, d.test_x, d.test_y, d.classes)
+        for e in range(cfgd["epochs"]):
+            T.train_epoch_parallel(tm, pool, 1, e)
+        accs.append(T.evaluate_accuracy(tm, test))
+    gpu, cpu = float(np.mean(accs)), ref["mean_final"]
+    print(f"{case}: gpu mean {gpu:.4f} vs reference mean {cpu:.4f} (per-seed {accs})")
+    assert gpu >= cpu - 0.005  # BASELINE.json: <= 0.5 pt, mean over 5 seeds
+
+
 def test_async_accuracy_parity_mnist():
     ref = _ref_acc().get("mnist_q6000")
     if ref is None:
