@@ -16,8 +16,9 @@
 //     bit-exactly (sync-mirror kernel); workers > 1 runs Algorithm 1 over all
 //     clauses concurrently (the asynchronous GPU kernel), which, like the
 //     reference's multi-threaded trainer, is not bit-reproducible.
-//   * PolarityScheme::AllPositive banks (the regression head) are not yet
-//     supported on the device and are rejected with std::invalid_argument.
+//   * PolarityScheme::AllPositive banks are the regression head's
+//     (RegressionHead, regression.cpp) and run on the device's regression
+//     kernels (tmg_machine_create_regress).
 #pragma once
 
 #include <cstdint>

@@ -125,10 +125,12 @@ struct DevBuf {
 
 // Supported words-per-lane instantiations of the training kernels.
 int round_nw(int nw) {
+  // Compiled widths first (register-held rows); wider rows take the
+  // runtime-width shared-memory kernel (train_smem.cu, NW = 0) as they are.
   static const int kNW[] = {1, 2, 3, 4, 6, 8, 10, 12, 16};
   for (int v : kNW)
     if (nw <= v) return v;
-  fail(TMG_EINVAL, "feature count too large for the register-resident clause kernels (max 16384)");
+  return nw;
 }
 
 int planes_for(int N) {
@@ -305,6 +307,12 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->Wx = words_x(o);
     tm->Wp = wp_for(o);
     tm->NW = tm->Wp / 32;
+    // Rows wider than 4 words per lane keep a clause's automata in shared
+    // memory (train_smem.cu): B x 2 x Wp words plus the 16 KB alias table.
+    if (tm->NW > 4 && sizeof(uint32_t) * (static_cast<size_t>(tm->B) * 2 * tm->Wp + 256 * 16) > 227 * 1024)
+      fail(TMG_EINVAL, "feature count too large: one clause's automata exceed shared memory (max " +
+                           std::to_string(((227 * 1024 / 4 - 4096) / (2 * tm->B)) / 32 * 32 * 32) + " features at " +
+                           std::to_string(tm->B) + " planes)");
     tm->device = device;
     tm->all_positive = all_positive ? 1 : 0;
     CK(cudaStreamCreateWithFlags(&tm->stream, cudaStreamNonBlocking));

@@ -1,9 +1,15 @@
-// train_smem.cu — Algorithm 1 for wide literal rows (IMDb-shaped, 2o up to
-// ~20k literals): the same per-warp clause pass as train_async_kernel
+// train_smem.cu — Algorithm 1 for wide literal rows (IMDb-shaped, 2o above
+// 8192 literals): the same per-warp clause pass as train_async_kernel
 // (train.cu), but the clause's automaton planes live in shared memory
 // (B x 2 x Wp words per warp, 20 KB at IMDb) instead of registers, and the
 // feedback walks the clause one 32-literal word pair per lane at a time, so
 // register use does not grow with the feature count.
+//
+// NW > 0: the step's literal row is held in registers (6..16 words per lane,
+// up to 16 384 features). NW == 0: any width — the row stays in global
+// memory (L1-cached) and is read where it is used, and a CTA holds one or two
+// clauses depending on what fits in shared memory.
+#include "clause.cuh"
 #include "kernels.h"
 #include "tm_device.cuh"
 
@@ -16,14 +22,7 @@ namespace tmg {
 namespace {
 
 constexpr int kSmemUnroll = TMG_SMEM_UNROLL;
-constexpr int kSmemWarps = 2;  // clauses (warps) per CTA
-
-__device__ __forceinline__ uint64_t splitmix_dev2(uint64_t x) {
-  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  return z ^ (z >> 31);
-}
+constexpr size_t kSmemMax = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 
 template <int B>
 struct SmemPlanes {
@@ -40,15 +39,45 @@ struct SmemPlanes {
   __device__ __forceinline__ uint32_t top(int part, int w) const { return s[((B - 1) * 2 + part) * Wp + w]; }
 };
 
+// A step's literal row as seen by one lane: words p*32 + lane of the x- and
+// !x-planes, p < words(). Held in registers for a compile-time width.
+template <int NW>
+struct LitRow {
+  uint32_t xw[NW], nw_[NW];
+  __device__ __forceinline__ void load(const uint32_t* rp, int Wp) {
+#pragma unroll
+    for (int p = 0; p < NW; ++p) {
+      xw[p] = __ldg(rp + p * 32);
+      nw_[p] = __ldg(rp + Wp + p * 32);
+    }
+  }
+  __device__ __forceinline__ uint32_t x(int p) const { return xw[p]; }
+  __device__ __forceinline__ uint32_t n(int p) const { return nw_[p]; }
+  __device__ __forceinline__ int words() const { return NW; }
+};
+
+// Runtime width: the row stays in global memory and is read on use.
+template <>
+struct LitRow<0> {
+  const uint32_t* rp;
+  int Wp;
+  __device__ __forceinline__ void load(const uint32_t* r, int w) {
+    rp = r;
+    Wp = w;
+  }
+  __device__ __forceinline__ uint32_t x(int p) const { return __ldg(rp + p * 32); }
+  __device__ __forceinline__ uint32_t n(int p) const { return __ldg(rp + Wp + p * 32); }
+  __device__ __forceinline__ int words() const { return Wp >> 5; }
+};
+
 template <int NW, int B>
-__device__ __forceinline__ int eval_train_smem(const SmemPlanes<B>& S, const uint32_t (&x)[NW],
-                                               const uint32_t (&n)[NW], int lane) {
+__device__ __forceinline__ int eval_train_smem(const SmemPlanes<B>& S, const LitRow<NW>& r, int lane) {
   uint32_t viol = 0, any = 0;
 #pragma unroll
-  for (int p = 0; p < NW; ++p) {
+  for (int p = 0; p < r.words(); ++p) {
     const int w = p * 32 + lane;
     const uint32_t ix = S.top(0, w), in = S.top(1, w);
-    viol |= (ix & ~x[p]) | (in & ~n[p]);
+    viol |= (ix & ~r.x(p)) | (in & ~r.n(p));
     any |= ix | in;
   }
   const unsigned vb = __ballot_sync(kFull, viol != 0), ab = __ballot_sync(kFull, any != 0);
@@ -61,19 +90,18 @@ __device__ __forceinline__ uint32_t valid_of(int w, int o) {
 }
 
 // Type I (feedback.cpp:32-70) on a shared-memory clause, one word pair per
-// lane at a time, with the register kernel's draws (train.cu type_i_async):
+// lane at a time, with the register kernel's draws (clause.cuh type_i_async):
 // alias patterns from Philox counters (clause, example, 2*word + part, 0),
 // or the bit-serial sampler when p_high != 1 - p_low.
 template <int NW, int B, bool P2>
-__device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
-                                            int before, const TrainParams& P, uint32_t g, uint32_t i32, int lane,
-                                            const uint32_t* atab) {
+__device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& r, int before, const TrainParams& P,
+                                            uint32_t g, uint32_t i32, int lane, const uint32_t* atab) {
 #pragma unroll kSmemUnroll
-  for (int p = 0; p < NW; ++p) {
+  for (int p = 0; p < r.words(); ++p) {
     const int w = p * 32 + lane;
     const uint32_t vm = valid_of(w, P.o);
     const uint32_t need[2] = {vm, vm};
-    const uint32_t sel[2] = {x[p], n[p]};
+    const uint32_t sel[2] = {r.x(p), r.n(p)};
     uint32_t bern[2];
     auto gen = [&](int slot, int blk) {
       const uint32_t wid = slot < 2 ? static_cast<uint32_t>(w * 2 + slot)
@@ -115,60 +143,42 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const uint32_t (&x
   __syncwarp();
 }
 
+// One warp per clause, blockDim.x / 32 clauses per CTA; dynamic shared memory
+// = the clauses' planes, then kAliasCopies copies of the alias table.
 template <int NW, int B, bool P2>
-__global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(TrainParams P) {
+__global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
   extern __shared__ uint32_t smem[];
   const int Wp = P.Wp;
+  const int cpb = blockDim.x >> 5;
   const size_t words = static_cast<size_t>(B) * 2 * Wp;
-  uint32_t* atab = smem + kSmemWarps * words;  // alias table copies after the clause planes
+  uint32_t* atab = smem + cpb * words;
   for (int k = threadIdx.x; k < 256 * kAliasCopies; k += blockDim.x) atab[k] = __ldg(P.alias8 + k / kAliasCopies);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int lc = blockIdx.x * kSmemWarps + wib;
+  const int lc = blockIdx.x * cpb + wib;
   if (lc >= P.m * P.n_loc) return;
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
   const bool positive = P.all_positive || (j & 1) == 0;
-  const int64_t q = P.q;
-  const int T = P.margin;
   SmemPlanes<B> S{smem + wib * words, Wp};
   uint32_t* st = P.state + static_cast<size_t>(lc) * words;
   for (size_t k = lane; k < words; k += 32) S.s[k] = st[k];
   __syncwarp();
   uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
-  const int64_t offset = static_cast<int64_t>(splitmix_dev2(static_cast<uint64_t>(g) + 1) % static_cast<uint64_t>(q));
+  const int64_t offset = clause_offset_dev(g, P.q);
   unsigned long long events = 0, events_type1 = 0;
 
   for (int64_t t0 = P.t_begin; t0 < P.t_end; t0 += 32) {
     const int64_t t = t0 + lane;
     int64_t i = 0;
     int target = 0;
-    bool gated = false;
-    if (t < P.t_end) {
-      int64_t pos = offset + t;
-      if (pos >= q) pos -= q;
-      i = P.order ? __ldg(P.order + pos) : pos;
-      const int label = __ldg(P.labels + i);
-      int v = __ldcg(P.tallies + i * P.m + c);
-      int64_t e;
-      if (P.regress) {  // regression.cpp:46-67
-        v = v < 0 ? 0 : (v > T ? T : v);
-        e = label > v ? static_cast<int64_t>(label) - v : static_cast<int64_t>(v) - label;
-        target = v < label ? 1 : 0;
-      } else {
-        const int y = label == c ? 1 : 0;
-        v = v < -T ? -T : (v > T ? T : v);
-        e = y ? static_cast<int64_t>(T) - v : static_cast<int64_t>(T) + v;
-        target = (y == 1) == positive ? 1 : 0;
-      }
-      const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.rkey);
-      gated = static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
-    }
+    const bool gated = t < P.t_end && gate_step(P, c, positive, g, offset, t, i, target);
     unsigned gm = __ballot_sync(kFull, gated);
     if (!gm) continue;
     events += __popc(gm);
+    events_type1 += __popc(__ballot_sync(kFull, gated && target));
     // Lane-owned bookkeeping, published after the window (see train.cu).
     uint32_t prevbit = 0;
     if (gated) prevbit = (__ldcg(prev_row + (i >> 5)) >> (i & 31)) & 1u;
@@ -179,25 +189,20 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
       gm &= gm - 1;
       const int cd = __shfl_sync(kFull, code, sl);
       const int64_t is = cd < 0 ? ~cd : cd;
-      const int tg = cd < 0;
-      uint32_t x[NW], n[NW];
-#pragma unroll
-      for (int p = 0; p < NW; ++p) {
-        x[p] = __ldg(P.xplane + is * 2 * Wp + p * 32 + lane);
-        n[p] = __ldg(P.nplane + is * 2 * Wp + p * 32 + lane);
-      }
-      const int before = eval_train_smem<NW, B>(S, x, n, lane);
+      LitRow<NW> r;
+      r.load(P.xplane + is * 2 * Wp + lane, Wp);
+      const int before = eval_train_smem<NW, B>(S, r, lane);
       int after = before;
-      if (tg == 0) {  // Type II (feedback.cpp:72-83)
+      if (cd >= 0) {  // Type II (feedback.cpp:72-83)
         if (before) {
           uint32_t moved = 0;
 #pragma unroll
-          for (int p = 0; p < NW; ++p) {
+          for (int p = 0; p < r.words(); ++p) {
             const int w = p * 32 + lane;
             const uint32_t vm = valid_of(w, P.o);
 #pragma unroll
             for (int part = 0; part < 2; ++part) {
-              const uint32_t inc = ~(part ? n[p] : x[p]) & ~S.top(part, w) & vm;
+              const uint32_t inc = ~(part ? r.n(p) : r.x(p)) & ~S.top(part, w) & vm;
               if (inc) {
                 Planes<B> pl;
                 S.get(part, w, pl);
@@ -208,17 +213,15 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
             }
           }
           __syncwarp();
-          if (__any_sync(kFull, moved != 0)) after = eval_train_smem<NW, B>(S, x, n, lane);
+          if (__any_sync(kFull, moved != 0)) after = eval_train_smem<NW, B>(S, r, lane);
         }
       } else {  // Type I (feedback.cpp:32-70), one word pair at a time
-        ++events_type1;
-        type_i_smem<NW, B, P2>(S, x, n, before, P, g, static_cast<uint32_t>(is), lane, atab);
-        __syncwarp();
-        after = eval_train_smem<NW, B>(S, x, n, lane);
+        type_i_smem<NW, B, P2>(S, r, before, P, g, static_cast<uint32_t>(is), lane, atab);
+        after = eval_train_smem<NW, B>(S, r, lane);
       }
       outs |= static_cast<unsigned>(after) << sl;
     }
-    if (gated && ((outs >> lane) & 1u) != prevbit) {
+    if (gated && ((outs >> lane) & 1u) != prevbit) {  // pool.cpp:93-106
       atomicXor(prev_row + (i >> 5), 1u << (i & 31));
       int delta = prevbit ? -1 : 1;
       if (!positive) delta = -delta;
@@ -242,24 +245,31 @@ __global__ void __launch_bounds__(32 * kSmemWarps) train_async_smem_kernel(Train
   }
 }
 
+size_t smem_bytes(int B, int Wp, int cpb) {
+  return sizeof(uint32_t) * (static_cast<size_t>(cpb) * B * 2 * Wp + 256 * kAliasCopies);
+}
+
 template <int NW, int B, bool P2>
-void launch_smem_p2(const TrainParams& p, cudaStream_t s, int grid, size_t shm) {
+bool launch_smem_p2(const TrainParams& p, cudaStream_t s, int* blocks) {
+  // Two clauses per CTA where they fit, else one; none: the row is too wide.
+  const int cpb = smem_bytes(B, p.Wp, 2) <= kSmemMax ? 2 : 1;
+  const size_t shm = smem_bytes(B, p.Wp, cpb);
+  if (shm > kSmemMax) return false;
+  const int clauses = p.m * p.n_loc;
+  const int grid = (clauses + cpb - 1) / cpb;
+  if (blocks) *blocks = grid;
   if (shm > 48 * 1024)
     cudaFuncSetAttribute(train_async_smem_kernel<NW, B, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(shm));
   count_launch();
-  train_async_smem_kernel<NW, B, P2><<<grid, 32 * kSmemWarps, shm, s>>>(p);
+  train_async_smem_kernel<NW, B, P2><<<grid, 32 * cpb, shm, s>>>(p);
+  return true;
 }
 
 template <int NW, int B>
 bool launch_smem(const TrainParams& p, cudaStream_t s, int* blocks) {
-  const int clauses = p.m * p.n_loc;
-  const int grid = (clauses + kSmemWarps - 1) / kSmemWarps;
-  const size_t shm = sizeof(uint32_t) * (kSmemWarps * B * 2 * p.Wp + 256 * kAliasCopies);
-  if (blocks) *blocks = grid;
-  if (p.lo == 0 && p.hi == (1u << B) - 1u) launch_smem_p2<NW, B, true>(p, s, grid, shm);
-  else launch_smem_p2<NW, B, false>(p, s, grid, shm);
-  return true;
+  if (p.lo == 0 && p.hi == (1u << B) - 1u) return launch_smem_p2<NW, B, true>(p, s, blocks);
+  return launch_smem_p2<NW, B, false>(p, s, blocks);
 }
 
 // One Type I feedback of the shared-memory path on the clause planes at
@@ -276,22 +286,22 @@ __global__ void __launch_bounds__(32) type_i_smem_once_kernel(TrainParams P, uin
   for (size_t k = lane; k < words; k += 32) smem[k] = state[k];
   __syncwarp();
   SmemPlanes<B> S{smem, P.Wp};
-  uint32_t x[NW], n[NW];
-#pragma unroll
-  for (int p = 0; p < NW; ++p) {
-    x[p] = P.xplane[p * 32 + lane];
-    n[p] = P.nplane[p * 32 + lane];
-  }
-  type_i_smem<NW, B, P2>(S, x, n, out, P, g, i, lane, atab);
+  LitRow<NW> r;
+  r.load(P.xplane + lane, P.Wp);
+  type_i_smem<NW, B, P2>(S, r, out, P, g, i, lane, atab);
   for (size_t k = lane; k < words; k += 32) state[k] = smem[k];
 }
+
+// Row widths (words per lane) with a register-held literal row.
+bool compiled_width(int NW) { return NW == 6 || NW == 8 || NW == 10 || NW == 12 || NW == 16; }
 
 }  // namespace
 
 bool type_i_smem_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, uint32_t i, int out, int B, int NW,
                              cudaStream_t s) {
   const bool p2 = p.lo == 0 && p.hi == (1u << B) - 1u;
-  const size_t shm = sizeof(uint32_t) * (static_cast<size_t>(B) * 2 * p.Wp + 256 * kAliasCopies);
+  const size_t shm = smem_bytes(B, p.Wp, 1);
+  if (shm > kSmemMax) return false;
   auto go = [&](auto kern) {
     if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
     count_launch();
@@ -305,17 +315,23 @@ bool type_i_smem_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, 
   TMG_SONCE(10, 4) TMG_SONCE(10, 8) TMG_SONCE(10, 15) TMG_SONCE(12, 4) TMG_SONCE(12, 8) TMG_SONCE(12, 15)
   TMG_SONCE(16, 4) TMG_SONCE(16, 8) TMG_SONCE(16, 15)
 #undef TMG_SONCE
+  if (!compiled_width(NW)) {
+    if (B == 4) return p2 ? go(type_i_smem_once_kernel<0, 4, true>) : go(type_i_smem_once_kernel<0, 4, false>);
+    if (B == 8) return p2 ? go(type_i_smem_once_kernel<0, 8, true>) : go(type_i_smem_once_kernel<0, 8, false>);
+    if (B == 15) return p2 ? go(type_i_smem_once_kernel<0, 15, true>) : go(type_i_smem_once_kernel<0, 15, false>);
+  }
   return false;
 }
 
 bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
+  const int nw = compiled_width(NW) ? NW : 0;
 #define TMG_SMEM(nw_)                                        \
-  if (NW == nw_) {                                           \
+  if (nw == nw_) {                                           \
     if (B == 4) return launch_smem<nw_, 4>(p, s, blocks);    \
     if (B == 8) return launch_smem<nw_, 8>(p, s, blocks);    \
     if (B == 15) return launch_smem<nw_, 15>(p, s, blocks);  \
   }
-  TMG_SMEM(6) TMG_SMEM(8) TMG_SMEM(10) TMG_SMEM(12) TMG_SMEM(16)
+  TMG_SMEM(6) TMG_SMEM(8) TMG_SMEM(10) TMG_SMEM(12) TMG_SMEM(16) TMG_SMEM(0)
 #undef TMG_SMEM
   return false;
 }

@@ -135,9 +135,10 @@ def test_two_clause_shards_one_gpu():
     assert acc_sharded > acc_single - 0.03, (acc_sharded, acc_single)
 
 
-@pytest.mark.parametrize("o", [5000, 15000])
+@pytest.mark.parametrize("o", [5000, 15000, 20000])
 def test_async_epoch_invariants_very_wide(o):
-    """6- and 16-word-per-lane shared-memory clause kernels on random
+    """Shared-memory clause kernels at 6 and 16 words per lane and the
+    runtime-width instantiation (20 000 features, 20 words per lane) on random
     prototype data: tally invariant, counter range, exact refresh."""
     rng = np.random.default_rng(o)
     m, q, n = 3, 256, 8
@@ -261,7 +262,8 @@ def test_type_i_table1_conformance(o, N, s, boost, out):
                                          (12, 128, 3.9, False), (40, 5, 2.0, True), (2352, 128, 15.0, False),
                                          (1500, 300, 7.5, False), (2000, 128, 1.0, False),
                                          (5000, 128, 15.0, False), (10000, 128, 15.0, True),
-                                         (9000, 100, 25.0, False), (15000, 128, 10.0, False)])
+                                         (9000, 100, 25.0, False), (15000, 128, 10.0, False),
+                                         (20000, 128, 10.0, False), (40000, 5, 3.0, True)])
 def test_async_type_i_bit_exact(o, N, s, boost):
     """The asynchronous Type I draw (Philox counters (clause, example) under the
     epoch key; alias-table patterns, or the exact bit-serial sampler when
