@@ -207,6 +207,32 @@ def inference_line(args, tm, d, local, stream):
     return out
 
 
+def other_configs(local):
+    """BASELINE.json configs[2] and [3] on this GPU: one fresh async epoch
+    (after one untimed one) of the FMNIST- and IMDb-shaped workloads,
+    device time on the engine stream. Reported beside the headline; the
+    parity tests cover their accuracy."""
+    import paper_2009_04861_b200 as T
+    from paper_2009_04861_b200 import synth
+    out = []
+    for kind, q, n, T_, s_, seed in (("fmnist", 60000, 8000, 100, 15.0, 2352), ("imdb", 25000, 10000, 100, 15.0, 10000)):
+        d = synth.make(kind, q, 0, seed)
+        tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=T_, specificity=s_, seed=TM_SEED), d.features, d.classes,
+                            device=local)
+        pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes, device=local)
+        for r in range(2):
+            tm.reset()
+            pool.reset_tallies()
+            rep = T.train_epoch_parallel(tm, pool, 1, 0)
+        t = rep.device_seconds
+        out.append({"workload": f"{kind} {d.features}b x {d.classes}c x {n} clauses, q={q}, fresh epoch 0",
+                    "ms_per_epoch": t * 1e3, "examples_per_s": q / t,
+                    "clause_literal_evals_per_s": d.classes * n * q * 2.0 * d.features / t,
+                    "feedback_events": rep.total_feedback_events()})
+        del tm, pool
+    return out
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -376,6 +402,8 @@ def run_ours(args):
     # file for a bounded row sample, predictions compared row for row.
     if world == 1:
         line["inference"] = inference_line(args, tm, d, local, stream)
+        if not args.no_other_configs:
+            line["other_configs"] = other_configs(local)
     # ---- CPU reference beside it (rank 0, N=1 only)
     if world == 1 and not args.no_cpu and os.path.exists(REF_DRIVER):
         cores = os.cpu_count() or 1
@@ -402,6 +430,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--windows", type=int, default=16, help="tally all-reduce windows per epoch (N>1; 16 costs ~2%% on one GPU, tools/window_cost.py)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the FMNIST/IMDb side measurements")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (tests: gloo)")
     ap.add_argument("--share-device", action="store_true",
                     help="run every rank on cuda:0 (one-GPU test of the N>1 protocol; not a measurement)")

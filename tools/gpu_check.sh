@@ -14,8 +14,8 @@ if [ "${BENCH:-1}" = "1" ]; then
 fi
 if [ "${NCU:-1}" = "1" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
-      --log-file "$out/launches_$tag.csv" python bench.py --steps 2 --warmup 3 --no-cpu > "$out/ncu_launch_bench_$tag.txt" 2>&1
+      --log-file "$out/launches_$tag.csv" python bench.py --steps 2 --warmup 3 --no-cpu --no-other-configs > "$out/ncu_launch_bench_$tag.txt" 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:train_async -s 1 -c 1 \
-      -o "$out/prof_train_$tag" -f python bench.py --steps 1 --warmup 3 --no-cpu > "$out/ncu_full_train_$tag.txt" 2>&1
+      -o "$out/prof_train_$tag" -f python bench.py --steps 1 --warmup 3 --no-cpu --no-other-configs > "$out/ncu_full_train_$tag.txt" 2>&1
 fi
 echo done
