@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtmgpu.so")
+# TMG_LIB selects another build of the engine (tools/build_variants.sh variants).
+LIB_PATH = os.environ.get("TMG_LIB") or os.path.join(HERE, "_lib", "libtmgpu.so")
 
 TMG_OK, TMG_EINVAL, TMG_ERANGE, TMG_ERUNTIME = 0, 1, 2, 3
 MODE_ASYNC, MODE_SYNC_MIRROR = 0, 1

@@ -12,8 +12,6 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2009_04861_b200 import _capi  # noqa: E402
 
-if os.environ.get("TMG_LIB"):
-    _capi.LIB_PATH = os.environ["TMG_LIB"]
 import paper_2009_04861_b200 as T  # noqa: E402
 from paper_2009_04861_b200 import synth  # noqa: E402
 

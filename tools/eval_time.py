@@ -15,8 +15,6 @@ import torch  # noqa: E402
 
 from paper_2009_04861_b200 import _capi  # noqa: E402
 
-if os.environ.get("TMG_LIB"):  # a tools/build_variants.sh build
-    _capi.LIB_PATH = os.environ["TMG_LIB"]
 import paper_2009_04861_b200 as T  # noqa: E402
 from paper_2009_04861_b200 import model_io, synth  # noqa: E402
 from paper_2009_04861_b200.tsetlin import machine_stream  # noqa: E402
