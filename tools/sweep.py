@@ -1,26 +1,74 @@
 #!/usr/bin/env python3
-"""Clause-count sweep (BASELINE.json configs[4]): fresh async epoch-0 time on
-MNIST-shaped data vs clauses per class, plus the FMNIST-/IMDb-shaped configs
-(configs[2], configs[3]) on one GPU. Prints one JSON line per point.
-Usage: python tools/sweep.py [mnist|fmnist|imdb|all] [q]"""
+"""Clause-count sweep (BASELINE.json configs[4]): per
+clauses-per-class point on MNIST-shaped data, the fresh async epoch-0 time
+(training examples/s, clause-literal evals/s), the inference time for the
+test rows (class sums, eval kernel), and — with --ref — the reference's
+train_epoch_parallel on all host cores over a bounded training prefix, so
+every point carries its own x-CPU ratio. Also the FMNIST-/IMDb-shaped
+configs (configs[2], configs[3]). Prints one JSON line per point.
+Usage: python tools/sweep.py [mnist|fmnist|imdb|all] [q] [--ref]"""
 import json
 import os
+import subprocess
 import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import paper_2009_04861_b200 as T  # noqa: E402
-from paper_2009_04861_b200 import synth  # noqa: E402
+import torch  # noqa: E402
 
-what = sys.argv[1] if len(sys.argv) > 1 else "all"
+import paper_2009_04861_b200 as T  # noqa: E402
+from paper_2009_04861_b200 import _capi, synth  # noqa: E402
+from paper_2009_04861_b200.tsetlin import machine_stream  # noqa: E402
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+what = args[0] if args else "all"
+q_arg = int(args[1]) if len(args) > 1 else 60000
+with_ref = "--ref" in sys.argv
+SEEDS = {"mnist": 2009, "fmnist": 2352, "imdb": 10000}
+
+
+def infer_ms(tm, test, qt, m):
+    sums = torch.zeros(qt * m, dtype=torch.int32, device="cuda:0")
+    stream = torch.cuda.ExternalStream(machine_stream(tm), device="cuda:0")
+    best = None
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _capi.check(_capi.lib().tmg_class_sums_device(tm.handle, test.handle, T.PREDICT, sums.data_ptr()))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    return best
+
+
+def ref_point(kind, n, T_, s, q_full, budget_s=8.0):
+    """Reference examples/s on a training prefix sized to ~budget_s of CPU."""
+    cores = os.cpu_count() or 1
+
+    def run(qu):
+        out = subprocess.run([REF, "train", "--data", kind, "--q", str(q_full), "--qtest", "16", "--q-use",
+                              str(qu), "--clauses", str(n), "--T", str(T_), "--s", str(s), "--epochs", "1",
+                              "--workers", str(cores), "--seed", "42", "--data-seed", str(SEEDS[kind]),
+                              "--eval", "0", "--fresh", "1"], check=True, capture_output=True, text=True).stdout
+        return json.loads(out.splitlines()[0])
+
+    probe = run(100)
+    qu = int(max(100, min(q_full, budget_s * 100 / max(probe["seconds"], 1e-6))))
+    r = run(qu) if qu > 100 else probe
+    return {"q_sample": qu, "seconds": r["seconds"], "examples_per_s": r["examples_per_s"], "cores": cores,
+            "feedback_events": r["feedback_events"]}
 
 
 def run(kind, clauses_list, q, qt, T_, s, epochs=2):
-    d = synth.make(kind, q, qt, {"mnist": 2009, "fmnist": 2352, "imdb": 10000}[kind])
+    d = synth.make(kind, q, qt, SEEDS[kind])
     pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes)
-    test = T.ExamplePool(d.features, d.test_x, d.test_y, d.classes)
+    test = T.ExamplePool(d.features, d.test_x, d.test_y, d.classes) if qt else None
+    m, o = d.classes, d.features
     for n in clauses_list:
-        tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=T_, specificity=s, seed=42), d.features, d.classes)
+        tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=T_, specificity=s, seed=42), o, m)
         pool.reset_tallies()
         rows = []
         for e in range(epochs):
@@ -29,15 +77,20 @@ def run(kind, clauses_list, q, qt, T_, s, epochs=2):
             wall = time.perf_counter() - t0
             rows.append({"epoch": e, "kernel_ms": rep.device_seconds * 1e3, "wall_ms": wall * 1e3,
                          "events": rep.total_feedback_events(), "type1": sum(rep.type_i_events)})
-        acc = T.evaluate_accuracy(tm, test) if qt else None
-        m, o = d.classes, d.features
-        print(json.dumps({"config": kind, "clauses_per_class": n, "q": q, "T": T_, "s": s, "epochs": rows,
-                          "test_accuracy": acc,
-                          "clause_literal_evals_per_s_e0": m * n * q * 2 * o / (rows[0]["kernel_ms"] * 1e-3),
-                          "examples_per_s_e0": q / (rows[0]["kernel_ms"] * 1e-3)}), flush=True)
-
-
-q = int(sys.argv[2]) if len(sys.argv) > 2 else 60000
+        line = {"config": kind, "clauses_per_class": n, "q": q, "T": T_, "s": s, "epochs": rows,
+                "clause_literal_evals_per_s_e0": m * n * q * 2 * o / (rows[0]["kernel_ms"] * 1e-3),
+                "examples_per_s_e0": q / (rows[0]["kernel_ms"] * 1e-3)}
+        if test is not None:
+            ims = infer_ms(tm, test, qt, m)
+            line.update({"test_accuracy": T.evaluate_accuracy(tm, test), "infer_ms": ims,
+                         "infer_rows_per_s": qt / (ims * 1e-3),
+                         "infer_clause_literal_evals_per_s": m * n * qt * 2 * o / (ims * 1e-3)})
+        if with_ref and os.path.exists(REF):
+            r = ref_point(kind, n, T_, s, q)
+            line["reference"] = r
+            line["x_reference_examples_per_s"] = line["examples_per_s_e0"] / r["examples_per_s"]
+        print(json.dumps(line), flush=True)
+        del tm
 
 
 def warm_up():
@@ -51,8 +104,9 @@ def warm_up():
 
 warm_up()
 if what in ("mnist", "all"):
-    run("mnist", [20, 100, 200, 500, 1000, 2000, 5000, 7000, 10000], q, 10000, 50, 10.0)
+    run("mnist", [20, 50, 100, 200, 500, 1000, 2000, 5000, 7000, 10000, 20000, 50000, 100000], q_arg, 10000,
+        50, 10.0)
 if what in ("fmnist", "all"):
-    run("fmnist", [8000], q, 10000, 100, 15.0)
+    run("fmnist", [8000], q_arg, 10000, 100, 15.0)
 if what in ("imdb", "all"):
     run("imdb", [10000], 25000, 25000, 100, 15.0)
