@@ -285,7 +285,10 @@ def run_ours(args):
         if world == 1:
             rep = T.train_epoch_parallel(tm, p, 1, 0)
             return rep.feedback_events, rep.type_i_events, rep.device_seconds
-        ev = D.train_epoch_windows(D.GpuShardEngine(tm, p), 0, windows, allreduce)
+        if args.exchange == "overlapped":
+            ev = D.train_epoch_overlapped(tm, p, 0, windows)
+        else:
+            ev = D.train_epoch_windows(D.GpuShardEngine(tm, p), 0, windows, allreduce)
         return ev, None, None
 
     # ---- integer-pipe peak (roofline denominator), measured on this GPU
@@ -360,6 +363,7 @@ def run_ours(args):
                    "clauses_per_class_per_gpu": N_CLAUSES, "clauses_per_class_total": n_total,
                    "T": MARGIN, "s": SPEC, "state_bits": 8, "parallelism": f"clause-shard{world}",
                    "windows": windows if world > 1 else 1,
+                   "exchange": args.exchange if world > 1 else "none",
                    "l2": "flushed (256 MB write) between timed steps; working set (prev bits 150 MB) > L2"},
         "examples_per_s": Q_TRAIN / (ms * 1e-3),
         "feedback_events_per_step": statistics.mean(events),
@@ -432,6 +436,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-other-configs", action="store_true", help="skip the FMNIST/IMDb side measurements")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (tests: gloo)")
+    ap.add_argument("--exchange", choices=["overlapped", "sync"], default="overlapped",
+                    help="N>1 tally exchange: double-buffered on a side stream, or host-synchronous per window")
     ap.add_argument("--share-device", action="store_true",
                     help="run every rank on cuda:0 (one-GPU test of the N>1 protocol; not a measurement)")
     args = ap.parse_args()

@@ -199,6 +199,17 @@ int tmg_train_window(tmg_machine* tm, tmg_pool* pool, int32_t epoch, int64_t t_b
 int tmg_epoch_begin(tmg_machine* tm, tmg_pool* pool, int32_t epoch);
 /* tallies += reduced - own_delta; own_delta = 0. d_reduced: q x m int32 on device. */
 int tmg_pool_apply_reduced(tmg_pool* pool, const void* d_reduced);
+/* Overlapped windows (double-buffered exchange). All three
+ * only ENQUEUE on the machine's stream (tmg_machine_stream) and return:
+ *   tmg_train_window_async     one window, events accumulate since tmg_epoch_begin;
+ *   tmg_window_delta_snapshot  d_snapshot = own delta, own delta = 0;
+ *   tmg_window_apply_remote    tallies += d_reduced - d_snapshot (the remote share
+ *                              of an earlier window, once its all-reduce is done).
+ * tmg_epoch_events synchronises the stream and reads the per-class events. */
+int tmg_train_window_async(tmg_machine* tm, tmg_pool* pool, int32_t epoch, int64_t t_begin, int64_t t_end);
+int tmg_window_delta_snapshot(tmg_machine* tm, tmg_pool* pool, void* d_snapshot);
+int tmg_window_apply_remote(tmg_machine* tm, tmg_pool* pool, const void* d_reduced, const void* d_snapshot);
+int tmg_epoch_events(tmg_machine* tm, uint64_t* feedback_events);
 /* update_clause (trainer.cpp:102-136) with the reference stream: rng_state is
  * the 4-word xoshiro256++ state, advanced in place. order may be NULL (natural
  * order) or hold order_len == q indices. */

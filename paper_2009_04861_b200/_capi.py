@@ -52,6 +52,10 @@ SIGNATURES = {
     "tmg_debug_feedback_rates": (C.c_int, [P, I32, I32, P, I32, C.c_uint32, P, P]),
     "tmg_debug_type_i_async": (C.c_int, [P, I32, I32, P, I32, C.c_uint32, I32]),
     "tmg_debug_counters": (C.c_int, [P, P, I32, I32]),
+    "tmg_train_window_async": (C.c_int, [P, P, I32, I64, I64]),
+    "tmg_window_delta_snapshot": (C.c_int, [P, P, P]),
+    "tmg_window_apply_remote": (C.c_int, [P, P, P, P]),
+    "tmg_epoch_events": (C.c_int, [P, P]),
     "tmg_alias8_table": (C.c_int, [C.c_uint32, P]),
     "tmg_config_default": (None, [C.POINTER(Config)]),
     "tmg_config_validate": (C.c_int, [C.POINTER(Config)]),

@@ -891,6 +891,49 @@ TMG_API int tmg_epoch_begin(tmg_machine* tm, tmg_pool* pool, int32_t epoch) {
     if (tm->q_bound != pool->q) bind(tm, pool->q);
     upload_order(tm, pool, epoch);
     epoch_keys(tm, epoch);
+    CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
+  });
+}
+
+TMG_API int tmg_train_window_async(tmg_machine* tm, tmg_pool* pool, int32_t epoch, int64_t t0, int64_t t1) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    if (tm->cur_epoch != epoch || tm->q_bound != pool->q) fail(TMG_EINVAL, "call tmg_epoch_begin first");
+    if (t0 < 0 || t1 > pool->q || t0 > t1) fail(TMG_ERANGE, "window outside [0, q]");
+    DeviceGuard dg(tm->device);
+    run_async_window(tm, pool, t0, t1, true);
+  });
+}
+
+TMG_API int tmg_window_delta_snapshot(tmg_machine* tm, tmg_pool* pool, void* d_snapshot) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    if (!d_snapshot) fail(TMG_EINVAL, "null snapshot buffer");
+    DeviceGuard dg(tm->device);
+    CK(cudaMemcpyAsync(d_snapshot, pool->delta.ptr, pool->delta.bytes(), cudaMemcpyDeviceToDevice, tm->stream));
+    CK(cudaMemsetAsync(pool->delta.ptr, 0, pool->delta.bytes(), tm->stream));
+  });
+}
+
+TMG_API int tmg_window_apply_remote(tmg_machine* tm, tmg_pool* pool, const void* d_reduced, const void* d_snapshot) {
+  return guarded([&] {
+    check_compatible(M(tm), pool);
+    if (!d_reduced || !d_snapshot) fail(TMG_EINVAL, "null buffer");
+    DeviceGuard dg(tm->device);
+    tmg::apply_snapshot_launch(pool->tallies.ptr, static_cast<const int32_t*>(d_reduced),
+                               static_cast<const int32_t*>(d_snapshot), pool->q * pool->m, tm->stream);
+    CK(cudaGetLastError());
+  });
+}
+
+TMG_API int tmg_epoch_events(tmg_machine* tm, uint64_t* feedback_events) {
+  return guarded([&] {
+    DeviceGuard dg(M(tm)->device);
+    std::vector<unsigned long long> ev(2 * static_cast<size_t>(tm->m));
+    CK(cudaMemcpyAsync(ev.data(), tm->events.ptr, tm->events.bytes(), cudaMemcpyDeviceToHost, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    if (feedback_events)
+      for (int c = 0; c < tm->m; ++c) feedback_events[c] = ev[static_cast<size_t>(c)];
   });
 }
 

@@ -400,6 +400,20 @@ void init_state_launch(uint32_t* state, int clauses, int B, int Wp, cudaStream_t
   }
 }
 
+__global__ void apply_snapshot_kernel(int32_t* __restrict__ tallies, const int32_t* __restrict__ reduced,
+                                      const int32_t* __restrict__ snap, int64_t count) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx < count) tallies[idx] += reduced[idx] - snap[idx];
+}
+
+void apply_snapshot_launch(int32_t* tallies, const int32_t* reduced, const int32_t* snap, int64_t count,
+                           cudaStream_t s) {
+  if (count > 0) {
+    count_launch();
+    apply_snapshot_kernel<<<blocks_for(count, 256), 256, 0, s>>>(tallies, reduced, snap, count);
+  }
+}
+
 void apply_remote_delta_launch(int32_t* tallies, const int32_t* reduced, int32_t* own, int64_t count,
                                cudaStream_t s) {
   if (count > 0) {

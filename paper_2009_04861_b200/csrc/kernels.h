@@ -136,6 +136,8 @@ void init_state_launch(uint32_t* state, int clauses, int B, int Wp, cudaStream_t
 void clamp_launch(const int32_t* sums, int32_t* out, int64_t q, int T, cudaStream_t s);
 void apply_remote_delta_launch(int32_t* tallies, const int32_t* reduced, int32_t* own, int64_t count,
                                cudaStream_t s);
+void apply_snapshot_launch(int32_t* tallies, const int32_t* reduced, const int32_t* snap, int64_t count,
+                           cudaStream_t s);
 // Integer-pipe peak micro-benchmark: returns thread-ops/s for LOP3-only and LOP3+IMAD streams.
 bool int_peak_launch(int sms, double* lop3_ops, double* mixed_ops);
 

@@ -113,6 +113,58 @@ def train_epoch_windows(engine, epoch: int, windows: int, allreduce: Optional[Ca
     return [int(v) for v in total]
 
 
+def train_epoch_overlapped(tm: MultiClassTM, pool: ExamplePool, epoch: int, windows: int, group=None,
+                           comm_stream=None) -> List[int]:
+    """One asynchronous epoch as `windows` windows with the tally exchange
+    double-buffered and overlapped: the window kernels run
+    back to back on the machine's stream; after window w its own deltas are
+    snapshotted (and zeroed) on that stream, all-reduced on a side stream
+    while window w+1 runs, and the remote share (reduced - own) of window w is
+    added before window w+2 — one window more staleness than
+    train_epoch_windows and no host round trip per window. With one rank
+    (group world size 1 / no process group) the exchange is skipped."""
+    import torch
+    import torch.distributed as dist
+
+    from .tsetlin import machine_stream
+    device = pool.device
+    q, m = pool.size(), tm.num_banks()
+    multi = dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    ms = torch.cuda.ExternalStream(machine_stream(tm), device=f"cuda:{device}")
+    cs = comm_stream if comm_stream is not None else torch.cuda.Stream(device=f"cuda:{device}")
+    snaps = [torch.empty(q * m, dtype=torch.int32, device=f"cuda:{device}") for _ in range(2)]
+    reds = [torch.empty_like(snaps[0]) for _ in range(2)]
+    done = [None, None]
+    check(lib().tmg_epoch_begin(tm.handle, pool.handle, epoch))
+    bounds = window_bounds(q, windows)
+    for w, (t0, t1) in enumerate(bounds):
+        b = w % 2
+        check(lib().tmg_train_window_async(tm.handle, pool.handle, epoch, t0, t1))
+        check(lib().tmg_window_delta_snapshot(tm.handle, pool.handle, C.c_void_p(snaps[b].data_ptr())))
+        if multi:
+            ready = torch.cuda.Event()
+            ready.record(ms)
+            with torch.cuda.stream(cs):
+                cs.wait_event(ready)
+                reds[b].copy_(snaps[b])
+                dist.all_reduce(reds[b], op=dist.ReduceOp.SUM, group=group)
+                done[b] = torch.cuda.Event()
+                done[b].record(cs)
+            if w >= 1:
+                p = (w - 1) % 2
+                ms.wait_event(done[p])
+                check(lib().tmg_window_apply_remote(tm.handle, pool.handle, C.c_void_p(reds[p].data_ptr()),
+                                                    C.c_void_p(snaps[p].data_ptr())))
+    if multi and bounds:
+        p = (len(bounds) - 1) % 2
+        ms.wait_event(done[p])
+        check(lib().tmg_window_apply_remote(tm.handle, pool.handle, C.c_void_p(reds[p].data_ptr()),
+                                            C.c_void_p(snaps[p].data_ptr())))
+    ev = np.zeros(m, np.uint64)
+    check(lib().tmg_epoch_events(tm.handle, ev.ctypes.data))
+    return [int(v) for v in ev]
+
+
 def nccl_allreduce(device: int, group=None) -> Callable:
     return torch_allreduce(group)
 

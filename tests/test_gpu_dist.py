@@ -27,7 +27,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, overlapped=False):
     import torch
     import torch.distributed as dist
 
@@ -43,7 +43,10 @@ def _worker(rank, world, port, out_dir):
     pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M)
     eng = D.GpuShardEngine(tm, pool)
     for e in range(2):
-        D.train_epoch_windows(eng, e, windows=5, allreduce=D.torch_allreduce())
+        if overlapped:
+            D.train_epoch_overlapped(tm, pool, e, windows=5)
+        else:
+            D.train_epoch_windows(eng, e, windows=5, allreduce=D.torch_allreduce())
     np.save(os.path.join(out_dir, f"tallies{rank}.npy"), pool.tallies())
     np.save(os.path.join(out_dir, f"prev{rank}.npy"), np.stack([tm.banks[c].prev_outputs() for c in range(M)]))
     np.save(os.path.join(out_dir, f"counters{rank}.npy"), np.stack([tm.banks[c].counters() for c in range(M)]))
@@ -60,13 +63,17 @@ def _bits(prev, q):
     return b[..., :q].astype(np.int64)
 
 
-def test_gpu_shards_two_processes(tmp_path):
+@pytest.mark.parametrize("overlapped", [False, True])
+def test_gpu_shards_two_processes(tmp_path, overlapped):
+    """Synchronous windows (train_epoch_windows) and the double-buffered,
+    overlapped exchange (train_epoch_overlapped) both end each epoch with
+    identical replicas satisfying the invariant over both shards."""
     import torch.multiprocessing as mp
 
     from paper_2009_04861_b200 import distributed as D
     from paper_2009_04861_b200 import synth
     world = 2
-    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path), overlapped), nprocs=world, join=True,
                        start_method="spawn")
     t0, t1 = np.load(tmp_path / "tallies0.npy"), np.load(tmp_path / "tallies1.npy")
     assert np.array_equal(t0, t1), "replicas diverged after the final all-reduce"
