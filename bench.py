@@ -368,6 +368,7 @@ def run_ours(args):
         "examples_per_s": Q_TRAIN / (ms * 1e-3),
         "feedback_events_per_step": statistics.mean(events),
         "feedback_events_per_s": statistics.mean(events) / (ms * 1e-3),
+        "ta_updates_per_s": statistics.mean(events) * 2.0 * O_FEAT / (ms * 1e-3),  # 2o per event
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -381,8 +382,8 @@ def run_ours(args):
         if os.path.exists(tpath):  # the committed ncu --set full summary of this kernel
             prof = json.load(open(tpath))
             traffic = prof.get("dram_bytes_per_launch")
-            hw = {k: prof.get(k) for k in ("pipe_alu_pct", "pipe_fmaheavy_pct", "issue_active_pct", "ipc_active",
-                                           "duration_ms", "source")}
+            hw = {k: prof.get(k) for k in ("pipe_alu_pct", "pipe_fma_pct", "pipe_fmaheavy_pct", "pipe_lsu_inst_pct",
+                                           "issue_active_pct", "ipc_active", "duration_ms", "source")}
         line["roofline"] = {"bound": "int-alu", "achieved": ops / k / 1e12, "peak": mixed_peak / 1e12,
                             "unit": "Tops/s", "frac": ops / k / mixed_peak, "traffic": traffic,
                             "frac_note": "algorithmic ops (SURVEY 8(d) model) / kernel time; >1 = the sampler "
