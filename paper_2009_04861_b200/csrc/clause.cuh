@@ -234,15 +234,17 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32
 // integer form r * 2T < e * 2^32 of u < e / 2T (feedback.cpp:24-28) with the
 // Philox word r of counter (g, i, ~0, 0). The class tally is read relaxed
 // through L2 (deliberately stale, the reference's atomic load).
-__device__ __forceinline__ bool gate_step(const TrainParams& P, int c, bool positive, uint32_t g, int64_t offset,
-                                          int64_t t, int64_t& i, int& target) {
-  const int64_t q = P.q;
-  const int T = P.margin;
+// The example at position offset + t of the epoch order.
+__device__ __forceinline__ int64_t order_at(const TrainParams& P, int64_t offset, int64_t t) {
   int64_t pos = offset + t;
-  if (pos >= q) pos -= q;
-  i = P.order ? __ldg(P.order + pos) : pos;
-  const int label = __ldg(P.labels + i);
-  int v = __ldcg(P.tallies + i * P.m + c);
+  if (pos >= P.q) pos -= P.q;
+  return P.order ? __ldg(P.order + pos) : pos;
+}
+
+// The gate decision from the step's example, label and (stale) tally.
+__device__ __forceinline__ bool gate_decide(const TrainParams& P, int c, bool positive, uint32_t g, int64_t i,
+                                            int label, int v, int& target) {
+  const int T = P.margin;
   int64_t e;
   if (P.regress) {
     v = v < 0 ? 0 : (v > T ? T : v);
@@ -256,6 +258,12 @@ __device__ __forceinline__ bool gate_step(const TrainParams& P, int c, bool posi
   }
   const U4 r = philox4x32(U4{g, static_cast<uint32_t>(i), 0xFFFFFFFFu, 0u}, P.rkey);
   return static_cast<uint64_t>(r.x) * (2 * static_cast<uint64_t>(T)) < (static_cast<uint64_t>(e) << 32);
+}
+
+__device__ __forceinline__ bool gate_step(const TrainParams& P, int c, bool positive, uint32_t g, int64_t offset,
+                                          int64_t t, int64_t& i, int& target) {
+  i = order_at(P, offset, t);
+  return gate_decide(P, c, positive, g, i, __ldg(P.labels + i), __ldcg(P.tallies + i * P.m + c), target);
 }
 
 // Per-clause starting position in the epoch order (trainer.cpp:41-44, 222-223).
