@@ -96,6 +96,51 @@ def test_gpu_shards_two_processes(tmp_path, overlapped):
     assert np.array_equal(np.load(tmp_path / "sums1.npy"), full)
 
 
+def _acc_worker(rank, world, port, out_dir, windows):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_04861_b200 as T
+    from paper_2009_04861_b200 import distributed as D
+    from paper_2009_04861_b200 import synth
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    cfg = json.load(open(os.path.join(REPO, "tests", "golden", "accuracy_ref.json")))["mnist_q6000"]["config"]
+    d = synth.make("mnist", cfg["q"], cfg["qtest"], cfg["data_seed"])
+    accs = []
+    for seed in range(1, 6):
+        jb, je = D.shard_range(cfg["clauses"], rank, world)
+        tm = T.MultiClassTM(T.TMConfig(clauses=cfg["clauses"], margin=cfg["T"], specificity=cfg["s"], seed=seed),
+                            784, 10, clause_range=(jb, je))
+        pool = T.ExamplePool(784, d.train_x, d.train_y, 10)
+        for e in range(cfg["epochs"]):
+            D.train_epoch_overlapped(tm, pool, e, windows=windows)
+        test = T.ExamplePool(784, d.test_x, d.test_y, 10)
+        part = torch.from_numpy(T.class_sums(tm, test).astype(np.int64))
+        dist.all_reduce(part)
+        accs.append(float((part.numpy().argmax(1) == d.test_y).mean()))
+    if rank == 0:
+        json.dump(accs, open(os.path.join(out_dir, "accs.json"), "w"))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_accuracy_parity(tmp_path):
+    """Clause-sharded training (2 ranks x 1000 clauses/class, overlapped
+    16-window exchange, MNIST-shaped q = 6000, 3 epochs, 5 seeds) matches the
+    reference's multi-threaded trainer on the same data within 0.5 pt — the
+    multi-GPU staleness does not cost accuracy."""
+    import torch.multiprocessing as mp
+    ref = json.load(open(os.path.join(REPO, "tests", "golden", "accuracy_ref.json")))["mnist_q6000"]
+    mp.start_processes(_acc_worker, args=(2, _free_port(), str(tmp_path), 16), nprocs=2, join=True,
+                       start_method="spawn")
+    accs = json.load(open(tmp_path / "accs.json"))
+    gpu = float(np.mean(accs))
+    print(f"2-rank sharded: mean {gpu:.4f} vs reference {ref['mean_final']:.4f} (per-seed {accs})")
+    assert gpu >= ref["mean_final"] - 0.005
+
+
 def test_bench_two_ranks_protocol():
     """bench.py under torchrun with 2 ranks (gloo, shared device): one JSON
     line from rank 0 with n_gpus = 2 and a positive value."""
