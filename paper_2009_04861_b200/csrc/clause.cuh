@@ -275,7 +275,7 @@ __device__ __forceinline__ int64_t clause_offset_dev(uint32_t g, int64_t q) {
 // interleaved shared-memory copies; every thread of the CTA takes part.
 __device__ __forceinline__ void load_alias(const TrainParams& P, uint32_t* tab) {
 #if TMG_ALIAS
-  for (int k = threadIdx.x; k < 256 * kAliasCopies; k += blockDim.x) tab[k] = __ldg(P.alias8 + k / kAliasCopies);
+  fill_alias(tab, P.alias8, threadIdx.x, blockDim.x);
   __syncthreads();
 #endif
 }

@@ -211,13 +211,38 @@ __device__ __forceinline__ void add_one_sat1(Planes<B>& s, uint32_t inc) {
 // `tab` holds kAliasCopies interleaved copies of the 256 entries so the 32
 // lanes' random lookups hit at most two shared-memory wavefronts.
 constexpr int kAliasCopies = 16;
+// Shared-memory image of the table: thresholds (threshold << 8, low byte 0)
+// as 256 x kAliasCopies u32, then the alias patterns as 256 x kAliasCopies
+// bytes (20 KB). The threshold test is then a plain u < E (no masking), and
+// the second lookup goes to the lightly used LSU pipe instead of the ALU.
+constexpr int kAliasWords = 256 * kAliasCopies + 256 * kAliasCopies / 4;
 
-template <int K, typename Gen>
+// The packed image (16 KB: entries threshold << 8 | alias as they are),
+// for kernels whose occupancy is bound by shared memory (train_smem.cu).
+constexpr int kAliasWordsPacked = 256 * kAliasCopies;
+__device__ __forceinline__ void fill_alias_packed(uint32_t* tab, const uint32_t* entries, int tid, int n) {
+  for (int k = tid; k < 256 * kAliasCopies; k += n) tab[k] = __ldg(entries + k / kAliasCopies);
+}
+
+// Fills the split image from the machine's 256 packed entries
+// (threshold << 8 | alias), with the n threads of index tid.
+__device__ __forceinline__ void fill_alias(uint32_t* tab, const uint32_t* entries, int tid, int n) {
+  uint8_t* pat = reinterpret_cast<uint8_t*>(tab + 256 * kAliasCopies);
+  for (int k = tid; k < 256 * kAliasCopies; k += n) {
+    const uint32_t e = __ldg(entries + k / kAliasCopies);
+    tab[k] = e & ~0xFFu;
+    pat[k] = static_cast<uint8_t>(e & 0xFFu);
+  }
+}
+
+template <int K, bool SPLIT = true, typename Gen>
 __device__ __forceinline__ void alias_words(const uint32_t (&need)[K], const uint32_t* tab, uint32_t laneoff,
                                             uint32_t (&bern)[K], Gen&& gen) {
-  // Shared-space byte address of this lane's copy of column 0; column c is
-  // 4 * kAliasCopies * c further (one IMAD per lookup, on the FMA pipe).
+  // Shared-space byte addresses of this lane's copies of column 0 (threshold
+  // and pattern); column c is 4 * kAliasCopies * c (kAliasCopies * c) further
+  // (one IMAD per lookup, on the FMA pipe).
   const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 4u * laneoff;
+  const uint32_t pbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab + 256 * kAliasCopies)) + laneoff;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const U4 r = gen(k, 0);
@@ -225,9 +250,16 @@ __device__ __forceinline__ void alias_words(const uint32_t (&need)[K], const uin
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint32_t u = j == 0 ? r.x : (j == 1 ? r.y : (j == 2 ? r.z : r.w));
+      const uint32_t col = u & 0xFFu;
       uint32_t e;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(mad_u32(u & 0xFFu, 4u * kAliasCopies, base)));
-      b[j] = (u | 0xFFu) < e ? u : e;  // low byte: the drawn pattern
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(mad_u32(col, 4u * kAliasCopies, base)));
+      if (SPLIT) {
+        uint32_t a;
+        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(a) : "r"(mad_u32(col, kAliasCopies, pbase)));
+        b[j] = u < e ? u : a;  // (u >> 8) < threshold: the column's own pattern; low byte = the draw
+      } else {
+        b[j] = (u | 0xFFu) < e ? u : e;  // the same test on the packed entry
+      }
     }
     const uint32_t lo = __byte_perm(b[0], b[1], 0x0040), hi = __byte_perm(b[2], b[3], 0x0040);
     bern[k] = __byte_perm(lo, hi, 0x5410) & need[k];

@@ -38,7 +38,7 @@ constexpr int async_min_blocks(int NW, int B) {
 #endif
 template <int NW, int B, bool P2>
 __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
-  __shared__ uint32_t atab[TMG_ALIAS ? 256 * kAliasCopies : 1];
+  __shared__ uint32_t atab[TMG_ALIAS ? kAliasWords : 1];
   load_alias(P, atab);
   const int lane = static_cast<int>(lane_id());
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
                                                              int out, uint32_t trials,
                                                              unsigned long long* inc_cnt,
                                                              unsigned long long* dec_cnt) {
-  __shared__ uint32_t atab[TMG_ALIAS ? 256 * kAliasCopies : 1];
+  __shared__ uint32_t atab[TMG_ALIAS ? kAliasWords : 1];
   load_alias(P, atab);
   const int lane = threadIdx.x & 31;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
 template <int NW, int B, bool P2>
 __global__ void __launch_bounds__(32) type_i_async_once_kernel(TrainParams P, uint32_t* state, uint32_t g,
                                                                uint32_t i, int out) {
-  __shared__ uint32_t atab[TMG_ALIAS ? 256 * kAliasCopies : 1];
+  __shared__ uint32_t atab[TMG_ALIAS ? kAliasWords : 1];
   load_alias(P, atab);
   const int lane = threadIdx.x;
   Clause<NW, B, P2> cl;

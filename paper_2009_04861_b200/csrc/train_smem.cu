@@ -111,7 +111,7 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& 
     if (before && !P.alias_sel) {
       bernoulli_words<2, true>(need, sel, P.bern, bern, gen);
     } else {
-      alias_words<2>(need, atab, static_cast<uint32_t>(lane) & (kAliasCopies - 1), bern, gen);
+      alias_words<2, false>(need, atab, static_cast<uint32_t>(lane) & (kAliasCopies - 1), bern, gen);
       if (before) {
         bern[0] = (bern[0] ^ sel[0]) & need[0];
         bern[1] = (bern[1] ^ sel[1]) & need[1];
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
   const int cpb = blockDim.x >> 5;
   const size_t words = static_cast<size_t>(B) * 2 * Wp;
   uint32_t* atab = smem + cpb * words;
-  for (int k = threadIdx.x; k < 256 * kAliasCopies; k += blockDim.x) atab[k] = __ldg(P.alias8 + k / kAliasCopies);
+  fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
 }
 
 size_t smem_bytes(int B, int Wp, int cpb) {
-  return sizeof(uint32_t) * (static_cast<size_t>(cpb) * B * 2 * Wp + 256 * kAliasCopies);
+  return sizeof(uint32_t) * (static_cast<size_t>(cpb) * B * 2 * Wp + kAliasWordsPacked);
 }
 
 template <int NW, int B, bool P2>
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(32) type_i_smem_once_kernel(TrainParams P, uin
   const int lane = threadIdx.x;
   const size_t words = static_cast<size_t>(B) * 2 * P.Wp;
   uint32_t* atab = smem + words;
-  for (int k = lane; k < 256 * kAliasCopies; k += 32) atab[k] = __ldg(P.alias8 + k / kAliasCopies);
+  fill_alias_packed(atab, P.alias8, lane, 32);
   for (size_t k = lane; k < words; k += 32) smem[k] = state[k];
   __syncwarp();
   SmemPlanes<B> S{smem, P.Wp};
