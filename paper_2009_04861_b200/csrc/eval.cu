@@ -87,8 +87,6 @@ __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
   const int c = blockIdx.y / chunks;
   const int jl0 = (blockIdx.y % chunks) * P.chunk;
   const int jl1 = min(jl0 + P.chunk, P.n_loc);
-  const uint32_t* xs = tile + tid;
-  const uint32_t* ns = tile + P.Wx * kTS + tid;
   // Clause include-word lists are staged P.stage clauses at a time (every
   // warp copies whole lists, coalesced), so the evaluation loop reads them
   // from shared memory instead of a dependent global load per clause.
@@ -103,7 +101,12 @@ __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
       const int lc = c * P.n_loc + jb + cs;
       const int ne = __ldg(P.nentries + lc);
       const uint4* src = reinterpret_cast<const uint4*>(P.entries + static_cast<size_t>(lc) * P.Wx);
-      for (int k = lane; k < ne; k += 32) sent[cs * P.Wx + k] = __ldg(src + k);
+      for (int k = lane; k < ne; k += 32) {
+        uint4 en = __ldg(src + k);
+        en.w = (P.Wx + en.x) * kTS;  // !x-plane row of word w in the tile
+        en.x *= kTS;                 // x-plane row
+        sent[cs * P.Wx + k] = en;
+      }
       if (lane == 0) sne[cs] = ne;
     }
     __syncthreads();
@@ -116,12 +119,15 @@ __global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
         out = TRAIN ? 1 : 0;  // empty-clause convention (core.hpp:211-213)
       } else {
         const uint4* en = sent + cs * P.Wx;
+        const uint32_t* xt = tile + tid;  // this example's column of the tile
         uint32_t viol = 0;
         for (int k = 0; k < ne; k += 4) {
-          const int kend = min(k + 4, ne);
-          for (int kk = k; kk < kend; ++kk) {
-            const uint4 ent = en[kk];
-            viol |= (ent.y & ~xs[ent.x * kTS]) | (ent.z & ~ns[ent.x * kTS]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (k + u < ne) {
+              const uint4 ent = en[k + u];
+              viol |= (ent.y & ~xt[ent.x]) | (ent.z & ~xt[ent.w]);
+            }
           }
           if (__all_sync(kFull, viol != 0 || !live)) break;
         }
