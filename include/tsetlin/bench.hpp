@@ -1,0 +1,4 @@
+// Drop-in replacement for the reference header tsetlin/bench.hpp: declared by
+// tsetlin_b200_data.hpp (implemented in csrc/facade_data.cpp).
+#pragma once
+#include "tsetlin_b200_data.hpp"

@@ -12,3 +12,8 @@ done
 "$repo/oracle/_ref/ref_driver" golden "$here"
 # Transcript of the same-source drop-in driver built against the reference.
 "$repo/oracle/_ref/api_driver_ref" > "$here/api_driver_ref.txt"
+# Transcripts of the host-companion driver (data_io, metrics, bench).
+tmp="$(mktemp -d)"
+"$repo/oracle/_ref/data_driver_ref" host "$tmp" > "$here/data_driver_host_ref.txt" 2>/dev/null
+"$repo/oracle/_ref/data_driver_ref" bench > "$here/data_driver_bench_ref.txt" 2>/dev/null
+rm -rf "$tmp"

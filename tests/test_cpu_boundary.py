@@ -123,3 +123,20 @@ def test_shard_ranges_even_aligned_and_cover():
             assert max(sizes) - min(sizes) <= 2
     assert window_bounds(10, 3) == [(0, 3), (3, 6), (6, 10)]
     assert window_bounds(5, 9) == [(k, k + 1) for k in range(5)]
+
+
+def test_host_companions_match_reference(tmp_path):
+    """data_io.hpp / metrics.hpp / bench CSV of the drop-in (csrc/facade_data.cpp,
+    host code, no GPU): tests/cpp/data_driver.cpp "host" — generators, dense
+    binary and CSV files with their error messages, the binarizer (fit, apply,
+    tmbinarizer v1 round trip), metrics, bench CSV — prints the reference's
+    transcript (tests/golden/data_driver_host_ref.txt) line for line."""
+    import subprocess
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    drv = os.path.join(repo, "paper_2009_04861_b200", "_lib", "data_driver_gpu")
+    out = subprocess.run([drv, "host", str(tmp_path)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    want = [l for l in open(os.path.join(repo, "tests", "golden", "data_driver_host_ref.txt")).read().splitlines()
+            if l.strip()]
+    got = [l for l in out.stdout.splitlines() if l.strip()]
+    assert got == want

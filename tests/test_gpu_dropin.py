@@ -33,6 +33,19 @@ def test_same_source_driver_matches_reference():
     assert len(got) == len(want) and not diffs, f"first differences: {diffs[:5]}"
 
 
+def test_same_source_bench_sweep_matches_reference():
+    """bench.hpp's bench_sweep (f4) on the GPU trainers: tests/cpp/data_driver.cpp
+    "bench" (seq and one-worker par, classification and regression) prints the
+    reference's records (seconds excluded) line for line."""
+    drv = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "data_driver_gpu")
+    out = subprocess.run([drv, "bench"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    want = _lines(open(os.path.join(GOLDEN, "data_driver_bench_ref.txt")).read())
+    got = _lines(out.stdout)
+    diffs = [(w, g) for w, g in zip(want, got) if w != g]
+    assert len(got) == len(want) and not diffs, f"first differences: {diffs[:5]}"
+
+
 @pytest.mark.parametrize("name", EPOCH_CASES)
 def test_sequential_trainer_bit_exact(name):
     """train_epoch_sequential (f1) replayed on the GPU == the reference."""
