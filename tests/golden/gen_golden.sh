@@ -17,3 +17,6 @@ tmp="$(mktemp -d)"
 "$repo/oracle/_ref/data_driver_ref" host "$tmp" > "$here/data_driver_host_ref.txt" 2>/dev/null
 "$repo/oracle/_ref/data_driver_ref" bench > "$here/data_driver_bench_ref.txt" 2>/dev/null
 rm -rf "$tmp"
+# Transcript of the scripted `tm` command-line session (tests/cli_session.py)
+# with our CLI source linked against the reference library.
+(cd "$repo" && python -m tests.cli_session oracle/_ref/tm_ref all > "$here/cli_session_ref.txt")

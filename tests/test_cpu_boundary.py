@@ -140,3 +140,22 @@ def test_host_companions_match_reference(tmp_path):
             if l.strip()]
     got = [l for l in out.stdout.splitlines() if l.strip()]
     assert got == want
+
+
+def _cli_golden(part):
+    lines = open(os.path.join(REPO, "tests", "golden", "cli_session_ref.txt")).read().splitlines()
+    from tests.cli_session import HOST
+    # the host part is the transcript up to the first command of the gpu part
+    n_host = [i for i, l in enumerate(lines) if l.startswith("$ ")][len(HOST)]
+    return lines[:n_host] if part == "host" else lines
+
+
+def test_cli_host_part_matches_reference():
+    """The `tm` command line (f4, cli.cpp:429-530) without a GPU: synth files,
+    parse failures with CLI11's exit codes, validation errors, missing files
+    (exit 2) — the same transcript as our CLI source linked with the reference
+    library (tests/golden/cli_session_ref.txt)."""
+    from tests.cli_session import run
+    tm = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "tm")
+    assert os.path.exists(tm), "build first: make -C paper_2009_04861_b200/csrc"
+    assert run(tm, "host") == _cli_golden("host")

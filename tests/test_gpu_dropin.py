@@ -66,3 +66,41 @@ def test_sequential_trainer_bit_exact(name):
     test = T.ExamplePool(man["o"], load(*d, "test_x.npy"), load(*d, "test_y.npy"), man["m"])
     assert np.array_equal(T.class_sums(tm, test), load(*d, "test_sums.npy"))
     assert np.array_equal(T.predict_all(tm, test), load(*d, "test_pred.npy"))
+
+
+def test_cli_session_matches_reference():
+    """The `tm` command line (f4, cli.cpp:429-530) on the GPU facade: train
+    (seq, one-worker par, TM_THREADS override, classify and regress, dense and
+    CSV input with the binarizer), eval of the saved models, bench CSV — every
+    stdout line and every written file (seconds masked) identical to the same
+    CLI source linked with the reference library."""
+    from tests.cli_session import run
+    from tests.test_cpu_boundary import _cli_golden
+    tm = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "tm")
+    want = _cli_golden("all")
+    ref = os.path.join(REPO, "oracle", "_ref", "tm_ref")
+    if os.path.exists(ref):
+        want = run(ref, "all")
+    got = run(tm, "all")
+    diffs = [(w, g) for w, g in zip(want, got) if w != g]
+    assert len(got) == len(want) and not diffs, f"first differences: {diffs[:5]}"
+
+
+def test_cli_parallel_mode_trains(tmp_path):
+    """`tm train --mode par --workers 8`: the asynchronous all-clause trainer
+    behind the command line (not a replay); learns the synthetic patterns."""
+    tm = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "tm")
+    env = {k: v for k, v in os.environ.items() if k != "TM_THREADS"}
+    p = subprocess.run([tm, "train", "--synth", "patterns", "--synth-train", "2000", "--synth-test", "500",
+                        "--classes", "4", "--clauses", "40", "--epochs", "5", "--mode", "par", "--workers", "8",
+                        "--report", str(tmp_path / "r.csv"), "--out", str(tmp_path / "m.model")],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert p.returncode == 0, p.stderr
+    vals = dict(l.split(" ", 1) for l in p.stdout.splitlines() if " " in l)
+    assert float(vals["test_accuracy"]) >= 0.9, p.stdout
+    rows = open(tmp_path / "r.csv").read().splitlines()
+    assert rows[0] == "mode,workers,clauses,epoch,seconds,metric_name,metric_value"
+    assert len(rows) == 1 + 2 * 5 and all(r.startswith("par,8,40,") for r in rows[1:])
+    e = subprocess.run([tm, "eval", "--model", str(tmp_path / "m.model"), "--data", str(tmp_path / "m.model")],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert e.returncode == 1  # a model file is not a dataset: the loader's runtime_error -> exit 1
