@@ -119,12 +119,12 @@ struct Clause {
     Planes<B>& w = s[part][p];
     if (out) {
       const uint32_t incl = w.p[B - 1];
-      const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid[p];
-      const uint32_t dec = ~lit & bern & ~incl & valid[p];
-      if (P2) {  // inc and dec lanes are disjoint
-        add_one_sat1<B>(w, inc);
-        sub_one_sat0<B>(w, dec);
+      if (P2) {  // one up/down pass: false literals of excluded automata step down
+        const uint32_t move = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern)) & valid[p];
+        step_sat<B>(w, move, ~(lit | incl));
       } else {
+        const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid[p];
+        const uint32_t dec = ~lit & bern & ~incl & valid[p];
         step<B>(w, inc, dec, lo, hi);
       }
     } else if (P2) {

@@ -186,14 +186,21 @@ __device__ __forceinline__ void sub_one_sat0(Planes<B>& s, uint32_t dec) {
   for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
 }
 
+// Both at once (P2 layout): lanes in `move` take one step, down (-1) where
+// `down` is set, up (+1) elsewhere. The chain continues through plane b while
+// that bit equals the direction's ripple value (1 for +1, 0 for -1), i.e.
+// t &= p[b] ^ down: one LOP3 per plane, one more for the flip. What leaves the
+// top plane is the set of lanes already saturated in their direction, which
+// are left untouched -- the same result as a saturating +1 pass then a
+// saturating -1 pass on disjoint masks, at half the cost.
 template <int B>
-__device__ __forceinline__ void add_one_sat1(Planes<B>& s, uint32_t inc) {
+__device__ __forceinline__ void step_sat(Planes<B>& s, uint32_t move, uint32_t down) {
   uint32_t chain[B];
-  uint32_t t = inc;
+  uint32_t t = move;
 #pragma unroll
   for (int b = 0; b < B; ++b) {
     chain[b] = t;
-    t &= s.p[b];
+    t &= s.p[b] ^ down;
   }
 #pragma unroll
   for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;

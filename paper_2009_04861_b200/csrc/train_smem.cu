@@ -124,12 +124,12 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& 
       const uint32_t lit = sel[part];
       if (before) {
         const uint32_t incl = pl.p[B - 1];
-        const uint32_t inc = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part] & incl)) & vm;
-        const uint32_t dec = ~lit & bern[part] & ~incl & vm;
-        if (P2) {
-          add_one_sat1<B>(pl, inc);
-          sub_one_sat0<B>(pl, dec);
+        if (P2) {  // one up/down pass (step_sat)
+          const uint32_t move = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part])) & vm;
+          step_sat<B>(pl, move, ~(lit | incl));
         } else {
+          const uint32_t inc = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part] & incl)) & vm;
+          const uint32_t dec = ~lit & bern[part] & ~incl & vm;
           step<B>(pl, inc, dec, P.lo, P.hi);
         }
       } else if (P2) {
