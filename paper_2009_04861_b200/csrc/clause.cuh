@@ -109,29 +109,10 @@ struct Clause {
     return __any_sync(kFull, moved != 0);
   }
 
-  // Type I (feedback.cpp:32-70) given per-word Bernoulli masks:
-  //   out=1, lit=1 : +1 w.p. (s-1)/s  (always if boost and included)
-  //   out=1, lit=0 : Reward w.p. 1/s  (-1 if excluded; +1 if included, which
-  //                  only a caller-forced output can reach, feedback.cpp:55-57)
-  //   out=0        : -1 w.p. 1/s       (Penalty on Include, Reward on Exclude)
+  // Type I on word slot p of part `part` (tm_device.cuh type_i_planes).
   __device__ __forceinline__ void type_i_word(int part, int p, uint32_t lit, int out, int boost,
                                               uint32_t bern, uint32_t lo, uint32_t hi) {
-    Planes<B>& w = s[part][p];
-    if (out) {
-      const uint32_t incl = w.p[B - 1];
-      if (P2) {  // one up/down pass: false literals of excluded automata step down
-        const uint32_t move = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern)) & valid[p];
-        step_sat<B>(w, move, ~(lit | incl));
-      } else {
-        const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid[p];
-        const uint32_t dec = ~lit & bern & ~incl & valid[p];
-        step<B>(w, inc, dec, lo, hi);
-      }
-    } else if (P2) {
-      sub_one_sat0<B>(w, bern & valid[p]);
-    } else {
-      step_down<B>(w, bern & valid[p], lo);
-    }
+    type_i_planes<B, P2>(s[part][p], lit, out, boost, bern, valid[p], lo, hi);
   }
 };
 

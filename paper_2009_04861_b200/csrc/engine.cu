@@ -308,11 +308,7 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->Wp = wp_for(o);
     tm->NW = tm->Wp / 32;
     // Rows wider than 4 words per lane keep a clause's automata in shared
-    // memory (train_smem.cu): B x 2 x Wp words plus the 16 KB alias table.
-    if (tm->NW > 4 && sizeof(uint32_t) * (static_cast<size_t>(tm->B) * 2 * tm->Wp + 4096) > 227 * 1024)
-      fail(TMG_EINVAL, "feature count too large: one clause's automata exceed shared memory (max " +
-                           std::to_string(((227 * 1024 / 4 - 4096) / (2 * tm->B)) / 32 * 32 * 32) + " features at " +
-                           std::to_string(tm->B) + " planes)");
+    // memory (train_smem.cu), or in place in HBM beyond what shared memory holds.
     tm->device = device;
     tm->all_positive = all_positive ? 1 : 0;
     CK(cudaStreamCreateWithFlags(&tm->stream, cudaStreamNonBlocking));

@@ -302,6 +302,47 @@ __global__ void init_state_kernel(uint32_t* __restrict__ state, int64_t words, i
   state[idx] = b < B - 1 ? kFull : 0u;
 }
 
+// Rows too wide for even a 32-example staged tile (beyond ~26k features):
+// each thread reads its example's literal words straight from HBM/L2 at the
+// clause's include-list positions, and the lists are read from global memory.
+template <bool TRAIN>
+__global__ void __launch_bounds__(128) eval_sums_direct_kernel(EvalParams P) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * 128 + tid;
+  const bool live = i < P.q;
+  const uint32_t* xr = P.xplane + (live ? i : 0) * 2 * P.Wp;
+  const int chunks = (P.n_loc + P.chunk - 1) / P.chunk;
+  const int c = blockIdx.y / chunks;
+  const int jl0 = (blockIdx.y % chunks) * P.chunk;
+  const int jl1 = min(jl0 + P.chunk, P.n_loc);
+  int sum = 0;
+  for (int jl = jl0; jl < jl1; ++jl) {
+    const int lc = c * P.n_loc + jl;
+    const int ne = __ldg(P.nentries + lc);
+    int out;
+    if (ne == 0) {
+      out = TRAIN ? 1 : 0;  // empty-clause convention (core.hpp:211-213)
+    } else {
+      const uint4* en = reinterpret_cast<const uint4*>(P.entries + static_cast<size_t>(lc) * P.Wx);
+      uint32_t viol = 0;
+      for (int k = 0; k < ne; ++k) {
+        const uint4 ent = __ldg(en + k);
+        viol |= (ent.y & ~__ldg(xr + ent.x)) | (ent.z & ~__ldg(xr + P.Wp + ent.x));
+        if (__all_sync(kFull, viol != 0 || !live)) break;
+      }
+      out = viol == 0 ? 1 : 0;
+    }
+    const int j = P.j_begin + jl;
+    sum += (!P.all_positive && (j & 1)) ? -out : out;
+    if (TRAIN && P.prev != nullptr) {
+      const unsigned bits = __ballot_sync(kFull, live && out);
+      if (lane == 0 && i < P.q) P.prev[static_cast<size_t>(lc) * P.Wq + (i >> 5)] = bits;
+    }
+  }
+  if (live) atomicAdd(P.sums + i * P.m + c, sum);
+}
+
 inline unsigned blocks_for(int64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
 
 }  // namespace
@@ -329,6 +370,14 @@ void eval_sums_launch(const EvalParams& p, bool train_mode, cudaStream_t s) {
     kern<<<grid, tile, shm, s>>>(q);
   };
   const bool wide = sizeof(uint32_t) * 2 * p.Wx * 129 > 200 * 1024;
+  const bool direct = sizeof(uint32_t) * 2 * p.Wx * 33 + 16 * p.Wx + 16 > 200 * 1024;
+  if (direct) {
+    dim3 grid(blocks_for(p.q, 128), p.m * chunks);
+    count_launch();
+    if (train_mode) eval_sums_direct_kernel<true><<<grid, 128, 0, s>>>(p);
+    else eval_sums_direct_kernel<false><<<grid, 128, 0, s>>>(p);
+    return;
+  }
   if (train_mode) {
     if (wide) go(eval_sums_kernel<true, 32>, 32);
     else go(eval_sums_kernel<true, 128>, 128);

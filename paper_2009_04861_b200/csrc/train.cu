@@ -279,6 +279,170 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
   }
 }
 
+// The same replay for rows wider than the register-held widths (NW > 16,
+// more than 16 384 features): the clause's planes are read and written in
+// place in HBM (lane-owned words, as in sequential.cu), the row is read on use.
+template <int B>
+__global__ void __launch_bounds__(32) train_mirror_wide_kernel(TrainParams P, MirrorParams M) {
+  extern __shared__ uint32_t smem[];
+  const int lane = threadIdx.x;
+  const int L = 2 * P.o;
+  const int refw = (L + 31) / 32 + 2;
+  uint32_t* hbits = smem;
+  uint32_t* lbits = smem + refw;
+  const int64_t q = P.q;
+  const int T = P.margin;
+  const int Wp = P.Wp, words = P.Wp >> 5;
+  for (int k = lane; k < 2 * refw; k += 32) smem[k] = 0;
+  __syncwarp();
+
+  for (int jb = 0; jb < M.njobs; ++jb) {
+    const MirrorJob job = M.jobs[jb];
+    const int c = job.c;
+    const int lc = c * P.n_loc + (job.j - P.j_begin);
+    const bool positive = P.all_positive || (job.j & 1) == 0;
+    Xoshiro rng;
+    uint64_t* rs = M.rng + 4 * job.worker;
+    rng.s0 = rs[0];
+    rng.s1 = rs[1];
+    rng.s2 = rs[2];
+    rng.s3 = rs[3];
+    uint32_t* st = P.state + static_cast<size_t>(lc) * B * 2 * Wp;
+    uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
+    unsigned long long events = 0;
+    auto get = [&](int part, int w, Planes<B>& pl) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) pl.p[b] = st[(b * 2 + part) * Wp + w];
+    };
+    auto put = [&](int part, int w, const Planes<B>& pl) {
+#pragma unroll
+      for (int b = 0; b < B; ++b) st[(b * 2 + part) * Wp + w] = pl.p[b];
+    };
+    auto valid = [&](int w) {
+      const int first = w * 32;
+      return first >= P.o ? 0u : (P.o - first >= 32 ? kFull : ((1u << (P.o - first)) - 1u));
+    };
+
+    const bool forced = job.forced != 0;
+    for (int64_t t = 0; t < job.batch; ++t) {
+      int64_t i = 0;
+      int target = 0, gated = 1;
+      if (lane == 0 && !forced) {  // identical to train_mirror_kernel
+        const int64_t pos = (job.offset + t) % q;
+        i = P.order ? P.order[pos] : pos;
+        const int v0 = P.tallies[i * P.m + c];
+        const int label = P.labels[i];
+        double p;
+        if (P.regress) {
+          const int v = v0 < 0 ? 0 : (v0 > T ? T : v0);
+          const int e = label > v ? label - v : v - label;
+          p = fmin(1.0, static_cast<double>(e) / (2.0 * static_cast<double>(T)));
+          target = v < label ? 1 : 0;
+        } else {
+          const int y = label == c ? 1 : 0;
+          const int v = v0 < -T ? -T : (v0 > T ? T : v0);
+          const int e = y ? T - v : T + v;
+          p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+          target = (y == 1) == positive ? 1 : 0;
+        }
+        gated = rng.uniform() < p ? 1 : 0;
+      }
+      gated = __shfl_sync(kFull, gated, 0);
+      if (!gated) continue;
+      ++events;
+      i = __shfl_sync(kFull, i, 0);
+      target = __shfl_sync(kFull, target, 0);
+      const uint32_t* xr = P.xplane + i * 2 * Wp;
+      const uint32_t* nr = P.nplane + i * 2 * Wp;
+      auto eval = [&]() {  // Train mode (core.hpp:208-219): empty clause -> 1
+        uint32_t viol = 0, any = 0;
+        for (int p = 0; p < words; ++p) {
+          const int w = p * 32 + lane;
+          const uint32_t ix = st[((B - 1) * 2) * Wp + w], in = st[((B - 1) * 2 + 1) * Wp + w];
+          viol |= (ix & ~xr[w]) | (in & ~nr[w]);
+          any |= ix | in;
+        }
+        const unsigned vb = __ballot_sync(kFull, viol != 0), ab = __ballot_sync(kFull, any != 0);
+        return ab == 0 ? 1 : (vb == 0 ? 1 : 0);
+      };
+      const bool type2 = forced ? job.forced == 2 : target == 0;
+      const int evald = eval();
+      const int before = (forced && job.out_override >= 0) ? job.out_override : evald;
+      int after = evald;
+      if (type2) {
+        if (before) {  // Type II (feedback.cpp:72-83)
+          uint32_t moved = 0;
+          for (int p = 0; p < words; ++p) {
+            const int w = p * 32 + lane;
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {
+              const uint32_t lit = part ? nr[w] : xr[w];
+              const uint32_t inc = ~lit & ~st[((B - 1) * 2 + part) * Wp + w] & valid(w);
+              if (inc) {
+                Planes<B> pl;
+                get(part, w, pl);
+                add_one<B>(pl, inc);
+                put(part, w, pl);
+              }
+              moved |= inc;
+            }
+          }
+          __syncwarp();
+          if (__any_sync(kFull, moved != 0)) after = eval();
+        }
+      } else {
+        if (lane == 0) {
+          uint32_t hw = 0, lw = 0;
+          for (int k = 0; k < L; ++k) {
+            const double u = rng.uniform();
+            hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
+            lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
+            if ((k & 31) == 31 || k == L - 1) {
+              hbits[k >> 5] = hw;
+              lbits[k >> 5] = lw;
+              hw = lw = 0;
+            }
+          }
+        }
+        __syncwarp();
+        for (int p = 0; p < words; ++p) {
+          const int wi = p * 32 + lane;
+          if (wi * 32 >= P.o) continue;
+          const int k1 = P.o + wi * 32;
+          const uint32_t h[2] = {hbits[wi], __funnelshift_r(hbits[k1 >> 5], hbits[(k1 >> 5) + 1], k1 & 31)};
+          const uint32_t l[2] = {lbits[wi], __funnelshift_r(lbits[k1 >> 5], lbits[(k1 >> 5) + 1], k1 & 31)};
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+            const uint32_t lit = part ? nr[wi] : xr[wi];
+            const uint32_t bern = before ? (lit & h[part]) | (~lit & l[part]) : l[part];
+            Planes<B> pl;
+            get(part, wi, pl);
+            type_i_planes<B, false>(pl, lit, before, P.boost, bern, valid(wi), P.lo, P.hi);
+            put(part, wi, pl);
+          }
+        }
+        __syncwarp();
+        after = eval();
+      }
+      if (lane == 0 && !forced) record(P, prev_row, i, c, positive, prev_row[i >> 5], after);
+      __syncwarp();
+    }
+    int cnt = 0;
+    for (int w = lane; w < 2 * Wp; w += 32) cnt += __popc(st[(B - 1) * 2 * Wp + w]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+    if (lane == 0) {
+      P.inc_count[lc] = cnt;
+      P.events[c] += events;
+      rs[0] = rng.s0;
+      rs[1] = rng.s1;
+      rs[2] = rng.s2;
+      rs[3] = rng.s3;
+    }
+    __syncwarp();
+  }
+}
+
 // --------------------------------------------------- feedback-rate probe ---
 // Statistical conformance of the async Type I path (acceptance criterion 1,
 // SPEC.md:530): every trial applies type_i_async to a fresh copy of one
@@ -400,7 +564,17 @@ bool dispatch_mirror(const TrainParams& p, const MirrorParams& mp, int NW, cudaS
     case 10: launch_mirror<10, B>(p, mp, s); return true;
     case 12: launch_mirror<12, B>(p, mp, s); return true;
     case 16: launch_mirror<16, B>(p, mp, s); return true;
-    default: return false;
+    default: {  // rows wider than 16 words per lane: planes in place
+      const int refw = (2 * p.o + 31) / 32 + 2;
+      const size_t shm = sizeof(uint32_t) * 2 * refw;
+      if (shm > 227 * 1024) return false;
+      if (shm > 48 * 1024)
+        cudaFuncSetAttribute(train_mirror_wide_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(shm));
+      count_launch();
+      train_mirror_wide_kernel<B><<<1, 32, shm, s>>>(p, mp);
+      return true;
+    }
   }
 }
 

@@ -121,22 +121,7 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& 
     for (int part = 0; part < 2; ++part) {
       Planes<B> pl;
       S.get(part, w, pl);
-      const uint32_t lit = sel[part];
-      if (before) {
-        const uint32_t incl = pl.p[B - 1];
-        if (P2) {  // one up/down pass (step_sat)
-          const uint32_t move = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part])) & vm;
-          step_sat<B>(pl, move, ~(lit | incl));
-        } else {
-          const uint32_t inc = ((lit & (bern[part] | (P.boost ? incl : 0u))) | (~lit & bern[part] & incl)) & vm;
-          const uint32_t dec = ~lit & bern[part] & ~incl & vm;
-          step<B>(pl, inc, dec, P.lo, P.hi);
-        }
-      } else if (P2) {
-        sub_one_sat0<B>(pl, bern[part] & vm);
-      } else {
-        step_down<B>(pl, bern[part] & vm, P.lo);
-      }
+      type_i_planes<B, P2>(pl, sel[part], before, P.boost, bern[part], vm, P.lo, P.hi);
       S.put(part, w, pl);
     }
   }
@@ -145,13 +130,16 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& 
 
 // One warp per clause, blockDim.x / 32 clauses per CTA; dynamic shared memory
 // = the clauses' planes, then kAliasCopies copies of the alias table.
-template <int NW, int B, bool P2>
+// INPLACE (rows whose planes exceed shared memory, beyond ~107k features at
+// 8 planes): one clause per CTA, the planes stay in HBM/L2 and are updated in
+// place (every word is lane-owned), shared memory holds the alias table only.
+template <int NW, int B, bool P2, bool INPLACE = false>
 __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
   extern __shared__ uint32_t smem[];
   const int Wp = P.Wp;
   const int cpb = blockDim.x >> 5;
   const size_t words = static_cast<size_t>(B) * 2 * Wp;
-  uint32_t* atab = smem + cpb * words;
+  uint32_t* atab = INPLACE ? smem : smem + cpb * words;
   fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -162,9 +150,10 @@ __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
   const bool positive = P.all_positive || (j & 1) == 0;
-  SmemPlanes<B> S{smem + wib * words, Wp};
   uint32_t* st = P.state + static_cast<size_t>(lc) * words;
-  for (size_t k = lane; k < words; k += 32) S.s[k] = st[k];
+  SmemPlanes<B> S{INPLACE ? st : smem + wib * words, Wp};
+  if (!INPLACE)
+    for (size_t k = lane; k < words; k += 32) S.s[k] = st[k];
   __syncwarp();
   uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
   const int64_t offset = clause_offset_dev(g, P.q);
@@ -233,7 +222,7 @@ __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
   __syncwarp();
   int cnt = 0;
   for (size_t k = lane; k < words; k += 32) {
-    st[k] = S.s[k];
+    if (!INPLACE) st[k] = S.s[k];
     if (k >= static_cast<size_t>(B - 1) * 2 * Wp) cnt += __popc(S.s[k]);
   }
 #pragma unroll
@@ -251,11 +240,21 @@ size_t smem_bytes(int B, int Wp, int cpb) {
 
 template <int NW, int B, bool P2>
 bool launch_smem_p2(const TrainParams& p, cudaStream_t s, int* blocks) {
-  // Two clauses per CTA where they fit, else one; none: the row is too wide.
+  // Two clauses per CTA where they fit, else one; none: planes in place.
   const int cpb = smem_bytes(B, p.Wp, 2) <= kSmemMax ? 2 : 1;
   const size_t shm = smem_bytes(B, p.Wp, cpb);
-  if (shm > kSmemMax) return false;
   const int clauses = p.m * p.n_loc;
+  if (shm > kSmemMax) {
+    if constexpr (NW != 0) {
+      return false;
+    } else {
+      if (blocks) *blocks = clauses;
+      const size_t ashm = sizeof(uint32_t) * kAliasWordsPacked;
+      count_launch();
+      train_async_smem_kernel<0, B, P2, true><<<clauses, 32, ashm, s>>>(p);
+      return true;
+    }
+  }
   const int grid = (clauses + cpb - 1) / cpb;
   if (blocks) *blocks = grid;
   if (shm > 48 * 1024)

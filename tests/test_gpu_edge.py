@@ -2,7 +2,8 @@
 (core.cpp:48-74, pool.cpp:23-80) through the GPU engine: one feature, one
 bank, one or two examples, the smallest and largest state depths (N = 1 ->
 4 bit planes, N = 16383 -> 15), margin 1, s = 1, boost, widths straddling the
-word and warp boundaries. Each runs the sync-mirror epoch against the oracle
+word and warp boundaries, and rows past every shared-memory capacity (the
+reference has no width limit). Each runs the sync-mirror epoch against the oracle
 (bit-exact) and asynchronous epochs under the tally invariant."""
 import numpy as np
 import pytest
@@ -22,6 +23,13 @@ CASES = [
     ("depth_16383", 64, 2, 4, 16383, 50, 10.0, False, 60),
     ("word_edges", 1025, 2, 2, 8, 4, 3.9, True, 30),
     ("many_classes", 20, 37, 2, 128, 3, 4.0, False, 200),
+    # runtime-width rows: replay kernel with planes in place (> 16 384 features),
+    # direct evaluation (> ~26k), async planes in HBM (> 107 520 at 8 planes,
+    # > 57 344 at 15)
+    ("wide_20k", 20000, 2, 2, 128, 6, 3.0, True, 48),
+    ("wide_40k", 40000, 3, 2, 100, 4, 5.0, False, 40),
+    ("wide_110k_inplace", 110000, 2, 2, 128, 5, 3.0, False, 33),
+    ("wide_60k_deep_inplace", 60000, 2, 2, 9000, 8, 4.0, False, 20),
 ]
 
 
