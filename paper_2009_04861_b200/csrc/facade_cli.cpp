@@ -521,10 +521,11 @@ int run_cli(const std::vector<std::string>& args) {
 
   Command* chosen = nullptr;
   try {
-    if (!args.empty() && (args[0] == "--help" || args[0] == "-h")) {
-      std::cout << kUsage;
-      return 0;
-    }
+    for (const auto& a : args)
+      if (a == "--help" || a == "-h") {  // CLI11: help anywhere wins, exit 0
+        std::cout << kUsage;
+        return 0;
+      }
     if (args.empty()) throw ParseFailure(kRequiredError, "A subcommand is required");
     for (Command* c : {&train, &eval, &bench, &synth})
       if (c->name() == args[0]) chosen = c;

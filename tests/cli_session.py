@@ -51,6 +51,7 @@ HOST = [
     ["eval", "--model", "missing.txt", "--data", "pat.test"],
     ["bench", "--synth", "xor", "--bench-mode", "seq"],
     ["bench", "--clauses", "4", "--bench-mode", "sometimes"],
+    ["train", "--epochs", "3", "--help"],
 ]
 
 GPU = [
