@@ -16,8 +16,12 @@ q examples — the most expensive epoch, and identical work every step.
           reset, the epoch runs, the per-class feedback-event report is read
           back.
 Multi-GPU (torchrun): weak scaling in clauses — every rank owns 2000 clauses
-per class (global n = 2000 * world), tally deltas are all-reduced with NCCL
-every window (paper_2009_04861_b200/distributed.py).
+per class (global n = 2000 * world). Default exchange "peer": every rank's
+tally replica is mapped into every other rank (CUDA IPC over NVLink) and the
+training kernels add each tally change into all replicas as it happens;
+"overlapped"/"sync" all-reduce tally deltas with NCCL every window
+(paper_2009_04861_b200/distributed.py). "peer" falls back to "overlapped"
+(and says so in config.exchange_note) when the replicas cannot be mapped.
 
 --impl reference times the UNMODIFIED reference (oracle/_ref/ref_driver, the
 reference sources compiled with their own Release flags) on the host cores:
@@ -278,6 +282,17 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=f"cuda:{local}")  # > 126 MB L2
     allreduce = D.nccl_allreduce(local) if world > 1 else None
     windows = args.windows
+    exchange, exchange_note = (args.exchange if world > 1 else "none"), None
+    if exchange == "peer":  # tally replicas over peer memory; NCCL windows if P2P is unavailable
+        try:
+            D.attach_peer_tallies(pool)
+        except Exception as e:  # noqa: BLE001 - any IPC failure falls back, and is reported
+            exchange, exchange_note = "overlapped", f"peer memory unavailable ({e}); fell back"
+        ok = torch.tensor([1 if exchange == "peer" else 0], device=f"cuda:{local}")
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+        if int(ok.item()) == 0 and exchange == "peer":
+            D.detach_peer_tallies(pool)
+            exchange, exchange_note = "overlapped", "a peer could not map the replicas; fell back"
 
     def one_epoch(p):
         tm.reset()
@@ -285,7 +300,9 @@ def run_ours(args):
         if world == 1:
             rep = T.train_epoch_parallel(tm, p, 1, 0)
             return rep.feedback_events, rep.type_i_events, rep.device_seconds
-        if args.exchange == "overlapped":
+        if exchange == "peer":
+            ev = D.train_epoch_peer(tm, p, 0)
+        elif exchange == "overlapped":
             ev = D.train_epoch_overlapped(tm, p, 0, windows)
         else:
             ev = D.train_epoch_windows(D.GpuShardEngine(tm, p), 0, windows, allreduce)
@@ -334,10 +351,15 @@ def run_ours(args):
         barrier()
         t0 = time.perf_counter()
         p2 = T.ExamplePool(O_FEAT, host_bits, host_lab, M_CLS, device=local)
+        if exchange == "peer":
+            D.attach_peer_tallies(p2)
         t1 = time.perf_counter()
         ev, _, _ = one_epoch(p2)
         _ = [int(v) for v in ev]  # per-class report read back to the host
         t2 = time.perf_counter()
+        if exchange == "peer":
+            D.detach_peer_tallies(p2)
+            barrier()
         del p2
         torch.cuda.synchronize()
         barrier()
@@ -362,8 +384,9 @@ def run_ours(args):
         "config": {"workload": "mnist-784b-10c-2000cl fresh epoch 0", "q": Q_TRAIN,
                    "clauses_per_class_per_gpu": N_CLAUSES, "clauses_per_class_total": n_total,
                    "T": MARGIN, "s": SPEC, "state_bits": 8, "parallelism": f"clause-shard{world}",
-                   "windows": windows if world > 1 else 1,
-                   "exchange": args.exchange if world > 1 else "none",
+                   "windows": windows if world > 1 and exchange != "peer" else 1,
+                   "exchange": exchange,
+                   **({"exchange_note": exchange_note} if exchange_note else {}),
                    "l2": "flushed (256 MB write) between timed steps; working set (prev bits 150 MB) > L2"},
         "examples_per_s": Q_TRAIN / (ms * 1e-3),
         "feedback_events_per_step": statistics.mean(events),
@@ -437,8 +460,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-other-configs", action="store_true", help="skip the FMNIST/IMDb side measurements")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (tests: gloo)")
-    ap.add_argument("--exchange", choices=["overlapped", "sync"], default="overlapped",
-                    help="N>1 tally exchange: double-buffered on a side stream, or host-synchronous per window")
+    ap.add_argument("--exchange", choices=["peer", "overlapped", "sync"], default="peer",
+                    help="N>1 tally exchange: replicas updated by the training kernels over peer memory "
+                         "(NVLink), or windowed all-reduce double-buffered on a side stream, or "
+                         "host-synchronous per window")
     ap.add_argument("--share-device", action="store_true",
                     help="run every rank on cuda:0 (one-GPU test of the N>1 protocol; not a measurement)")
     args = ap.parse_args()

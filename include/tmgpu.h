@@ -176,6 +176,18 @@ int tmg_pool_reset_tallies(tmg_pool* pool);
 int tmg_pool_tally_device_ptr(tmg_pool* pool, void** ptr);
 /* Device pointer of the q x m int32 tally-delta buffer (multi-GPU windows). */
 int tmg_pool_delta_device_ptr(tmg_pool* pool, void** ptr);
+/* Multi-GPU over peer memory (replaces the window exchange
+ * of the reference's shared atomic tallies, pool.hpp:66-69, across GPUs):
+ * every rank keeps a full q x m tally replica, and the training kernels add
+ * each tally change into the local replica AND, over NVLink, into every
+ * peer's — the collective is fused into the clause kernel, no windows.
+ * tmg_pool_tally_ipc_handle moves the replica to IPC-exportable memory (once)
+ * and writes its 64-byte cudaIpcMemHandle_t; tmg_pool_set_peers opens the
+ * other ranks' handles (npeers <= 7, concatenated 64-byte handles; 0
+ * detaches). Callers reset every replica and barrier before an epoch, and
+ * barrier after it. */
+int tmg_pool_tally_ipc_handle(tmg_pool* pool, unsigned char* handle);
+int tmg_pool_set_peers(tmg_pool* pool, const unsigned char* handles, int32_t npeers);
 
 /* ---- training */
 /* train_epoch_parallel (trainer.cpp:181-242).

@@ -83,6 +83,8 @@ SIGNATURES = {
     "tmg_pool_reset_tallies": (C.c_int, [P]),
     "tmg_pool_tally_device_ptr": (C.c_int, [P, PP]),
     "tmg_pool_delta_device_ptr": (C.c_int, [P, PP]),
+    "tmg_pool_tally_ipc_handle": (C.c_int, [P, P]),
+    "tmg_pool_set_peers": (C.c_int, [P, P, I32]),
     "tmg_train_epoch": (C.c_int, [P, P, I32, I32, I32, C.POINTER(EpochReportC)]),
     "tmg_train_window": (C.c_int, [P, P, I32, I64, I64, P]),
     "tmg_train_epoch_sequential": (C.c_int, [P, P, I32, C.POINTER(D), P]),

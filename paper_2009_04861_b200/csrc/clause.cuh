@@ -134,6 +134,7 @@ __device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row,
   if (!positive) delta = -delta;
   atomicAdd(&P.tallies[i * P.m + c], delta);
   if (P.tally_delta) atomicAdd(&P.tally_delta[i * P.m + c], delta);
+  for (int k = 0; k < P.npeers; ++k) atomicAdd(P.peer_tallies[k] + i * P.m + c, delta);
 }
 
 // --------------------------------------------------------------- async ---

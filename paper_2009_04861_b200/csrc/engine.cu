@@ -111,15 +111,34 @@ struct DevBuf {
     }
     count = n;
   }
+  // Plain cudaMalloc memory instead (IPC-exportable: the stream-ordered
+  // pool's blocks cannot be shared with cudaIpcGetMemHandle).
+  void alloc_plain(size_t n) {
+    release();
+    if (n) CK(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
+    count = n;
+    plain = n != 0;
+  }
   void release() {
     if (ptr) {
       cudaDeviceSynchronize();
-      cudaFreeAsync(ptr, cudaStreamPerThread);
-      cudaStreamSynchronize(cudaStreamPerThread);
+      if (plain) {
+        cudaFree(ptr);
+      } else {
+        cudaFreeAsync(ptr, cudaStreamPerThread);
+        cudaStreamSynchronize(cudaStreamPerThread);
+      }
     }
     ptr = nullptr;
     count = 0;
+    plain = false;
   }
+  void swap(DevBuf& o) {
+    std::swap(ptr, o.ptr);
+    std::swap(count, o.count);
+    std::swap(plain, o.plain);
+  }
+  bool plain = false;
   size_t bytes() const { return count * sizeof(T); }
 };
 
@@ -206,6 +225,13 @@ struct tmg_pool {
   uint32_t* nplane() const { return rows.ptr + Wp; }
   DevBuf<int32_t> labels, tallies, delta, order;
   std::vector<int32_t> host_labels;
+  // Tally replicas of the other ranks (multi-GPU over peer memory): every
+  // tally change is also added into each of them by the training kernels.
+  std::vector<int32_t*> peers;
+  void close_peers() {
+    for (int32_t* p : peers) cudaIpcCloseMemHandle(p);
+    peers.clear();
+  }
 };
 
 struct tmg_machine {
@@ -368,6 +394,8 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   p.labels = pool->labels.ptr;
   p.tallies = pool->tallies.ptr;
   p.tally_delta = nullptr;
+  p.npeers = static_cast<int32_t>(pool->peers.size());
+  for (int k = 0; k < tmg::kMaxPeers; ++k) p.peer_tallies[k] = k < p.npeers ? pool->peers[k] : nullptr;
   p.q = pool->q;
   p.order = pool->order.ptr;
   p.margin = tm->cfg.margin;
@@ -785,6 +813,7 @@ TMG_API int tmg_pool_destroy(tmg_pool* pool) {
   cudaGetDevice(&prev);
   cudaSetDevice(pool->device);
   if (pool->stream) cudaStreamSynchronize(pool->stream);
+  pool->close_peers();
   pool->rows.release();
   pool->labels.release();
   pool->tallies.release();
@@ -850,6 +879,46 @@ TMG_API int tmg_pool_reset_tallies(tmg_pool* pool) {
     CK(cudaMemsetAsync(pool->tallies.ptr, 0, pool->tallies.bytes(), pool->stream));
     CK(cudaMemsetAsync(pool->delta.ptr, 0, pool->delta.bytes(), pool->stream));
     CK(cudaStreamSynchronize(pool->stream));
+  });
+}
+
+TMG_API int tmg_pool_tally_ipc_handle(tmg_pool* pool, unsigned char* handle) {
+  return guarded([&] {
+    if (!pool || !handle) fail(TMG_EINVAL, "null argument");
+    DeviceGuard dg(pool->device);
+    CK(cudaStreamSynchronize(pool->stream));
+    if (!pool->tallies.plain && pool->tallies.count) {  // move the replica to exportable memory
+      DevBuf<int32_t> t;
+      t.alloc_plain(pool->tallies.count);
+      CK(cudaMemcpy(t.ptr, pool->tallies.ptr, t.bytes(), cudaMemcpyDeviceToDevice));
+      pool->tallies.swap(t);
+    }
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, pool->tallies.ptr));
+    std::memcpy(handle, &h, sizeof(h));
+  });
+}
+
+TMG_API int tmg_pool_set_peers(tmg_pool* pool, const unsigned char* handles, int32_t npeers) {
+  return guarded([&] {
+    if (!pool) fail(TMG_EINVAL, "null pool handle");
+    if (npeers < 0 || npeers > tmg::kMaxPeers)
+      fail(TMG_EINVAL, "peer count must be in [0, " + std::to_string(tmg::kMaxPeers) + "]");
+    if (npeers > 0 && !handles) fail(TMG_EINVAL, "null handles");
+    DeviceGuard dg(pool->device);
+    CK(cudaStreamSynchronize(pool->stream));
+    pool->close_peers();
+    for (int k = 0; k < npeers; ++k) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, handles + static_cast<size_t>(k) * sizeof(h), sizeof(h));
+      void* ptr = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        pool->close_peers();
+        fail(TMG_ERUNTIME, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
+      pool->peers.push_back(static_cast<int32_t*>(ptr));
+    }
   });
 }
 

@@ -21,6 +21,7 @@ struct BernThresholds {
 };
 
 constexpr int kMaxPhiloxRounds = 10;
+constexpr int kMaxPeers = 7;  // tally replicas of the other ranks (8 GPUs per node)
 
 // Device view of one machine shard + pool, shared by all training kernels.
 struct TrainParams {
@@ -38,6 +39,8 @@ struct TrainParams {
   const int32_t* labels;   // [q]
   int32_t* tallies;        // [q][m]
   int32_t* tally_delta;    // [q][m] or null: deltas also published here (multi-GPU)
+  int32_t* peer_tallies[kMaxPeers];  // other ranks' [q][m] replicas (peer memory)
+  int32_t npeers;
   int64_t q;
   // Epoch.
   const int32_t* order;  // [q] epoch permutation, or null = natural order

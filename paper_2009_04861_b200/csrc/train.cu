@@ -136,10 +136,12 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       const size_t ti = static_cast<size_t>(i) * P.m + c;
       atomicAdd(&P.tallies[ti], delta);
       if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
+      for (int k = 0; k < P.npeers; ++k) atomicAdd(P.peer_tallies[k] + ti, delta);  // NVLink reduction
     }
   }
   cl.store(st, P.Wp, lane);
   const int cnt = cl.include_count();
+  if (P.npeers) __threadfence_system();  // remote tally adds performed before the kernel retires
   if (lane == 0) {
     P.inc_count[lc] = cnt;
     atomicAdd(P.events + c, events);

@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
       const size_t ti = static_cast<size_t>(i) * P.m + c;
       atomicAdd(&P.tallies[ti], delta);
       if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
+      for (int k = 0; k < P.npeers; ++k) atomicAdd(P.peer_tallies[k] + ti, delta);  // NVLink reduction
     }
   }
   __syncwarp();
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  if (P.npeers) __threadfence_system();  // remote tally adds performed before the kernel retires
   if (lane == 0) {
     P.inc_count[lc] = cnt;
     atomicAdd(P.events + c, events);

@@ -10,6 +10,12 @@ sees other ranks' clause outputs with at most one window of extra staleness —
 the same relaxed, lock-free tally semantics as the reference's worker threads
 (pool.hpp:54-62), now across NVLink.
 
+The fused alternative (attach_peer_tallies / train_epoch_peer): every rank's
+replica is mapped into every other rank over CUDA IPC, and the training
+kernels add each tally change into all replicas as it happens (NVLink
+reductions inside the clause kernel) — no windows, no collective call, and a
+staleness of one NVLink round trip instead of one window.
+
 Clause keys (RNG counters, per-clause offsets) use the GLOBAL clause index, so
 sampling does not depend on the number of ranks.
 """
@@ -163,6 +169,51 @@ def train_epoch_overlapped(tm: MultiClassTM, pool: ExamplePool, epoch: int, wind
     ev = np.zeros(m, np.uint64)
     check(lib().tmg_epoch_events(tm.handle, ev.ctypes.data))
     return [int(v) for v in ev]
+
+
+def attach_peer_tallies(pool: ExamplePool, group=None) -> int:
+    """Peer-memory exchange, the fused alternative to the
+    windowed all-reduce: every rank exports its pool's tally replica
+    (cudaIpcMemHandle, gathered over the process group) and opens the others',
+    after which the training kernels add every tally change into all replicas
+    over NVLink as it happens. Returns the number of peers attached. Raises
+    TMError when a handle cannot be opened (no P2P path between the GPUs);
+    callers fall back to train_epoch_overlapped."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if world - 1 > 7:
+        raise ValueError("peer-memory exchange supports up to 8 ranks (one node)")
+    h = (C.c_ubyte * 64)()
+    check(lib().tmg_pool_tally_ipc_handle(pool.handle, h))
+    handles = [None] * world
+    dist.all_gather_object(handles, bytes(h), group=group)
+    others = b"".join(handles[r] for r in range(world) if r != rank)
+    buf = (C.c_ubyte * max(1, len(others))).from_buffer_copy(others or b"\0")
+    check(lib().tmg_pool_set_peers(pool.handle, buf, world - 1))
+    return world - 1
+
+
+def detach_peer_tallies(pool: ExamplePool) -> None:
+    check(lib().tmg_pool_set_peers(pool.handle, None, 0))
+
+
+def train_epoch_peer(tm: MultiClassTM, pool: ExamplePool, epoch: int, group=None) -> List[int]:
+    """One asynchronous epoch of this rank's clause shard with the tally
+    replicas attached by attach_peer_tallies: a barrier so that no rank adds
+    into a replica that another rank is still resetting, the epoch (the
+    kernels keep every replica current), and a barrier so that every rank's
+    remote adds have landed before anyone reads its tallies. Every replica
+    then holds the same tallies, over all shards."""
+    import torch
+    import torch.distributed as dist
+    from .tsetlin import MODE_ASYNC, train_epoch_parallel
+    torch.cuda.synchronize(pool.device)
+    dist.barrier(group=group)
+    rep = train_epoch_parallel(tm, pool, 1, epoch, mode=MODE_ASYNC)
+    torch.cuda.synchronize(pool.device)
+    dist.barrier(group=group)
+    return [int(v) for v in rep.feedback_events]
 
 
 def nccl_allreduce(device: int, group=None) -> Callable:

@@ -28,6 +28,9 @@ def _free_port():
 
 
 def _worker(rank, world, port, out_dir, overlapped=False):
+    """overlapped: False = synchronous windows, True = overlapped windows,
+    "peer" = replicas over peer memory (CUDA IPC; here two processes on one
+    GPU)."""
     import torch
     import torch.distributed as dist
 
@@ -42,8 +45,12 @@ def _worker(rank, world, port, out_dir, overlapped=False):
     tm = T.MultiClassTM(T.TMConfig(clauses=N, margin=20, specificity=10.0, seed=3), O_FEAT, M, clause_range=(jb, je))
     pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M)
     eng = D.GpuShardEngine(tm, pool)
+    if overlapped == "peer":
+        assert D.attach_peer_tallies(pool) == world - 1
     for e in range(2):
-        if overlapped:
+        if overlapped == "peer":
+            D.train_epoch_peer(tm, pool, e)
+        elif overlapped:
             D.train_epoch_overlapped(tm, pool, e, windows=5)
         else:
             D.train_epoch_windows(eng, e, windows=5, allreduce=D.torch_allreduce())
@@ -63,11 +70,13 @@ def _bits(prev, q):
     return b[..., :q].astype(np.int64)
 
 
-@pytest.mark.parametrize("overlapped", [False, True])
+@pytest.mark.parametrize("overlapped", [False, True, "peer"])
 def test_gpu_shards_two_processes(tmp_path, overlapped):
-    """Synchronous windows (train_epoch_windows) and the double-buffered,
-    overlapped exchange (train_epoch_overlapped) both end each epoch with
-    identical replicas satisfying the invariant over both shards."""
+    """Synchronous windows (train_epoch_windows), the double-buffered,
+    overlapped exchange (train_epoch_overlapped) and the peer-memory replicas
+    (train_epoch_peer: tally changes added into every replica by the clause
+    kernels) all end each epoch with identical replicas satisfying the
+    invariant over both shards."""
     import torch.multiprocessing as mp
 
     from paper_2009_04861_b200 import distributed as D
@@ -114,8 +123,16 @@ def _acc_worker(rank, world, port, out_dir, windows):
         tm = T.MultiClassTM(T.TMConfig(clauses=cfg["clauses"], margin=cfg["T"], specificity=cfg["s"], seed=seed),
                             784, 10, clause_range=(jb, je))
         pool = T.ExamplePool(784, d.train_x, d.train_y, 10)
+        if windows == "peer":
+            D.attach_peer_tallies(pool)
         for e in range(cfg["epochs"]):
-            D.train_epoch_overlapped(tm, pool, e, windows=windows)
+            if windows == "peer":
+                D.train_epoch_peer(tm, pool, e)
+            else:
+                D.train_epoch_overlapped(tm, pool, e, windows=windows)
+        if windows == "peer":
+            D.detach_peer_tallies(pool)
+            dist.barrier()
         test = T.ExamplePool(784, d.test_x, d.test_y, 10)
         part = torch.from_numpy(T.class_sums(tm, test).astype(np.int64))
         dist.all_reduce(part)
@@ -126,14 +143,16 @@ def _acc_worker(rank, world, port, out_dir, windows):
     dist.destroy_process_group()
 
 
-def test_two_rank_accuracy_parity(tmp_path):
-    """Clause-sharded training (2 ranks x 1000 clauses/class, overlapped
-    16-window exchange, MNIST-shaped q = 6000, 3 epochs, 5 seeds) matches the
-    reference's multi-threaded trainer on the same data within 0.5 pt — the
-    multi-GPU staleness does not cost accuracy."""
+@pytest.mark.parametrize("exchange", [16, "peer"])
+def test_two_rank_accuracy_parity(tmp_path, exchange):
+    """Clause-sharded training (2 ranks x 1000 clauses/class, MNIST-shaped
+    q = 6000, 3 epochs, 5 seeds; overlapped 16-window exchange, or the
+    peer-memory replicas) matches the reference's multi-threaded trainer on
+    the same data within 0.5 pt — the multi-GPU staleness does not cost
+    accuracy."""
     import torch.multiprocessing as mp
     ref = json.load(open(os.path.join(REPO, "tests", "golden", "accuracy_ref.json")))["mnist_q6000"]
-    mp.start_processes(_acc_worker, args=(2, _free_port(), str(tmp_path), 16), nprocs=2, join=True,
+    mp.start_processes(_acc_worker, args=(2, _free_port(), str(tmp_path), exchange), nprocs=2, join=True,
                        start_method="spawn")
     accs = json.load(open(tmp_path / "accs.json"))
     gpu = float(np.mean(accs))
@@ -152,3 +171,4 @@ def test_bench_two_ranks_protocol():
     assert len(lines) == 1
     assert lines[0]["n_gpus"] == 2 and lines[0]["value"] > 0
     assert lines[0]["config"]["clauses_per_class_total"] == 4000
+    assert lines[0]["config"]["exchange"] == "peer"  # replicas mapped over CUDA IPC, no fallback
