@@ -14,6 +14,9 @@
 #ifndef TMG_ASYNC_UNROLL_NW
 #define TMG_ASYNC_UNROLL_NW 1  // widest rows (words per lane) that get the 2x unrolled step loop
 #endif
+#ifndef TMG_STEP_SAT_REG
+#define TMG_STEP_SAT_REG 0  // register kernels: clause-output-1 Type I as two passes (tm_device.cuh type_i_planes)
+#endif
 #ifndef TMG_ALIAS
 #define TMG_ALIAS 1  // alias-table sampler for clause-output-0 Type I draws
 #endif
@@ -112,7 +115,7 @@ struct Clause {
   // Type I on word slot p of part `part` (tm_device.cuh type_i_planes).
   __device__ __forceinline__ void type_i_word(int part, int p, uint32_t lit, int out, int boost,
                                               uint32_t bern, uint32_t lo, uint32_t hi) {
-    type_i_planes<B, P2>(s[part][p], lit, out, boost, bern, valid[p], lo, hi);
+    type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(s[part][p], lit, out, boost, bern, valid[p], lo, hi);
   }
 };
 
@@ -121,6 +124,31 @@ __device__ __forceinline__ uint64_t splitmix_dev(uint64_t x) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
   return z ^ (z >> 31);
+}
+
+// Fire-and-forget reductions (RED, no return value to wait for).
+__device__ __forceinline__ void red_add_gpu(int32_t* p, int v) {
+  asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_xor_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.xor.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_sys(int32_t* p, int v) {
+  asm volatile("red.relaxed.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One tally change (pool.cpp:93-106 add_to_tally): the local replica, the
+// window delta buffer when windows are in use, and — with peer replicas —
+// every other rank's replica over NVLink. With peers, the local add is also
+// system-scoped: remote GPUs reduce into the same words.
+__device__ __forceinline__ void publish_tally(const TrainParams& P, size_t ti, int delta) {
+  if (P.npeers == 0) {
+    red_add_gpu(P.tallies + ti, delta);
+  } else {
+    red_add_sys(P.tallies + ti, delta);
+    for (int k = 0; k < P.npeers; ++k) red_add_sys(P.peer_tallies[k] + ti, delta);
+  }
+  if (P.tally_delta) red_add_gpu(P.tally_delta + ti, delta);
 }
 
 // Publishes the post-feedback output (pool.cpp:93-106); one lane.
@@ -132,9 +160,7 @@ __device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row,
   prev_row[i >> 5] = pword ^ bit;
   int delta = after ? 1 : -1;
   if (!positive) delta = -delta;
-  atomicAdd(&P.tallies[i * P.m + c], delta);
-  if (P.tally_delta) atomicAdd(&P.tally_delta[i * P.m + c], delta);
-  for (int k = 0; k < P.npeers; ++k) atomicAdd(P.peer_tallies[k] + i * P.m + c, delta);
+  publish_tally(P, static_cast<size_t>(i) * P.m + c, delta);
 }
 
 // --------------------------------------------------------------- async ---
@@ -202,10 +228,20 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32
   if (before) bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
   else bernoulli_words<K, false>(need, sel, P.bern, bern, gen);
 #endif
+  // The clause output is warp-uniform: branch once on it (constant `out` in
+  // each arm) rather than leave the compiler to predicate both updates.
+  if (before) {
 #pragma unroll
-  for (int p = 0; p < NW; ++p) {
-    cl.type_i_word(0, p, x[p], before, P.boost, bern[2 * p], P.lo, P.hi);
-    cl.type_i_word(1, p, n[p], before, P.boost, bern[2 * p + 1], P.lo, P.hi);
+    for (int p = 0; p < NW; ++p) {
+      cl.type_i_word(0, p, x[p], 1, P.boost, bern[2 * p], P.lo, P.hi);
+      cl.type_i_word(1, p, n[p], 1, P.boost, bern[2 * p + 1], P.lo, P.hi);
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < NW; ++p) {
+      cl.type_i_word(0, p, x[p], 0, P.boost, bern[2 * p], P.lo, P.hi);
+      cl.type_i_word(1, p, n[p], 0, P.boost, bern[2 * p + 1], P.lo, P.hi);
+    }
   }
 }
 

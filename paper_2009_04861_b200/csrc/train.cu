@@ -130,13 +130,11 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       }
     }
     if (gated && ((outs >> lane) & 1u) != prevbit) {
-      atomicXor(prev_row + (i >> 5), 1u << (i & 31));
+      red_xor_gpu(prev_row + (i >> 5), 1u << (i & 31));
       int delta = prevbit ? -1 : 1;
       if (!positive) delta = -delta;
       const size_t ti = static_cast<size_t>(i) * P.m + c;
-      atomicAdd(&P.tallies[ti], delta);
-      if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
-      for (int k = 0; k < P.npeers; ++k) atomicAdd(P.peer_tallies[k] + ti, delta);  // NVLink reduction
+      publish_tally(P, ti, delta);  // local replica (+ window deltas, + peers over NVLink)
     }
   }
   cl.store(st, P.Wp, lane);

@@ -21,6 +21,10 @@ namespace tmg {
 
 namespace {
 
+#ifndef TMG_STEP_SAT_SMEM
+#define TMG_STEP_SAT_SMEM 1  // clause-output-1 Type I as one up/down pass (tm_device.cuh type_i_planes)
+#endif
+
 constexpr int kSmemUnroll = TMG_SMEM_UNROLL;
 constexpr size_t kSmemMax = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 
@@ -93,9 +97,10 @@ __device__ __forceinline__ uint32_t valid_of(int w, int o) {
 // lane at a time, with the register kernel's draws (clause.cuh type_i_async):
 // alias patterns from Philox counters (clause, example, 2*word + part, 0),
 // or the bit-serial sampler when p_high != 1 - p_low.
-template <int NW, int B, bool P2>
-__device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& r, int before, const TrainParams& P,
-                                            uint32_t g, uint32_t i32, int lane, const uint32_t* atab) {
+template <int NW, int B, bool P2, int OUT>
+__device__ __forceinline__ void type_i_smem_out(SmemPlanes<B>& S, const LitRow<NW>& r, const TrainParams& P,
+                                                uint32_t g, uint32_t i32, int lane, const uint32_t* atab) {
+  constexpr int before = OUT;
 #pragma unroll kSmemUnroll
   for (int p = 0; p < r.words(); ++p) {
     const int w = p * 32 + lane;
@@ -121,11 +126,21 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& 
     for (int part = 0; part < 2; ++part) {
       Planes<B> pl;
       S.get(part, w, pl);
-      type_i_planes<B, P2>(pl, sel[part], before, P.boost, bern[part], vm, P.lo, P.hi);
+      type_i_planes<B, P2, TMG_STEP_SAT_SMEM != 0>(pl, sel[part], before, P.boost, bern[part], vm, P.lo, P.hi);
       S.put(part, w, pl);
     }
   }
   __syncwarp();
+}
+
+// The clause output is warp-uniform: one branch, each arm with a constant one.
+template <int NW, int B, bool P2>
+__device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& r, int before, const TrainParams& P,
+                                            uint32_t g, uint32_t i32, int lane, const uint32_t* atab) {
+  if (before)
+    type_i_smem_out<NW, B, P2, 1>(S, r, P, g, i32, lane, atab);
+  else
+    type_i_smem_out<NW, B, P2, 0>(S, r, P, g, i32, lane, atab);
 }
 
 // One warp per clause, blockDim.x / 32 clauses per CTA; dynamic shared memory
@@ -211,13 +226,11 @@ __global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
       outs |= static_cast<unsigned>(after) << sl;
     }
     if (gated && ((outs >> lane) & 1u) != prevbit) {  // pool.cpp:93-106
-      atomicXor(prev_row + (i >> 5), 1u << (i & 31));
+      red_xor_gpu(prev_row + (i >> 5), 1u << (i & 31));
       int delta = prevbit ? -1 : 1;
       if (!positive) delta = -delta;
       const size_t ti = static_cast<size_t>(i) * P.m + c;
-      atomicAdd(&P.tallies[ti], delta);
-      if (P.tally_delta) atomicAdd(&P.tally_delta[ti], delta);
-      for (int k = 0; k < P.npeers; ++k) atomicAdd(P.peer_tallies[k] + ti, delta);  // NVLink reduction
+      publish_tally(P, ti, delta);  // local replica (+ window deltas, + peers over NVLink)
     }
   }
   __syncwarp();
