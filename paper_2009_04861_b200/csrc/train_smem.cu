@@ -25,7 +25,12 @@ namespace {
 #define TMG_STEP_SAT_SMEM 1  // clause-output-1 Type I as one up/down pass (tm_device.cuh type_i_planes)
 #endif
 
+#ifndef TMG_SMEM_MAXCPB
+#define TMG_SMEM_MAXCPB 2  // most clauses (warps) per CTA; the launcher picks the count with the most warps per SM
+#endif
+
 constexpr int kSmemUnroll = TMG_SMEM_UNROLL;
+constexpr int kSmemMaxCpb = TMG_SMEM_MAXCPB;
 constexpr size_t kSmemMax = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 
 template <int B>
@@ -149,7 +154,7 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& 
 // 8 planes): one clause per CTA, the planes stay in HBM/L2 and are updated in
 // place (every word is lane-owned), shared memory holds the alias table only.
 template <int NW, int B, bool P2, bool INPLACE = false>
-__global__ void __launch_bounds__(64) train_async_smem_kernel(TrainParams P) {
+__global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(TrainParams P) {
   extern __shared__ uint32_t smem[];
   const int Wp = P.Wp;
   const int cpb = blockDim.x >> 5;
@@ -255,8 +260,22 @@ size_t smem_bytes(int B, int Wp, int cpb) {
 
 template <int NW, int B, bool P2>
 bool launch_smem_p2(const TrainParams& p, cudaStream_t s, int* blocks) {
-  // Two clauses per CTA where they fit, else one; none: planes in place.
-  const int cpb = smem_bytes(B, p.Wp, 2) <= kSmemMax ? 2 : 1;
+  // Clauses per CTA: the count (<= kSmemMaxCpb) with the most resident warps
+  // per SM (every CTA carries its own alias table); none fits: planes in place.
+  int cpb = 1, best = 0;
+  for (int c = 1; c <= kSmemMaxCpb; ++c) {
+    const size_t b = smem_bytes(B, p.Wp, c);
+    if (b > kSmemMax) break;
+    if (b > 48 * 1024)
+      cudaFuncSetAttribute(train_async_smem_kernel<NW, B, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(b));
+    int ctas = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, train_async_smem_kernel<NW, B, P2>, 32 * c, b);
+    if (ctas * c > best) {
+      best = ctas * c;
+      cpb = c;
+    }
+  }
   const size_t shm = smem_bytes(B, p.Wp, cpb);
   const int clauses = p.m * p.n_loc;
   if (shm > kSmemMax) {
