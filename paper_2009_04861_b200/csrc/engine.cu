@@ -442,6 +442,9 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
   tmg::TrainParams p = make_params(tm, pool);
   p.t_begin = t0;
   p.t_end = t1;
+  if (with_delta && !pool->peers.empty())
+    fail(TMG_EINVAL, "pool has peer tally replicas attached: the windowed exchange would count every change twice "
+                     "(detach with tmg_pool_set_peers(pool, NULL, 0))");
   if (with_delta) p.tally_delta = pool->delta.ptr;
   int blocks = 0;
   // Register-resident clauses up to 4 words per lane per part (o <= 4096);

@@ -47,6 +47,11 @@ def _worker(rank, world, port, out_dir, overlapped=False):
     eng = D.GpuShardEngine(tm, pool)
     if overlapped == "peer":
         assert D.attach_peer_tallies(pool) == world - 1
+        try:  # mixing the exchanges would count every tally change twice: refused
+            D.train_epoch_overlapped(tm, pool, 0, windows=2)
+            raise AssertionError("windowed exchange accepted a pool with peer replicas")
+        except ValueError as e:  # std::invalid_argument
+            assert "peer tally replicas" in str(e)
     for e in range(2):
         if overlapped == "peer":
             D.train_epoch_peer(tm, pool, e)
