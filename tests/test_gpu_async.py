@@ -214,10 +214,13 @@ def test_async_window_accounting():
 
 @pytest.mark.parametrize("o,N,s,boost,out", [(12, 128, 3.9, False, 0), (12, 128, 3.9, False, 1),
                                              (12, 128, 4.0, True, 1), (784, 128, 10.0, False, 0),
-                                             (784, 128, 10.0, False, 1), (40, 5, 2.0, False, 1)])
+                                             (784, 128, 10.0, False, 1), (40, 5, 2.0, False, 1),
+                                             (12, 128, 1.5, False, 0), (12, 128, 1.5, False, 1),
+                                             (12, 128, 15.0, False, 0), (12, 128, 15.0, True, 1)])
 def test_type_i_table1_conformance(o, N, s, boost, out):
     """SPEC acceptance 1: Table 1 transition frequencies of the
-    asynchronous Philox/bit-serial sampler within +-0.02 over 1e5 draws."""
+    asynchronous Philox/bit-serial sampler within +-0.02 over 1e5 draws, at
+    the criterion's s = 1.5, 4, 15 and the configs' 3.9 and 10."""
     from paper_2009_04861_b200.tsetlin import feedback_rates
     rng = np.random.default_rng(o + N)
     x = (rng.random(o) < 0.5).astype(np.uint8)
