@@ -171,7 +171,7 @@ __device__ __forceinline__ void record(const TrainParams& P, uint32_t* prev_row,
 template <int NW, int B, bool P2>
 __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32_t (&x)[NW], const uint32_t (&n)[NW],
                                              int before, const TrainParams& P, uint32_t g, uint32_t i,
-                                             int lane, const uint32_t* atab) {
+                                             int lane, AliasRef atab) {
   constexpr int K = 2 * NW;
   uint32_t need[K], sel[K], bern[K];
 #pragma unroll
@@ -215,7 +215,7 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32
   if (before && !P.alias_sel) {
     bernoulli_words<K, true>(need, sel, P.bern, bern, gen);
   } else {
-    alias_words<K>(need, atab, static_cast<uint32_t>(lane) & (kAliasCopies - 1), bern, gen);
+    alias_words<K>(need, atab, bern, gen);
     // Clause output 1: a true literal fires w.p. p_high = 1 - p_low, a false
     // one w.p. p_low, so one Bernoulli(p_low) bit serves either, negated on
     // the true literals (independence across literals is untouched).
@@ -291,6 +291,21 @@ __device__ __forceinline__ int64_t clause_offset_dev(uint32_t g, int64_t q) {
 
 // Copies the machine's alias table (P.alias8, 256 entries) into kAliasCopies
 // interleaved shared-memory copies; every thread of the CTA takes part.
+// This lane's view of the alias image. TMG_ALIAS_HOIST: computed once in the
+// kernel prologue and kept in two registers (an opaque copy stops the
+// compiler from re-deriving it from %laneid at every Type I event).
+#ifndef TMG_ALIAS_HOIST
+#define TMG_ALIAS_HOIST 1
+#endif
+__device__ __forceinline__ AliasRef lane_alias(const uint32_t* tab, int lane) {
+  AliasRef r = alias_ref(tab, static_cast<uint32_t>(lane) & (kAliasCopies - 1));
+#if TMG_ALIAS_HOIST
+  asm volatile("mov.u32 %0, %0;" : "+r"(r.base));
+  asm volatile("mov.u32 %0, %0;" : "+r"(r.pbase));
+#endif
+  return r;
+}
+
 __device__ __forceinline__ void load_alias(const TrainParams& P, uint32_t* tab) {
 #if TMG_ALIAS
   fill_alias(tab, P.alias8, threadIdx.x, blockDim.x);

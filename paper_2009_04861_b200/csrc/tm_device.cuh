@@ -278,14 +278,20 @@ __device__ __forceinline__ void fill_alias(uint32_t* tab, const uint32_t* entrie
   }
 }
 
+// Shared-space byte addresses of a lane's copies of column 0 of the alias
+// image (threshold and pattern); column c is 4 * kAliasCopies * c
+// (kAliasCopies * c) further (one IMAD per lookup, on the FMA pipe).
+struct AliasRef {
+  uint32_t base, pbase;
+};
+__device__ __forceinline__ AliasRef alias_ref(const uint32_t* tab, uint32_t laneoff) {
+  return AliasRef{static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 4u * laneoff,
+                  static_cast<uint32_t>(__cvta_generic_to_shared(tab + 256 * kAliasCopies)) + laneoff};
+}
+
 template <int K, bool SPLIT = true, typename Gen>
-__device__ __forceinline__ void alias_words(const uint32_t (&need)[K], const uint32_t* tab, uint32_t laneoff,
-                                            uint32_t (&bern)[K], Gen&& gen) {
-  // Shared-space byte addresses of this lane's copies of column 0 (threshold
-  // and pattern); column c is 4 * kAliasCopies * c (kAliasCopies * c) further
-  // (one IMAD per lookup, on the FMA pipe).
-  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 4u * laneoff;
-  const uint32_t pbase = static_cast<uint32_t>(__cvta_generic_to_shared(tab + 256 * kAliasCopies)) + laneoff;
+__device__ __forceinline__ void alias_words(const uint32_t (&need)[K], AliasRef ar, uint32_t (&bern)[K], Gen&& gen) {
+  const uint32_t base = ar.base, pbase = ar.pbase;
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const U4 r = gen(k, 0);

@@ -41,6 +41,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   __shared__ uint32_t atab[TMG_ALIAS ? kAliasWords : 1];
   load_alias(P, atab);
   const int lane = static_cast<int>(lane_id());
+  const AliasRef aref = lane_alias(atab, lane);
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= P.m * P.n_loc) return;
   const int c = lc / P.n_loc;
@@ -101,7 +102,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       if (cd >= 0) {
         if (before && cl.type_ii(xs, ns)) after = cl.eval_train(xs, ns);
       } else {
-        type_i_async<NW, B, P2>(cl, xs, ns, before, P, g, static_cast<uint32_t>(~cd), lane, atab);
+        type_i_async<NW, B, P2>(cl, xs, ns, before, P, g, static_cast<uint32_t>(~cd), lane, aref);
         after = cl.eval_train(xs, ns);
       }
       outs = mad_u32(sl, static_cast<uint32_t>(after), outs);  // disjoint bits: OR as an FMA-pipe add
@@ -468,7 +469,7 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
     Clause<NW, B> cl, c0;
     cl.load(state0, P.Wp, lane, P.o);
     c0 = cl;
-    type_i_async<NW, B, false>(cl, x, n, out, P, 0u, trial, lane, atab);
+    type_i_async<NW, B, false>(cl, x, n, out, P, 0u, trial, lane, lane_alias(atab, lane));
 #pragma unroll
     for (int p = 0; p < NW; ++p)
 #pragma unroll
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(32) type_i_async_once_kernel(TrainParams P, ui
     x[p] = P.xplane[p * 32 + lane];
     n[p] = P.nplane[p * 32 + lane];
   }
-  type_i_async<NW, B, P2>(cl, x, n, out, P, g, i, lane, atab);
+  type_i_async<NW, B, P2>(cl, x, n, out, P, g, i, lane, lane_alias(atab, lane));
   cl.store(state, P.Wp, lane);
 }
 

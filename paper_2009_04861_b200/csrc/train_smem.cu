@@ -104,7 +104,7 @@ __device__ __forceinline__ uint32_t valid_of(int w, int o) {
 // or the bit-serial sampler when p_high != 1 - p_low.
 template <int NW, int B, bool P2, int OUT>
 __device__ __forceinline__ void type_i_smem_out(SmemPlanes<B>& S, const LitRow<NW>& r, const TrainParams& P,
-                                                uint32_t g, uint32_t i32, int lane, const uint32_t* atab) {
+                                                uint32_t g, uint32_t i32, int lane, AliasRef aref) {
   constexpr int before = OUT;
 #pragma unroll kSmemUnroll
   for (int p = 0; p < r.words(); ++p) {
@@ -121,7 +121,7 @@ __device__ __forceinline__ void type_i_smem_out(SmemPlanes<B>& S, const LitRow<N
     if (before && !P.alias_sel) {
       bernoulli_words<2, true>(need, sel, P.bern, bern, gen);
     } else {
-      alias_words<2, false>(need, atab, static_cast<uint32_t>(lane) & (kAliasCopies - 1), bern, gen);
+      alias_words<2, false>(need, aref, bern, gen);
       if (before) {
         bern[0] = (bern[0] ^ sel[0]) & need[0];
         bern[1] = (bern[1] ^ sel[1]) & need[1];
@@ -141,11 +141,11 @@ __device__ __forceinline__ void type_i_smem_out(SmemPlanes<B>& S, const LitRow<N
 // The clause output is warp-uniform: one branch, each arm with a constant one.
 template <int NW, int B, bool P2>
 __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& r, int before, const TrainParams& P,
-                                            uint32_t g, uint32_t i32, int lane, const uint32_t* atab) {
+                                            uint32_t g, uint32_t i32, int lane, AliasRef aref) {
   if (before)
-    type_i_smem_out<NW, B, P2, 1>(S, r, P, g, i32, lane, atab);
+    type_i_smem_out<NW, B, P2, 1>(S, r, P, g, i32, lane, aref);
   else
-    type_i_smem_out<NW, B, P2, 0>(S, r, P, g, i32, lane, atab);
+    type_i_smem_out<NW, B, P2, 0>(S, r, P, g, i32, lane, aref);
 }
 
 // One warp per clause, blockDim.x / 32 clauses per CTA; dynamic shared memory
@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const AliasRef aref = lane_alias(atab, lane);
   const int wib = threadIdx.x >> 5;
   const int lc = blockIdx.x * cpb + wib;
   if (lc >= P.m * P.n_loc) return;
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
           if (__any_sync(kFull, moved != 0)) after = eval_train_smem<NW, B>(S, r, lane);
         }
       } else {  // Type I (feedback.cpp:32-70), one word pair at a time
-        type_i_smem<NW, B, P2>(S, r, before, P, g, static_cast<uint32_t>(is), lane, atab);
+        type_i_smem<NW, B, P2>(S, r, before, P, g, static_cast<uint32_t>(is), lane, aref);
         after = eval_train_smem<NW, B>(S, r, lane);
       }
       outs |= static_cast<unsigned>(after) << sl;
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(32) type_i_smem_once_kernel(TrainParams P, uin
   SmemPlanes<B> S{smem, P.Wp};
   LitRow<NW> r;
   r.load(P.xplane + lane, P.Wp);
-  type_i_smem<NW, B, P2>(S, r, out, P, g, i, lane, atab);
+  type_i_smem<NW, B, P2>(S, r, out, P, g, i, lane, lane_alias(atab, lane));
   for (size_t k = lane; k < words; k += 32) state[k] = smem[k];
 }
 
