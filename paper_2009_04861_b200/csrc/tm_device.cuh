@@ -173,17 +173,39 @@ __device__ __forceinline__ void step_down(Planes<B>& s, uint32_t dec, uint32_t l
 // borrow (carry) chain is formed first; what leaves the top plane is exactly
 // the set of lanes already at lo (hi), which are then left untouched. One
 // LOP3 per plane for the chain and one for the flip, no separate compare.
-template <int B>
+// One LOP3 with an explicit truth table (inputs a = 0xF0, b = 0xCC, c = 0xAA).
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return d;
+}
+
+// EXPL: the chains as explicit LOP3s. In the register kernel ptxas rewrites
+// the plain form into 3 LOP3 per plane plus moves and is still faster (MNIST
+// 69.8 vs 70.3 ms); in the shared-memory kernel the explicit form wins (IMDb
+// 231.4 vs 235.3 ms).
+template <int B, bool EXPL = false>
 __device__ __forceinline__ void sub_one_sat0(Planes<B>& s, uint32_t dec) {
   uint32_t chain[B];
   uint32_t t = dec;
+  if constexpr (EXPL) {
 #pragma unroll
-  for (int b = 0; b < B; ++b) {
-    chain[b] = t;
-    t &= ~s.p[b];
+    for (int b = 0; b < B; ++b) {
+      chain[b] = t;
+      t = lop3<0x30>(t, s.p[b], 0u);  // t & ~p
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) s.p[b] = lop3<0xB4>(s.p[b], chain[b], t);  // p ^ (chain & ~t)
+  } else {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      chain[b] = t;
+      t &= ~s.p[b];
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
   }
-#pragma unroll
-  for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
 }
 
 // Both at once (P2 layout): lanes in `move` take one step, down (-1) where
@@ -193,17 +215,27 @@ __device__ __forceinline__ void sub_one_sat0(Planes<B>& s, uint32_t dec) {
 // top plane is the set of lanes already saturated in their direction, which
 // are left untouched -- the same result as a saturating +1 pass then a
 // saturating -1 pass on disjoint masks, at half the cost.
-template <int B>
+template <int B, bool EXPL = false>
 __device__ __forceinline__ void step_sat(Planes<B>& s, uint32_t move, uint32_t down) {
   uint32_t chain[B];
   uint32_t t = move;
+  if constexpr (EXPL) {
 #pragma unroll
-  for (int b = 0; b < B; ++b) {
-    chain[b] = t;
-    t &= s.p[b] ^ down;
+    for (int b = 0; b < B; ++b) {
+      chain[b] = t;
+      t = lop3<0x60>(t, s.p[b], down);  // t & (p ^ down)
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) s.p[b] = lop3<0xB4>(s.p[b], chain[b], t);  // p ^ (chain & ~t)
+  } else {
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      chain[b] = t;
+      t &= s.p[b] ^ down;
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
   }
-#pragma unroll
-  for (int b = 0; b < B; ++b) s.p[b] ^= chain[b] & ~t;
 }
 
 
@@ -217,26 +249,26 @@ __device__ __forceinline__ void step_sat(Planes<B>& s, uint32_t move, uint32_t d
 // then a -1 pass. Fewer instructions, but measured slower in the register
 // kernel (MNIST 72.8 vs 71.4 ms, FMNIST 656 vs 650 ms) and faster in the
 // shared-memory one (IMDb 235.3 vs 236.2 ms), so each kernel picks its own.
-template <int B, bool P2, bool FUSED = true>
+template <int B, bool P2, bool FUSED = true, bool EXPL = false>
 __device__ __forceinline__ void type_i_planes(Planes<B>& w, uint32_t lit, int out, int boost, uint32_t bern,
                                               uint32_t valid, uint32_t lo, uint32_t hi) {
   if (out) {
     const uint32_t incl = w.p[B - 1];
     if (P2 && FUSED) {  // one up/down pass: false literals of excluded automata step down
       const uint32_t move = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern)) & valid;
-      step_sat<B>(w, move, ~(lit | incl));
+      step_sat<B, EXPL>(w, move, ~(lit | incl));
     } else if (P2) {  // the same as two saturating passes on disjoint masks
       const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid;
       const uint32_t dec = ~lit & bern & ~incl & valid;
-      step_sat<B>(w, inc, 0u);
-      sub_one_sat0<B>(w, dec);
+      step_sat<B, EXPL>(w, inc, 0u);
+      sub_one_sat0<B, EXPL>(w, dec);
     } else {
       const uint32_t inc = ((lit & (bern | (boost ? incl : 0u))) | (~lit & bern & incl)) & valid;
       const uint32_t dec = ~lit & bern & ~incl & valid;
       step<B>(w, inc, dec, lo, hi);
     }
   } else if (P2) {
-    sub_one_sat0<B>(w, bern & valid);
+    sub_one_sat0<B, EXPL>(w, bern & valid);
   } else {
     step_down<B>(w, bern & valid, lo);
   }

@@ -131,7 +131,7 @@ __device__ __forceinline__ void type_i_smem_out(SmemPlanes<B>& S, const LitRow<N
     for (int part = 0; part < 2; ++part) {
       Planes<B> pl;
       S.get(part, w, pl);
-      type_i_planes<B, P2, TMG_STEP_SAT_SMEM != 0>(pl, sel[part], before, P.boost, bern[part], vm, P.lo, P.hi);
+      type_i_planes<B, P2, TMG_STEP_SAT_SMEM != 0, true>(pl, sel[part], before, P.boost, bern[part], vm, P.lo, P.hi);
       S.put(part, w, pl);
     }
   }
