@@ -91,6 +91,15 @@ struct SeqParams {  // classic sequential trainer mirror (trainer.cpp:138-179)
   uint64_t* rng;  // xoshiro state after the epoch shuffle (written back at the end)
   double p_high, p_low;
   unsigned long long* events;  // [m]
+  // Parallel replay of the Type I draws (null: the serial replay). The
+  // xoshiro256 state transition is linear over GF(2); jump_chunk = M^chunk
+  // and jump_lits = M^(2o) as 256 x 256 bit matrices in the lane-interleaved
+  // layout [row % 8][word][row / 8] (see sequential.cu gf2_apply).
+  const uint32_t* jump_chunk;
+  const uint32_t* jump_lits;
+  int32_t chunk;          // draws per lane: ceil(2o / 32)
+  int32_t par_warps;      // warps applying gated clauses in parallel (each with its own draw buffers)
+  uint64_t* tstate;       // [n][4]: a gated Type I clause's generator state at its first draw
 };
 bool train_sequential_launch(const TrainParams& p, const SeqParams& sp, int B, cudaStream_t s);
 

@@ -9,6 +9,8 @@
 // literal order, the negative-class draw below(m-1) — exactly the reference's
 // draw order, so automaton states match bit for bit. The automata are read
 // and written in place in their bit-plane layout (any NW, any B).
+#include <algorithm>
+
 #include "kernels.h"
 #include "tm_device.cuh"
 
@@ -48,6 +50,45 @@ __device__ __forceinline__ uint32_t valid_bits(int w, int o) {
   return first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
 }
 
+// ---- xoshiro256 jump-ahead on the GPU: the state update of rng.hpp next()
+// is linear over GF(2), so k steps are one 256 x 256 bit matrix (built on the
+// host, engine.cu seq_jump_rows). A warp applies it cooperatively: lane L
+// computes output bits 8L .. 8L+7 (row r of that byte: parity(row & s)),
+// the 32 bytes are gathered with one OR-reduction per 32-bit word. The
+// matrix lives in shared memory as [r][w][L] (row 8L + r, word w), so for a
+// fixed (r, w) the 32 lanes read 32 consecutive words (no bank conflicts).
+__device__ __forceinline__ void gf2_apply(const uint32_t* mt, uint32_t (&s)[8], int lane) {
+  uint32_t byte = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) acc ^= mt[(r * 8 + w) * 32 + lane] & s[w];
+    byte |= (static_cast<uint32_t>(__popc(acc)) & 1u) << r;
+  }
+  const uint32_t mine = byte << (8 * (lane & 3));
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s[w] = __reduce_or_sync(kFull, (lane >> 2) == w ? mine : 0u);
+}
+
+__device__ __forceinline__ void state_to_words(const Xoshiro& r, uint32_t (&s)[8]) {
+  const uint64_t q[4] = {r.s0, r.s1, r.s2, r.s3};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    s[2 * k] = static_cast<uint32_t>(q[k]);
+    s[2 * k + 1] = static_cast<uint32_t>(q[k] >> 32);
+  }
+}
+
+__device__ __forceinline__ Xoshiro words_to_state(const uint32_t (&s)[8]) {
+  Xoshiro r;
+  r.s0 = s[0] | static_cast<uint64_t>(s[1]) << 32;
+  r.s1 = s[2] | static_cast<uint64_t>(s[3]) << 32;
+  r.s2 = s[4] | static_cast<uint64_t>(s[5]) << 32;
+  r.s3 = s[6] | static_cast<uint64_t>(s[7]) << 32;
+  return r;
+}
+
 template <int B>
 __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainParams P, SeqParams S) {
   extern __shared__ uint32_t smem[];
@@ -56,6 +97,13 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
   uint32_t* hbits = smem;                 // u < p_high, reference literal order
   uint32_t* lbits = smem + refw;          // u < p_low
   uint32_t* outs = smem + 2 * refw;       // clause outputs of the fed bank (bit per clause)
+  // parallel replay (S.jump_chunk != null): jump matrices, gated bits, and
+  // per-warp draw buffers (hbits / lbits of the clause a warp is applying)
+  const int nwords = (P.n + 31) / 32;
+  uint32_t* jc = outs + nwords;
+  uint32_t* jl = jc + 2048;
+  uint32_t* gbits = jl + 2048;
+  uint32_t* wbuf = gbits + nwords;
   __shared__ int vote;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int n = P.n, Wp = P.Wp, T = P.margin;
@@ -63,6 +111,13 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
   Xoshiro rng{S.rng[0], S.rng[1], S.rng[2], S.rng[3]};
   unsigned long long ev_local = 0;
   for (int k = tid; k < 2 * refw; k += blockDim.x) smem[k] = 0;
+  const bool par = S.jump_chunk != nullptr;
+  if (par) {
+    for (int k = tid; k < 2048; k += blockDim.x) {
+      jc[k] = S.jump_chunk[k];
+      jl[k] = S.jump_lits[k];
+    }
+  }
 
   for (int64_t t = 0; t < P.q; ++t) {
     const int64_t i = P.order[t];
@@ -108,6 +163,153 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
         }
       }
       __syncthreads();
+      if (par) {
+        // ---- parallel replay. (1) warp 0 scans the clauses in order with the
+        // reference stream: one gate draw each; a gated Type I clause's 2o
+        // draws are skipped with one jump (M^(2o)) after recording the state
+        // they start from. (2) every warp applies gated clauses; a Type I
+        // clause regenerates its draws from the recorded state, lane L
+        // taking draws [L*chunk, (L+1)*chunk) from the state M^(L*chunk) s.
+        const int v0 = vote;
+        double p;
+        bool regress_type1 = false;
+        if (P.regress) {  // regression.cpp:46-48, 145-151 (t = scaled target)
+          const int vc = v0 < 0 ? 0 : (v0 > T ? T : v0);
+          const int e = y > vc ? y - vc : vc - y;
+          p = fmin(1.0, static_cast<double>(e) / (2.0 * static_cast<double>(T)));
+          regress_type1 = vc < y;
+        } else {
+          const int vc = v0 < -T ? -T : (v0 > T ? T : v0);
+          const int e = target ? T - vc : T + vc;
+          p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+        }
+        if (warp == 0) {
+          unsigned long long gated_n = 0;
+          for (int j0 = 0; j0 < n; j0 += 32) {
+            uint32_t gw = 0;
+            for (int j = j0; j < min(n, j0 + 32); ++j) {
+              int gated = 0;
+              if (lane == 0) gated = rng.uniform() < p ? 1 : 0;
+              gated = __shfl_sync(kFull, gated, 0);
+              if (!gated) continue;
+              gw |= 1u << (j - j0);
+              ++gated_n;
+              const bool positive = P.all_positive || (j & 1) == 0;
+              const bool type2 = P.regress ? !regress_type1 : (target == 1) != positive;
+              if (!type2) {
+                uint64_t* ts = S.tstate + static_cast<size_t>(j) * 4;
+                if (lane == 0) {
+                  ts[0] = rng.s0;
+                  ts[1] = rng.s1;
+                  ts[2] = rng.s2;
+                  ts[3] = rng.s3;
+                }
+                uint32_t sw[8];
+                state_to_words(rng, sw);
+#pragma unroll
+                for (int w = 0; w < 8; ++w) sw[w] = __shfl_sync(kFull, sw[w], 0);
+                gf2_apply(jl, sw, lane);
+                rng = words_to_state(sw);
+              }
+            }
+            if (lane == 0) gbits[j0 >> 5] = gw;
+          }
+          if (lane == 0) S.events[c] += gated_n;
+        }
+        __syncthreads();
+        if (warp < S.par_warps) {
+          uint32_t* hb = wbuf + static_cast<size_t>(warp) * 2 * refw;
+          uint32_t* lb = hb + refw;
+          for (int j = warp; j < n; j += S.par_warps) {
+            if (!((gbits[j >> 5] >> (j & 31)) & 1u)) continue;
+            const int out = (outs[j >> 5] >> (j & 31)) & 1;
+            uint32_t* base = P.state + (static_cast<size_t>(c) * n + j) * cstride;
+            const bool positive = P.all_positive || (j & 1) == 0;
+            const bool type2 = P.regress ? !regress_type1 : (target == 1) != positive;
+            if (type2) {  // Type II (feedback.cpp:72-83)
+              if (out) {
+                for (int w = lane; w < Wp; w += 32) {
+                  const uint32_t vm = valid_bits(w, P.o);
+                  for (int part = 0; part < 2; ++part) {
+                    Planes<B> s;
+                    load_word<B>(base, Wp, part, w, s);
+                    const uint32_t lit = part ? nr[w] : xr[w];
+                    const uint32_t inc = ~lit & ~s.p[B - 1] & vm;
+                    if (inc) {
+                      add_one<B>(s, inc);
+                      store_word<B>(base, Wp, part, w, s);
+                    }
+                  }
+                }
+              }
+              continue;
+            }
+            // Type I: this lane's start state, M^(lane*chunk) applied to the recorded one
+            for (int k = lane; k < 2 * refw; k += 32) hb[k] = 0;
+            const uint64_t* ts = S.tstate + static_cast<size_t>(j) * 4;
+            Xoshiro r0{ts[0], ts[1], ts[2], ts[3]};
+            uint32_t sw[8], mine[8];
+            state_to_words(r0, sw);
+#pragma unroll
+            for (int w = 0; w < 8; ++w) mine[w] = sw[w];
+            for (int hop = 1; hop < 32; ++hop) {
+              if (hop * S.chunk >= L) break;  // warp-uniform
+              gf2_apply(jc, sw, lane);
+              if (lane == hop) {
+#pragma unroll
+                for (int w = 0; w < 8; ++w) mine[w] = sw[w];
+              }
+            }
+            __syncwarp();
+            Xoshiro rl = words_to_state(mine);
+            const int k0 = lane * S.chunk, k1 = min(L, k0 + S.chunk);
+            uint32_t hw = 0, lw = 0;
+            int cw = k0 >> 5;
+            for (int k = k0; k < k1; ++k) {
+              if ((k >> 5) != cw) {
+                if (hw) atomicOr(&hb[cw], hw);
+                if (lw) atomicOr(&lb[cw], lw);
+                hw = lw = 0;
+                cw = k >> 5;
+              }
+              const double u = rl.uniform();
+              hw |= (u < S.p_high ? 1u : 0u) << (k & 31);
+              lw |= (u < S.p_low ? 1u : 0u) << (k & 31);
+            }
+            if (k1 > k0) {
+              if (hw) atomicOr(&hb[cw], hw);
+              if (lw) atomicOr(&lb[cw], lw);
+            }
+            __syncwarp();
+            for (int w = lane; w < Wp; w += 32) {
+              if (w * 32 >= P.o) continue;
+              const uint32_t vm = valid_bits(w, P.o);
+              const int kk = P.o + w * 32;
+              const uint32_t hsel[2] = {hb[w], __funnelshift_r(hb[kk >> 5], hb[(kk >> 5) + 1], kk & 31)};
+              const uint32_t lsel[2] = {lb[w], __funnelshift_r(lb[kk >> 5], lb[(kk >> 5) + 1], kk & 31)};
+              for (int part = 0; part < 2; ++part) {
+                Planes<B> s;
+                load_word<B>(base, Wp, part, w, s);
+                const uint32_t lit = part ? nr[w] : xr[w];
+                uint32_t inc = 0, dec;
+                if (out) {
+                  const uint32_t bern = (lit & hsel[part]) | (~lit & lsel[part]);
+                  const uint32_t incl = s.p[B - 1];
+                  inc = ((lit & (bern | (P.boost ? incl : 0u))) | (~lit & bern & incl)) & vm;
+                  dec = ~lit & bern & ~incl & vm;
+                } else {
+                  dec = lsel[part] & vm;
+                }
+                step<B>(s, inc, dec, P.lo, P.hi);
+                store_word<B>(base, Wp, part, w, s);
+              }
+            }
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+        continue;
+      }
       // ---- serial gate + feedback replay by warp 0 (trainer.cpp:69-83)
       if (warp == 0) {
         const int v0 = vote;
@@ -206,9 +408,23 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
 
 }  // namespace
 
-bool train_sequential_launch(const TrainParams& p, const SeqParams& sp, int B, cudaStream_t s) {
+bool train_sequential_launch(const TrainParams& p, const SeqParams& sp_in, int B, cudaStream_t s) {
   const int refw = (2 * p.o + 31) / 32 + 2;
-  const size_t shm = sizeof(uint32_t) * (2 * refw + (p.n + 31) / 32);
+  const size_t nwords = (p.n + 31) / 32;
+  SeqParams sp = sp_in;
+  size_t words = 2 * refw + nwords;
+  if (sp.jump_chunk) {  // parallel replay: as many applying warps as shared memory holds draw buffers for
+    const size_t fixed = words + 4096 + nwords;
+    const size_t budget = 200 * 1024 / sizeof(uint32_t);
+    const long pw = fixed < budget ? static_cast<long>((budget - fixed) / (2 * refw)) : 0;
+    sp.par_warps = static_cast<int32_t>(std::min<long>(kSeqThreads / 32, pw));
+    if (sp.par_warps < 1) {
+      sp.jump_chunk = sp.jump_lits = nullptr;  // rows too wide for even one buffer: serial replay
+    } else {
+      words = fixed + static_cast<size_t>(sp.par_warps) * 2 * refw;
+    }
+  }
+  const size_t shm = sizeof(uint32_t) * words;
   auto go = [&](auto kern) {
     if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
     count_launch();

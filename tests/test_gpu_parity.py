@@ -185,3 +185,24 @@ def test_errors_follow_reference():
     with pytest.raises(IndexError):
         tm.banks[0].set_counters  # accessor exists
         T.update_clause(tm.banks[1], 9, pool2, 1, None, 0, 1, 15, 3.0, False, T.Rng(1))
+
+
+@pytest.mark.parametrize("kind,q,n", [("mnist", 60, 200), ("imdb", 12, 60), ("xor", 300, 20), ("fmnist", 20, 100)])
+def test_sequential_parallel_replay_matches_serial(kind, q, n, monkeypatch):
+    """train_epoch_sequential's parallel replay (gate scan with xoshiro
+    jump-ahead over the Type I draws, then every gated clause applied by its
+    own warp from its recorded generator state; sequential.cu) leaves exactly
+    the serial replay's automata, tallies and events — which
+    test_gpu_dropin.py pins to the reference's goldens."""
+    from paper_2009_04861_b200 import synth
+    d = synth.make(kind, q, 4, 7)
+    got = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("TMG_SEQ_SERIAL", mode)
+        tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=20, specificity=5.0, boost_true_positive=True, seed=3),
+                            d.features, d.classes)
+        pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes)
+        ev = [T.train_epoch_sequential(tm, pool, e).feedback_events for e in range(2)]
+        got[mode] = (np.stack([tm.banks[c].counters() for c in range(d.classes)]), ev)
+    assert got["0"][1] == got["1"][1]
+    assert np.array_equal(got["0"][0], got["1"][0])
