@@ -237,6 +237,39 @@ def other_configs(local):
     return out
 
 
+def sequential_line(local, with_ref: bool) -> dict:
+    """train_epoch_sequential, the reference's classic
+    trainer replayed bit-exactly on the GPU (gate scan with xoshiro jump-ahead,
+    gated clauses applied grid-wide), fresh machine, epoch 0, on the first
+    500 MNIST-shaped rows; the reference's own sequential trainer (one thread
+    by construction) on the same rows beside it. Equal feedback-event counts
+    are the bit-exactness check visible here (the tests compare states)."""
+    import paper_2009_04861_b200 as T
+    from paper_2009_04861_b200 import synth
+    q = 500
+    d = synth.make("mnist", q, 0, DATA_SEED)
+    tm = T.MultiClassTM(T.TMConfig(clauses=N_CLAUSES, margin=MARGIN, specificity=SPEC, seed=TM_SEED), O_FEAT,
+                        M_CLS, device=local)
+    pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M_CLS, device=local)
+    T.train_epoch_sequential(tm, pool, 0)  # warm-up (matrices, scratch)
+    tm.reset()
+    pool.reset_tallies()
+    rep = T.train_epoch_sequential(tm, pool, 0)
+    line = {"workload": f"mnist-784b-10c-{N_CLAUSES}cl train_epoch_sequential, fresh epoch 0, first {q} rows",
+            "seconds": rep.seconds, "examples_per_s": q / rep.seconds,
+            "feedback_events": rep.total_feedback_events()}
+    if with_ref and os.path.exists(REF_DRIVER):
+        args = [REF_DRIVER, "train", "--data", "mnist", "--mode", "seq", "--q", str(q), "--qtest", "0", "--clauses",
+                str(N_CLAUSES), "--T", str(MARGIN), "--s", str(SPEC), "--N", str(STATE_N), "--epochs", "1",
+                "--seed", str(TM_SEED), "--data-seed", str(DATA_SEED), "--eval", "0", "--fresh", "1"]
+        r = json.loads(subprocess.run(args, check=True, capture_output=True, text=True).stdout.splitlines()[-1])
+        line["reference"] = {"seconds": r["seconds"], "examples_per_s": q / r["seconds"], "cores": 1,
+                             "feedback_events": r["feedback_events"], "kind": "reference"}
+        line["speedup_vs_reference"] = r["seconds"] / rep.seconds
+        line["events_identical"] = r["feedback_events"] == rep.total_feedback_events()
+    return line
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -432,6 +465,7 @@ def run_ours(args):
         line["inference"] = inference_line(args, tm, d, local, stream)
         if not args.no_other_configs:
             line["other_configs"] = other_configs(local)
+            line["sequential_trainer"] = sequential_line(local, not args.no_cpu)
     # ---- CPU reference beside it (rank 0, N=1 only)
     if world == 1 and not args.no_cpu and os.path.exists(REF_DRIVER):
         cores = os.cpu_count() or 1

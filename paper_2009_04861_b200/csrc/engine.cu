@@ -252,6 +252,7 @@ struct tmg_machine {
   // sequential-trainer jump matrices (M^chunk, M^(2o)) and per-clause states
   DevBuf<uint32_t> seq_jump;
   DevBuf<uint64_t> seq_tstate;
+  DevBuf<uint32_t> seq_scratch;  // grid-wide replay: output / gated bits, votes, negative class
   bool entries_dirty = true;
   // current async epoch
   int32_t cur_epoch = -1;
@@ -507,6 +508,12 @@ bool seq_parallel_enabled(const tmg_machine* tm) {
   return tm->n >= 64 || 2 * tm->o >= 128;
 }
 
+// TMG_SEQ_GRID=0 keeps the parallel replay on one CTA (A/B checks).
+bool seq_grid_enabled() {
+  const char* e = std::getenv("TMG_SEQ_GRID");
+  return !(e && e[0] == '0');
+}
+
 // Fills the parallel-replay fields of sp (matrices cached on the machine).
 void seq_jumps(tmg_machine* tm, tmg::SeqParams& sp) {
   const int L = 2 * tm->o;
@@ -523,6 +530,14 @@ void seq_jumps(tmg_machine* tm, tmg::SeqParams& sp) {
   sp.jump_lits = tm->seq_jump.ptr + 2048;
   sp.chunk = chunk;
   sp.tstate = tm->seq_tstate.ptr;
+  if (seq_grid_enabled()) {
+    const size_t nwords = (static_cast<size_t>(tm->n) + 31) / 32;
+    if (tm->seq_scratch.count != 3 * nwords + 3) tm->seq_scratch.alloc(3 * nwords + 3);
+    CK(cudaMemsetAsync(tm->seq_scratch.ptr, 0, tm->seq_scratch.bytes(), tm->stream));
+    sp.g_outs = tm->seq_scratch.ptr;
+    sp.g_gbits = tm->seq_scratch.ptr + 2 * nwords;
+    sp.g_misc = reinterpret_cast<int32_t*>(tm->seq_scratch.ptr + 3 * nwords);
+  }
 }
 
 void epoch_keys(tmg_machine* tm, int32_t epoch) {

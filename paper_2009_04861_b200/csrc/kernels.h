@@ -100,6 +100,12 @@ struct SeqParams {  // classic sequential trainer mirror (trainer.cpp:138-179)
   int32_t chunk;          // draws per lane: ceil(2o / 32)
   int32_t par_warps;      // warps applying gated clauses in parallel (each with its own draw buffers)
   uint64_t* tstate;       // [n][4]: a gated Type I clause's generator state at its first draw
+  // grid-wide replay (cooperative launch over all SMs; null: one CTA):
+  // clause-output bits of the two alternating feed slots, gated bits, and
+  // [vote slot 0, vote slot 1, negative class]
+  uint32_t* g_outs;  // [2][ceil(n/32)]
+  uint32_t* g_gbits;  // [ceil(n/32)]
+  int32_t* g_misc;    // [3]
 };
 bool train_sequential_launch(const TrainParams& p, const SeqParams& sp, int B, cudaStream_t s);
 

@@ -11,6 +11,8 @@
 // and written in place in their bit-plane layout (any NW, any B).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "kernels.h"
 #include "tm_device.cuh"
 
@@ -89,6 +91,153 @@ __device__ __forceinline__ Xoshiro words_to_state(const uint32_t (&s)[8]) {
   return r;
 }
 
+// The gate probability of a fed bank (feedback.cpp:24-28; regression:
+// regression.cpp:46-48, 145-151) and, for regression, whether the step is Type I.
+__device__ __forceinline__ double bank_gate(const TrainParams& P, int v0, int y, int target, bool& regress_type1) {
+  const int T = P.margin;
+  regress_type1 = false;
+  if (P.regress) {
+    const int vc = v0 < 0 ? 0 : (v0 > T ? T : v0);
+    const int e = y > vc ? y - vc : vc - y;
+    regress_type1 = vc < y;
+    return fmin(1.0, static_cast<double>(e) / (2.0 * static_cast<double>(T)));
+  }
+  const int vc = v0 < -T ? -T : (v0 > T ? T : v0);
+  const int e = target ? T - vc : T + vc;
+  return static_cast<double>(e) / (2.0 * static_cast<double>(T));
+}
+
+__device__ __forceinline__ bool is_type2(const TrainParams& P, int j, int target, bool regress_type1) {
+  const bool positive = P.all_positive || (j & 1) == 0;
+  return P.regress ? !regress_type1 : (target == 1) != positive;
+}
+
+// Parallel replay, phase 1 (one warp, lane 0 owns the stream): gate draws in
+// clause order; a gated Type I clause's state is recorded in S.tstate and its
+// 2o draws skipped with one jump (jl = M^(2o)). Gated bits go to gbits.
+// Returns the number of gated clauses.
+__device__ unsigned long long scan_bank(const TrainParams& P, const SeqParams& S, Xoshiro& rng, double p, int target,
+                                        bool regress_type1, const uint32_t* jl, uint32_t* gbits, int lane) {
+  unsigned long long gated_n = 0;
+  for (int j0 = 0; j0 < P.n; j0 += 32) {
+    uint32_t gw = 0;
+    for (int j = j0; j < min(P.n, j0 + 32); ++j) {
+      int gated = 0;
+      if (lane == 0) gated = rng.uniform() < p ? 1 : 0;
+      gated = __shfl_sync(kFull, gated, 0);
+      if (!gated) continue;
+      gw |= 1u << (j - j0);
+      ++gated_n;
+      if (!is_type2(P, j, target, regress_type1)) {
+        uint64_t* ts = S.tstate + static_cast<size_t>(j) * 4;
+        if (lane == 0) {
+          ts[0] = rng.s0;
+          ts[1] = rng.s1;
+          ts[2] = rng.s2;
+          ts[3] = rng.s3;
+        }
+        uint32_t sw[8];
+        state_to_words(rng, sw);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sw[w] = __shfl_sync(kFull, sw[w], 0);
+        gf2_apply(jl, sw, lane);
+        rng = words_to_state(sw);
+      }
+    }
+    if (lane == 0) gbits[j0 >> 5] = gw;
+  }
+  return gated_n;
+}
+
+// Parallel replay, phase 2: one warp applies gated clause j of bank c
+// (feedback.cpp:32-99). A Type I clause regenerates its 2o draws from the
+// recorded state: lane L jumps to draw L * chunk (jc = M^chunk, applied lane
+// by lane) and draws its segment into the warp's hb / lb bit buffers.
+template <int B>
+__device__ void apply_gated(const TrainParams& P, const SeqParams& S, int c, int j, int out, bool type2,
+                            const uint32_t* xr, const uint32_t* nr, const uint32_t* jc, uint32_t* hb, uint32_t* lb,
+                            int refw, int lane) {
+  const int Wp = P.Wp, L = 2 * P.o;
+  uint32_t* base = P.state + (static_cast<size_t>(c) * P.n + j) * (static_cast<size_t>(B) * 2 * Wp);
+  if (type2) {  // Type II (feedback.cpp:72-83)
+    if (!out) return;
+    for (int w = lane; w < Wp; w += 32) {
+      const uint32_t vm = valid_bits(w, P.o);
+      for (int part = 0; part < 2; ++part) {
+        Planes<B> s;
+        load_word<B>(base, Wp, part, w, s);
+        const uint32_t lit = part ? nr[w] : xr[w];
+        const uint32_t inc = ~lit & ~s.p[B - 1] & vm;
+        if (inc) {
+          add_one<B>(s, inc);
+          store_word<B>(base, Wp, part, w, s);
+        }
+      }
+    }
+    return;
+  }
+  for (int k = lane; k < 2 * refw; k += 32) hb[k] = 0;  // hb, then lb
+  const uint64_t* ts = S.tstate + static_cast<size_t>(j) * 4;  // written by the scanning warp (L2 reads)
+  Xoshiro r0{__ldcg(ts), __ldcg(ts + 1), __ldcg(ts + 2), __ldcg(ts + 3)};
+  uint32_t sw[8], mine[8];
+  state_to_words(r0, sw);
+#pragma unroll
+  for (int w = 0; w < 8; ++w) mine[w] = sw[w];
+  for (int hop = 1; hop < 32; ++hop) {
+    if (hop * S.chunk >= L) break;  // warp-uniform
+    gf2_apply(jc, sw, lane);
+    if (lane == hop) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) mine[w] = sw[w];
+    }
+  }
+  __syncwarp();
+  Xoshiro rl = words_to_state(mine);
+  const int k0 = lane * S.chunk, k1 = min(L, k0 + S.chunk);
+  uint32_t hw = 0, lw = 0;
+  int cw = k0 >> 5;
+  for (int k = k0; k < k1; ++k) {
+    if ((k >> 5) != cw) {
+      if (hw) atomicOr(&hb[cw], hw);
+      if (lw) atomicOr(&lb[cw], lw);
+      hw = lw = 0;
+      cw = k >> 5;
+    }
+    const double u = rl.uniform();
+    hw |= (u < S.p_high ? 1u : 0u) << (k & 31);
+    lw |= (u < S.p_low ? 1u : 0u) << (k & 31);
+  }
+  if (k1 > k0) {
+    if (hw) atomicOr(&hb[cw], hw);
+    if (lw) atomicOr(&lb[cw], lw);
+  }
+  __syncwarp();
+  for (int w = lane; w < Wp; w += 32) {
+    if (w * 32 >= P.o) continue;
+    const uint32_t vm = valid_bits(w, P.o);
+    const int kk = P.o + w * 32;
+    const uint32_t hsel[2] = {hb[w], __funnelshift_r(hb[kk >> 5], hb[(kk >> 5) + 1], kk & 31)};
+    const uint32_t lsel[2] = {lb[w], __funnelshift_r(lb[kk >> 5], lb[(kk >> 5) + 1], kk & 31)};
+    for (int part = 0; part < 2; ++part) {
+      Planes<B> s;
+      load_word<B>(base, Wp, part, w, s);
+      const uint32_t lit = part ? nr[w] : xr[w];
+      uint32_t inc = 0, dec;
+      if (out) {
+        const uint32_t bern = (lit & hsel[part]) | (~lit & lsel[part]);
+        const uint32_t incl = s.p[B - 1];
+        inc = ((lit & (bern | (P.boost ? incl : 0u))) | (~lit & bern & incl)) & vm;
+        dec = ~lit & bern & ~incl & vm;
+      } else {
+        dec = lsel[part] & vm;
+      }
+      step<B>(s, inc, dec, P.lo, P.hi);
+      store_word<B>(base, Wp, part, w, s);
+    }
+  }
+  __syncwarp();
+}
+
 template <int B>
 __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainParams P, SeqParams S) {
   extern __shared__ uint32_t smem[];
@@ -164,147 +313,24 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
       }
       __syncthreads();
       if (par) {
-        // ---- parallel replay. (1) warp 0 scans the clauses in order with the
-        // reference stream: one gate draw each; a gated Type I clause's 2o
-        // draws are skipped with one jump (M^(2o)) after recording the state
-        // they start from. (2) every warp applies gated clauses; a Type I
-        // clause regenerates its draws from the recorded state, lane L
-        // taking draws [L*chunk, (L+1)*chunk) from the state M^(L*chunk) s.
-        const int v0 = vote;
-        double p;
-        bool regress_type1 = false;
-        if (P.regress) {  // regression.cpp:46-48, 145-151 (t = scaled target)
-          const int vc = v0 < 0 ? 0 : (v0 > T ? T : v0);
-          const int e = y > vc ? y - vc : vc - y;
-          p = fmin(1.0, static_cast<double>(e) / (2.0 * static_cast<double>(T)));
-          regress_type1 = vc < y;
-        } else {
-          const int vc = v0 < -T ? -T : (v0 > T ? T : v0);
-          const int e = target ? T - vc : T + vc;
-          p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
-        }
+        // ---- parallel replay: the gate scan by warp 0 (scan_bank), then the
+        // gated clauses applied one warp each (apply_gated).
+        bool regress_type1;
+        const double p = bank_gate(P, vote, y, target, regress_type1);
         if (warp == 0) {
-          unsigned long long gated_n = 0;
-          for (int j0 = 0; j0 < n; j0 += 32) {
-            uint32_t gw = 0;
-            for (int j = j0; j < min(n, j0 + 32); ++j) {
-              int gated = 0;
-              if (lane == 0) gated = rng.uniform() < p ? 1 : 0;
-              gated = __shfl_sync(kFull, gated, 0);
-              if (!gated) continue;
-              gw |= 1u << (j - j0);
-              ++gated_n;
-              const bool positive = P.all_positive || (j & 1) == 0;
-              const bool type2 = P.regress ? !regress_type1 : (target == 1) != positive;
-              if (!type2) {
-                uint64_t* ts = S.tstate + static_cast<size_t>(j) * 4;
-                if (lane == 0) {
-                  ts[0] = rng.s0;
-                  ts[1] = rng.s1;
-                  ts[2] = rng.s2;
-                  ts[3] = rng.s3;
-                }
-                uint32_t sw[8];
-                state_to_words(rng, sw);
-#pragma unroll
-                for (int w = 0; w < 8; ++w) sw[w] = __shfl_sync(kFull, sw[w], 0);
-                gf2_apply(jl, sw, lane);
-                rng = words_to_state(sw);
-              }
-            }
-            if (lane == 0) gbits[j0 >> 5] = gw;
-          }
-          if (lane == 0) S.events[c] += gated_n;
+          const unsigned long long g = scan_bank(P, S, rng, p, target, regress_type1, jl, gbits, lane);
+          if (lane == 0) S.events[c] += g;
         }
         __syncthreads();
-        if (warp < S.par_warps) {
+#ifndef TMG_SEQ_SKIP_APPLY
+#define TMG_SEQ_SKIP_APPLY 0  // timing experiment only: scan without applying (wrong results)
+#endif
+        if (!TMG_SEQ_SKIP_APPLY && warp < S.par_warps) {
           uint32_t* hb = wbuf + static_cast<size_t>(warp) * 2 * refw;
-          uint32_t* lb = hb + refw;
           for (int j = warp; j < n; j += S.par_warps) {
             if (!((gbits[j >> 5] >> (j & 31)) & 1u)) continue;
-            const int out = (outs[j >> 5] >> (j & 31)) & 1;
-            uint32_t* base = P.state + (static_cast<size_t>(c) * n + j) * cstride;
-            const bool positive = P.all_positive || (j & 1) == 0;
-            const bool type2 = P.regress ? !regress_type1 : (target == 1) != positive;
-            if (type2) {  // Type II (feedback.cpp:72-83)
-              if (out) {
-                for (int w = lane; w < Wp; w += 32) {
-                  const uint32_t vm = valid_bits(w, P.o);
-                  for (int part = 0; part < 2; ++part) {
-                    Planes<B> s;
-                    load_word<B>(base, Wp, part, w, s);
-                    const uint32_t lit = part ? nr[w] : xr[w];
-                    const uint32_t inc = ~lit & ~s.p[B - 1] & vm;
-                    if (inc) {
-                      add_one<B>(s, inc);
-                      store_word<B>(base, Wp, part, w, s);
-                    }
-                  }
-                }
-              }
-              continue;
-            }
-            // Type I: this lane's start state, M^(lane*chunk) applied to the recorded one
-            for (int k = lane; k < 2 * refw; k += 32) hb[k] = 0;
-            const uint64_t* ts = S.tstate + static_cast<size_t>(j) * 4;
-            Xoshiro r0{ts[0], ts[1], ts[2], ts[3]};
-            uint32_t sw[8], mine[8];
-            state_to_words(r0, sw);
-#pragma unroll
-            for (int w = 0; w < 8; ++w) mine[w] = sw[w];
-            for (int hop = 1; hop < 32; ++hop) {
-              if (hop * S.chunk >= L) break;  // warp-uniform
-              gf2_apply(jc, sw, lane);
-              if (lane == hop) {
-#pragma unroll
-                for (int w = 0; w < 8; ++w) mine[w] = sw[w];
-              }
-            }
-            __syncwarp();
-            Xoshiro rl = words_to_state(mine);
-            const int k0 = lane * S.chunk, k1 = min(L, k0 + S.chunk);
-            uint32_t hw = 0, lw = 0;
-            int cw = k0 >> 5;
-            for (int k = k0; k < k1; ++k) {
-              if ((k >> 5) != cw) {
-                if (hw) atomicOr(&hb[cw], hw);
-                if (lw) atomicOr(&lb[cw], lw);
-                hw = lw = 0;
-                cw = k >> 5;
-              }
-              const double u = rl.uniform();
-              hw |= (u < S.p_high ? 1u : 0u) << (k & 31);
-              lw |= (u < S.p_low ? 1u : 0u) << (k & 31);
-            }
-            if (k1 > k0) {
-              if (hw) atomicOr(&hb[cw], hw);
-              if (lw) atomicOr(&lb[cw], lw);
-            }
-            __syncwarp();
-            for (int w = lane; w < Wp; w += 32) {
-              if (w * 32 >= P.o) continue;
-              const uint32_t vm = valid_bits(w, P.o);
-              const int kk = P.o + w * 32;
-              const uint32_t hsel[2] = {hb[w], __funnelshift_r(hb[kk >> 5], hb[(kk >> 5) + 1], kk & 31)};
-              const uint32_t lsel[2] = {lb[w], __funnelshift_r(lb[kk >> 5], lb[(kk >> 5) + 1], kk & 31)};
-              for (int part = 0; part < 2; ++part) {
-                Planes<B> s;
-                load_word<B>(base, Wp, part, w, s);
-                const uint32_t lit = part ? nr[w] : xr[w];
-                uint32_t inc = 0, dec;
-                if (out) {
-                  const uint32_t bern = (lit & hsel[part]) | (~lit & lsel[part]);
-                  const uint32_t incl = s.p[B - 1];
-                  inc = ((lit & (bern | (P.boost ? incl : 0u))) | (~lit & bern & incl)) & vm;
-                  dec = ~lit & bern & ~incl & vm;
-                } else {
-                  dec = lsel[part] & vm;
-                }
-                step<B>(s, inc, dec, P.lo, P.hi);
-                store_word<B>(base, Wp, part, w, s);
-              }
-            }
-            __syncwarp();
+            apply_gated<B>(P, S, c, j, (outs[j >> 5] >> (j & 31)) & 1, is_type2(P, j, target, regress_type1), xr, nr,
+                           jc, hb, hb + refw, refw, lane);
           }
         }
         __syncthreads();
@@ -406,6 +432,107 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
   }
 }
 
+// The same parallel replay over the whole GPU (cooperative launch, one CTA
+// per SM): per fed bank, (a) every warp of the grid evaluates clauses for the
+// vote, (b) one warp scans the gates (the only owner of the stream, which
+// also draws the negative class first, trainer.cpp:159-165), (c) every warp
+// of the grid applies gated clauses — three grid barriers per feed. Buffers
+// alternate between two slots (feed, or example for regression); the scan
+// zeroes the slot not in use.
+template <int B>
+__global__ void __launch_bounds__(kSeqThreads) train_sequential_grid_kernel(TrainParams P, SeqParams S) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint32_t smem[];
+  const int L = 2 * P.o;
+  const int refw = (L + 31) / 32 + 2;
+  uint32_t* jc = smem;
+  uint32_t* jl = jc + 2048;
+  uint32_t* wbuf = jl + 2048;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int n = P.n, Wp = P.Wp, nwords = (n + 31) / 32;
+  const int gwarp = blockIdx.x * nwarps + warp, gwarps = gridDim.x * nwarps;
+  const bool lead = blockIdx.x == 0 && warp == 0;  // owns the reference stream
+  const size_t cstride = static_cast<size_t>(B) * 2 * Wp;
+  Xoshiro rng{S.rng[0], S.rng[1], S.rng[2], S.rng[3]};
+  for (int k = tid; k < 2048; k += blockDim.x) {
+    jc[k] = S.jump_chunk[k];
+    jl[k] = S.jump_lits[k];
+  }
+  __syncthreads();
+  const int feeds = P.regress ? 1 : 2;
+  int slot = 0;
+  for (int64_t t = 0; t < P.q; ++t) {
+    const int64_t i = P.order[t];
+    const int y = P.labels[i];
+    const uint32_t* xr = P.xplane + i * 2 * Wp;
+    const uint32_t* nr = P.nplane + i * 2 * Wp;
+    for (int feed = 0; feed < feeds; ++feed, slot ^= 1) {
+      const int c = P.regress ? 0 : (feed == 0 ? y : __ldcg(S.g_misc + 2));
+      const int target = feed == 0 ? 1 : 0;
+      uint32_t* outs = S.g_outs + static_cast<size_t>(slot) * nwords;
+      int32_t* vote = S.g_misc + slot;
+      // (a) vote pass (trainer.cpp:62-68)
+      for (int j = gwarp; j < n; j += gwarps) {
+        const uint32_t* top = P.state + (static_cast<size_t>(c) * n + j) * cstride + static_cast<size_t>(B - 1) * 2 * Wp;
+        uint32_t viol = 0, any = 0;
+        for (int w = lane; w < Wp; w += 32) {
+          // planes another SM may have updated: read through L2
+          const uint32_t ix = __ldcg(top + w), in = __ldcg(top + Wp + w);
+          viol |= (ix & ~xr[w]) | (in & ~nr[w]);
+          any |= ix | in;
+        }
+        const unsigned vb = __ballot_sync(kFull, viol != 0), ab = __ballot_sync(kFull, any != 0);
+        const int out = ab == 0 ? 1 : (vb == 0 ? 1 : 0);
+        if (lane == 0 && out) {
+          atomicOr(&outs[j >> 5], 1u << (j & 31));
+          atomicAdd(vote, (!P.all_positive && (j & 1)) ? -1 : 1);
+        }
+      }
+      grid.sync();
+      // (b) gate scan
+      if (lead) {
+        if (feed == 0 && !P.regress && lane == 0) {
+          int neg;
+          if (P.m == 2) {
+            neg = 1 - y;
+          } else {
+            neg = static_cast<int>(below_dev(rng, static_cast<uint32_t>(P.m - 1)));
+            if (neg >= y) ++neg;
+          }
+          S.g_misc[2] = neg;
+        }
+        bool rt1;
+        const double p = bank_gate(P, __ldcg(vote), y, target, rt1);
+        const unsigned long long g = scan_bank(P, S, rng, p, target, rt1, jl, S.g_gbits, lane);
+        if (lane == 0) S.events[c] += g;
+        uint32_t* other = S.g_outs + static_cast<size_t>(slot ^ 1) * nwords;
+        for (int k = lane; k < nwords; k += 32) other[k] = 0;
+        if (lane == 0) S.g_misc[slot ^ 1] = 0;
+      }
+      grid.sync();
+      // (c) apply the gated clauses
+      if (warp < S.par_warps) {
+        bool rt1;
+        (void)bank_gate(P, __ldcg(vote), y, target, rt1);
+        uint32_t* hb = wbuf + static_cast<size_t>(warp) * 2 * refw;
+        for (int j = blockIdx.x * S.par_warps + warp; j < n; j += gridDim.x * S.par_warps) {
+          if (!((__ldcg(S.g_gbits + (j >> 5)) >> (j & 31)) & 1u)) continue;
+          apply_gated<B>(P, S, c, j, (__ldcg(outs + (j >> 5)) >> (j & 31)) & 1, is_type2(P, j, target, rt1), xr, nr,
+                         jc, hb, hb + refw, refw, lane);
+        }
+      }
+      grid.sync();
+    }
+  }
+  if (lead && lane == 0) {
+    S.rng[0] = rng.s0;
+    S.rng[1] = rng.s1;
+    S.rng[2] = rng.s2;
+    S.rng[3] = rng.s3;
+  }
+}
+
 }  // namespace
 
 bool train_sequential_launch(const TrainParams& p, const SeqParams& sp_in, int B, cudaStream_t s) {
@@ -425,6 +552,31 @@ bool train_sequential_launch(const TrainParams& p, const SeqParams& sp_in, int B
     }
   }
   const size_t shm = sizeof(uint32_t) * words;
+  if (sp.jump_chunk && sp.g_outs) {  // grid-wide replay: one CTA per SM, as many as there are clauses for
+    const size_t gshm = sizeof(uint32_t) * (4096 + static_cast<size_t>(sp.par_warps) * 2 * refw);
+    auto grid_go = [&](auto kern) {
+      if (gshm > 48 * 1024)
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gshm));
+      int dev = 0, sms = 0, per_sm = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSeqThreads, gshm);
+      const int want = std::max(1, (p.n + sp.par_warps - 1) / sp.par_warps);
+      const int grid = std::max(1, std::min(sms * std::max(per_sm, 1), want));
+      TrainParams pp = p;
+      SeqParams ss = sp;
+      void* args[] = {&pp, &ss};
+      count_launch();
+      return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, kSeqThreads, args, gshm, s) ==
+             cudaSuccess;
+    };
+    switch (B) {
+      case 4: return grid_go(train_sequential_grid_kernel<4>);
+      case 8: return grid_go(train_sequential_grid_kernel<8>);
+      case 15: return grid_go(train_sequential_grid_kernel<15>);
+      default: return false;
+    }
+  }
   auto go = [&](auto kern) {
     if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
     count_launch();
