@@ -570,12 +570,15 @@ bool train_sequential_launch(const TrainParams& p, const SeqParams& sp_in, int B
       return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), grid, kSeqThreads, args, gshm, s) ==
              cudaSuccess;
     };
+    bool ok = false;
     switch (B) {
-      case 4: return grid_go(train_sequential_grid_kernel<4>);
-      case 8: return grid_go(train_sequential_grid_kernel<8>);
-      case 15: return grid_go(train_sequential_grid_kernel<15>);
+      case 4: ok = grid_go(train_sequential_grid_kernel<4>); break;
+      case 8: ok = grid_go(train_sequential_grid_kernel<8>); break;
+      case 15: ok = grid_go(train_sequential_grid_kernel<15>); break;
       default: return false;
     }
+    if (ok) return true;
+    cudaGetLastError();  // cooperative launch refused (e.g. the GPU is shared): one CTA instead
   }
   auto go = [&](auto kern) {
     if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
