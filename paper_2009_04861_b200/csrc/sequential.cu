@@ -322,10 +322,7 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
           if (lane == 0) S.events[c] += g;
         }
         __syncthreads();
-#ifndef TMG_SEQ_SKIP_APPLY
-#define TMG_SEQ_SKIP_APPLY 0  // timing experiment only: scan without applying (wrong results)
-#endif
-        if (!TMG_SEQ_SKIP_APPLY && warp < S.par_warps) {
+        if (warp < S.par_warps) {
           uint32_t* hb = wbuf + static_cast<size_t>(warp) * 2 * refw;
           for (int j = warp; j < n; j += S.par_warps) {
             if (!((gbits[j >> 5] >> (j & 31)) & 1u)) continue;
