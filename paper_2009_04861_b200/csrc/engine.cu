@@ -514,8 +514,8 @@ bool seq_grid_enabled() {
   return !(e && e[0] == '0');
 }
 
-// Fills the parallel-replay fields of sp (matrices cached on the machine).
-void seq_jumps(tmg_machine* tm, tmg::SeqParams& sp) {
+// M^ceil(2o/32) and M^(2o), built once per machine.
+void ensure_jumps(tmg_machine* tm) {
   const int L = 2 * tm->o;
   const int chunk = (L + 31) / 32;
   if (tm->seq_jump.count != 4096) {
@@ -525,6 +525,25 @@ void seq_jumps(tmg_machine* tm, tmg::SeqParams& sp) {
     tm->seq_jump.alloc(4096);
     CK(cudaMemcpy(tm->seq_jump.ptr, host.data(), 4096 * 4, cudaMemcpyHostToDevice));
   }
+}
+
+// The W = 1 replay (train_mirror_kernel) draws a Type I step's 2o uniforms
+// by jump-ahead once 2o is large enough for 32 matrix applications to beat
+// 2o serial draws. TMG_SEQ_SERIAL=1 keeps them serial (A/B checks).
+void mirror_jumps(tmg_machine* tm, tmg::MirrorParams& mp) {
+  const char* e = std::getenv("TMG_SEQ_SERIAL");
+  if ((e && e[0] == '1') || 2 * tm->o < 256) return;
+  ensure_jumps(tm);
+  mp.jump_chunk = tm->seq_jump.ptr;
+  mp.jump_lits = tm->seq_jump.ptr + 2048;
+  mp.chunk = (2 * tm->o + 31) / 32;
+}
+
+// Fills the parallel-replay fields of sp (matrices cached on the machine).
+void seq_jumps(tmg_machine* tm, tmg::SeqParams& sp) {
+  const int L = 2 * tm->o;
+  const int chunk = (L + 31) / 32;
+  ensure_jumps(tm);
   if (tm->seq_tstate.count != static_cast<size_t>(tm->n) * 4) tm->seq_tstate.alloc(static_cast<size_t>(tm->n) * 4);
   sp.jump_chunk = tm->seq_jump.ptr;
   sp.jump_lits = tm->seq_jump.ptr + 2048;
@@ -1212,6 +1231,7 @@ static int train_epoch_impl(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32
       mp.rng = drng.ptr;
       mp.p_high = (tm->cfg.specificity - 1.0) / tm->cfg.specificity;
       mp.p_low = 1.0 / tm->cfg.specificity;
+      mirror_jumps(tm, mp);
       if (!tmg::train_mirror_launch(p, mp, tm->B, tm->NW, tm->stream))
         fail(TMG_ERUNTIME, "no mirror kernel instantiation for this shape");
       CK(cudaGetLastError());
@@ -1452,6 +1472,7 @@ TMG_API int tmg_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t c, int32_
     mp.rng = drng.ptr;
     mp.p_high = (s - 1.0) / s;
     mp.p_low = 1.0 / s;
+    mirror_jumps(tm, mp);
     if (!tmg::train_mirror_launch(p, mp, tm->B, tm->NW, tm->stream))
       fail(TMG_ERUNTIME, "no mirror kernel instantiation for this shape");
     CK(cudaGetLastError());
@@ -1516,6 +1537,7 @@ TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_
     mp.rng = drng.ptr;
     mp.p_high = (s - 1.0) / s;
     mp.p_low = 1.0 / s;
+    mirror_jumps(tm, mp);
     if (!tmg::train_mirror_launch(p, mp, tm->B, tm->NW, tm->stream))
       fail(TMG_ERUNTIME, "no mirror kernel instantiation for this shape");
     CK(cudaGetLastError());

@@ -85,6 +85,10 @@ struct MirrorParams {
   int32_t njobs;
   uint64_t* rng;  // [workers][4] xoshiro states, in/out
   double p_high, p_low;
+  // Type I draws by warp-cooperative jump-ahead (as SeqParams; null: lane 0 draws them serially)
+  const uint32_t* jump_chunk;
+  const uint32_t* jump_lits;
+  int32_t chunk;
 };
 
 struct SeqParams {  // classic sequential trainer mirror (trainer.cpp:138-179)

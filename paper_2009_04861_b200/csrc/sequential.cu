@@ -52,45 +52,6 @@ __device__ __forceinline__ uint32_t valid_bits(int w, int o) {
   return first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
 }
 
-// ---- xoshiro256 jump-ahead on the GPU: the state update of rng.hpp next()
-// is linear over GF(2), so k steps are one 256 x 256 bit matrix (built on the
-// host, engine.cu seq_jump_rows). A warp applies it cooperatively: lane L
-// computes output bits 8L .. 8L+7 (row r of that byte: parity(row & s)),
-// the 32 bytes are gathered with one OR-reduction per 32-bit word. The
-// matrix lives in shared memory as [r][w][L] (row 8L + r, word w), so for a
-// fixed (r, w) the 32 lanes read 32 consecutive words (no bank conflicts).
-__device__ __forceinline__ void gf2_apply(const uint32_t* mt, uint32_t (&s)[8], int lane) {
-  uint32_t byte = 0;
-#pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    uint32_t acc = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) acc ^= mt[(r * 8 + w) * 32 + lane] & s[w];
-    byte |= (static_cast<uint32_t>(__popc(acc)) & 1u) << r;
-  }
-  const uint32_t mine = byte << (8 * (lane & 3));
-#pragma unroll
-  for (int w = 0; w < 8; ++w) s[w] = __reduce_or_sync(kFull, (lane >> 2) == w ? mine : 0u);
-}
-
-__device__ __forceinline__ void state_to_words(const Xoshiro& r, uint32_t (&s)[8]) {
-  const uint64_t q[4] = {r.s0, r.s1, r.s2, r.s3};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    s[2 * k] = static_cast<uint32_t>(q[k]);
-    s[2 * k + 1] = static_cast<uint32_t>(q[k] >> 32);
-  }
-}
-
-__device__ __forceinline__ Xoshiro words_to_state(const uint32_t (&s)[8]) {
-  Xoshiro r;
-  r.s0 = s[0] | static_cast<uint64_t>(s[1]) << 32;
-  r.s1 = s[2] | static_cast<uint64_t>(s[3]) << 32;
-  r.s2 = s[4] | static_cast<uint64_t>(s[5]) << 32;
-  r.s3 = s[6] | static_cast<uint64_t>(s[7]) << 32;
-  return r;
-}
-
 // The gate probability of a fed bank (feedback.cpp:24-28; regression:
 // regression.cpp:46-48, 145-151) and, for regression, whether the step is Type I.
 __device__ __forceinline__ double bank_gate(const TrainParams& P, int v0, int y, int target, bool& regress_type1) {

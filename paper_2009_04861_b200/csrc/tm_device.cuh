@@ -95,6 +95,94 @@ struct Xoshiro {
   }
 };
 
+// ---- xoshiro256 jump-ahead on the GPU: the state update of rng.hpp next()
+// is linear over GF(2), so k steps are one 256 x 256 bit matrix (built on the
+// host, engine.cu seq_jump_rows). A warp applies it cooperatively: lane L
+// computes output bits 8L .. 8L+7 (row r of that byte: parity(row & s)),
+// the 32 bytes are gathered with one OR-reduction per 32-bit word. The
+// matrix lives in shared memory as [r][w][L] (row 8L + r, word w), so for a
+// fixed (r, w) the 32 lanes read 32 consecutive words (no bank conflicts).
+__device__ __forceinline__ void gf2_apply(const uint32_t* mt, uint32_t (&s)[8], int lane) {
+  uint32_t byte = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) acc ^= mt[(r * 8 + w) * 32 + lane] & s[w];
+    byte |= (static_cast<uint32_t>(__popc(acc)) & 1u) << r;
+  }
+  const uint32_t mine = byte << (8 * (lane & 3));
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s[w] = __reduce_or_sync(kFull, (lane >> 2) == w ? mine : 0u);
+}
+
+__device__ __forceinline__ void state_to_words(const Xoshiro& r, uint32_t (&s)[8]) {
+  const uint64_t q[4] = {r.s0, r.s1, r.s2, r.s3};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    s[2 * k] = static_cast<uint32_t>(q[k]);
+    s[2 * k + 1] = static_cast<uint32_t>(q[k] >> 32);
+  }
+}
+
+__device__ __forceinline__ Xoshiro words_to_state(const uint32_t (&s)[8]) {
+  Xoshiro r;
+  r.s0 = s[0] | static_cast<uint64_t>(s[1]) << 32;
+  r.s1 = s[2] | static_cast<uint64_t>(s[3]) << 32;
+  r.s2 = s[4] | static_cast<uint64_t>(s[5]) << 32;
+  r.s3 = s[6] | static_cast<uint64_t>(s[7]) << 32;
+  return r;
+}
+
+
+// Draws k .. k + 2o - 1 of a xoshiro stream (the 2o Type I draws of the
+// reference, feedback.cpp:45,63) as bit words in literal order: hbits bit k
+// = (u_k < p_high), lbits bit k = (u_k < p_low). Warp-cooperative: lane L
+// jumps to draw L * chunk (jc = M^chunk applied lane by lane) and draws its
+// segment; the stream then continues after the 2o draws (jl = M^(2o)).
+// hbits / lbits (at least ceil(2o/32) + 2 words) are zeroed here. rng is
+// lane 0's; every lane leaves with the advanced state.
+__device__ __forceinline__ void draw_type_i_bits(Xoshiro& rng, int L, int chunk, double p_high, double p_low,
+                                                 const uint32_t* jc, const uint32_t* jl, uint32_t* hbits,
+                                                 uint32_t* lbits, int refw, int lane) {
+  for (int k = lane; k < refw; k += 32) hbits[k] = lbits[k] = 0;
+  uint32_t sw[8], mine[8], start[8];
+  state_to_words(rng, sw);
+#pragma unroll
+  for (int w = 0; w < 8; ++w) start[w] = mine[w] = sw[w] = __shfl_sync(kFull, sw[w], 0);
+  for (int hop = 1; hop < 32; ++hop) {
+    if (hop * chunk >= L) break;  // warp-uniform
+    gf2_apply(jc, sw, lane);
+    if (lane == hop) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) mine[w] = sw[w];
+    }
+  }
+  __syncwarp();
+  Xoshiro rl = words_to_state(mine);
+  const int k0 = lane * chunk, k1 = min(L, k0 + chunk);
+  uint32_t hw = 0, lw = 0;
+  int cw = k0 >> 5;
+  for (int k = k0; k < k1; ++k) {
+    if ((k >> 5) != cw) {
+      if (hw) atomicOr(&hbits[cw], hw);
+      if (lw) atomicOr(&lbits[cw], lw);
+      hw = lw = 0;
+      cw = k >> 5;
+    }
+    const double u = rl.uniform();
+    hw |= (u < p_high ? 1u : 0u) << (k & 31);
+    lw |= (u < p_low ? 1u : 0u) << (k & 31);
+  }
+  if (k1 > k0) {
+    if (hw) atomicOr(&hbits[cw], hw);
+    if (lw) atomicOr(&lbits[cw], lw);
+  }
+  gf2_apply(jl, start, lane);  // the state after the 2o draws
+  rng = words_to_state(start);
+  __syncwarp();
+}
+
 // %laneid (one S2R when rematerialised, no mask).
 __device__ __forceinline__ uint32_t lane_id() {
   uint32_t l;

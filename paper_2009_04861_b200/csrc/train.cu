@@ -161,9 +161,16 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
   const int refw = (L + 31) / 32 + 2;  // + padding for funnel shifts
   uint32_t* hbits = smem;              // u < p_high, reference literal order
   uint32_t* lbits = smem + refw;       // u < p_low
+  uint32_t* jc = smem + 2 * refw;      // jump matrices (M.jump_chunk != null)
+  uint32_t* jl = jc + 2048;
   const int64_t q = P.q;
   const int T = P.margin;
   for (int k = lane; k < 2 * refw; k += 32) smem[k] = 0;
+  if (M.jump_chunk)
+    for (int k = lane; k < 2048; k += 32) {
+      jc[k] = M.jump_chunk[k];
+      jl[k] = M.jump_lits[k];
+    }
   __syncwarp();
 
   for (int jb = 0; jb < M.njobs; ++jb) {
@@ -225,20 +232,24 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
       if (type2) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
       } else {
-        if (lane == 0) {
-          uint32_t hw = 0, lw = 0;
-          for (int k = 0; k < L; ++k) {
-            const double u = rng.uniform();
-            hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
-            lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
-            if ((k & 31) == 31 || k == L - 1) {
-              hbits[k >> 5] = hw;
-              lbits[k >> 5] = lw;
-              hw = lw = 0;
+        if (M.jump_chunk) {
+          draw_type_i_bits(rng, L, M.chunk, M.p_high, M.p_low, jc, jl, hbits, lbits, refw, lane);
+        } else {
+          if (lane == 0) {
+            uint32_t hw = 0, lw = 0;
+            for (int k = 0; k < L; ++k) {
+              const double u = rng.uniform();
+              hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
+              lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
+              if ((k & 31) == 31 || k == L - 1) {
+                hbits[k >> 5] = hw;
+                lbits[k >> 5] = lw;
+                hw = lw = 0;
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
 #pragma unroll
         for (int p = 0; p < NW; ++p) {
           const int wi = p * 32 + lane;
@@ -291,10 +302,17 @@ __global__ void __launch_bounds__(32) train_mirror_wide_kernel(TrainParams P, Mi
   const int refw = (L + 31) / 32 + 2;
   uint32_t* hbits = smem;
   uint32_t* lbits = smem + refw;
+  uint32_t* jc = smem + 2 * refw;
+  uint32_t* jl = jc + 2048;
   const int64_t q = P.q;
   const int T = P.margin;
   const int Wp = P.Wp, words = P.Wp >> 5;
   for (int k = lane; k < 2 * refw; k += 32) smem[k] = 0;
+  if (M.jump_chunk)
+    for (int k = lane; k < 2048; k += 32) {
+      jc[k] = M.jump_chunk[k];
+      jl[k] = M.jump_lits[k];
+    }
   __syncwarp();
 
   for (int jb = 0; jb < M.njobs; ++jb) {
@@ -392,20 +410,24 @@ __global__ void __launch_bounds__(32) train_mirror_wide_kernel(TrainParams P, Mi
           if (__any_sync(kFull, moved != 0)) after = eval();
         }
       } else {
-        if (lane == 0) {
-          uint32_t hw = 0, lw = 0;
-          for (int k = 0; k < L; ++k) {
-            const double u = rng.uniform();
-            hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
-            lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
-            if ((k & 31) == 31 || k == L - 1) {
-              hbits[k >> 5] = hw;
-              lbits[k >> 5] = lw;
-              hw = lw = 0;
+        if (M.jump_chunk) {
+          draw_type_i_bits(rng, L, M.chunk, M.p_high, M.p_low, jc, jl, hbits, lbits, refw, lane);
+        } else {
+          if (lane == 0) {
+            uint32_t hw = 0, lw = 0;
+            for (int k = 0; k < L; ++k) {
+              const double u = rng.uniform();
+              hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
+              lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
+              if ((k & 31) == 31 || k == L - 1) {
+                hbits[k >> 5] = hw;
+                lbits[k >> 5] = lw;
+                hw = lw = 0;
+              }
             }
           }
+          __syncwarp();
         }
-        __syncwarp();
         for (int p = 0; p < words; ++p) {
           const int wi = p * 32 + lane;
           if (wi * 32 >= P.o) continue;
@@ -534,7 +556,7 @@ void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
 template <int NW, int B>
 void launch_mirror(const TrainParams& p, const MirrorParams& mp, cudaStream_t s) {
   const int refw = (2 * p.o + 31) / 32 + 2;
-  const size_t shm = sizeof(uint32_t) * 2 * refw;
+  const size_t shm = sizeof(uint32_t) * (2 * refw + (mp.jump_chunk ? 4096 : 0));
   if (shm > 48 * 1024)
     cudaFuncSetAttribute(train_mirror_kernel<NW, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(shm));
@@ -567,7 +589,7 @@ bool dispatch_mirror(const TrainParams& p, const MirrorParams& mp, int NW, cudaS
     case 16: launch_mirror<16, B>(p, mp, s); return true;
     default: {  // rows wider than 16 words per lane: planes in place
       const int refw = (2 * p.o + 31) / 32 + 2;
-      const size_t shm = sizeof(uint32_t) * 2 * refw;
+      const size_t shm = sizeof(uint32_t) * (2 * refw + (mp.jump_chunk ? 4096 : 0));
       if (shm > 227 * 1024) return false;
       if (shm > 48 * 1024)
         cudaFuncSetAttribute(train_mirror_wide_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -206,3 +206,23 @@ def test_sequential_parallel_replay_matches_serial(kind, q, n, monkeypatch):
         got[mode] = (np.stack([tm.banks[c].counters() for c in range(d.classes)]), ev)
     assert got["0"][1] == got["1"][1]
     assert np.array_equal(got["0"][0], got["1"][0])
+
+
+@pytest.mark.parametrize("kind,q,n", [("mnist", 40, 40), ("imdb", 6, 10)])
+def test_w1_replay_jump_draws_match_serial(kind, q, n, monkeypatch):
+    """train_epoch_parallel(workers=1)'s replay draws a Type I step's 2o
+    uniforms by warp-cooperative jump-ahead when 2o >= 256 (train.cu
+    draw_type_i_bits); it must leave exactly the automata, tallies and
+    events of the serial draws (TMG_SEQ_SERIAL=1)."""
+    from paper_2009_04861_b200 import synth
+    d = synth.make(kind, q, 4, 11)
+    got = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("TMG_SEQ_SERIAL", mode)
+        tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=10, specificity=4.0, seed=5), d.features, d.classes)
+        pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes)
+        ev = [T.train_epoch_parallel(tm, pool, 1, e, mode=T.MODE_SYNC_MIRROR).feedback_events for e in range(2)]
+        got[mode] = (np.stack([tm.banks[c].counters() for c in range(d.classes)]), pool.tallies(), ev)
+    assert got["0"][2] == got["1"][2]
+    assert np.array_equal(got["0"][0], got["1"][0])
+    assert np.array_equal(got["0"][1], got["1"][1])
