@@ -102,7 +102,7 @@ def test_scaling_shape(tmp_path):
     <= 0.5x the sequential one (on the GPU: far less). The criterion's lower
     bound (x1.6, the CPU trainer's linear cost) is not asserted: the GPU
     replay of the sequential trainer applies the gated clauses of an example
-    in parallel, so it grows sub-linearly (x1.59 / 1.67 / 2.06 measured; the
+    in parallel, so it grows sub-linearly (x1.44 / 1.64 / 1.89 measured; the
     serial replay, TMG_SEQ_SERIAL=1: x1.68 / 1.68 / 2.15)."""
     x, y, _, _ = _synth(tmp_path, "patterns", 1000, 10, 7, classes=4, zone=5)
 
