@@ -191,7 +191,122 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
     unsigned long long events = 0;
 
     const bool forced = job.forced != 0;
-    for (int64_t t = 0; t < job.batch; ++t) {
+    // Type I feedback of one step (feedback.cpp:32-70) with the 2o draws of
+    // the stream in literal order.
+    auto type_i = [&](const uint32_t (&x)[NW], const uint32_t (&n)[NW], int before) {
+      if (M.jump_chunk) {
+        draw_type_i_bits(rng, L, M.chunk, M.p_high, M.p_low, jc, jl, hbits, lbits, refw, lane);
+      } else {
+        if (lane == 0) {
+          uint32_t hw = 0, lw = 0;
+          for (int k = 0; k < L; ++k) {
+            const double u = rng.uniform();
+            hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
+            lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
+            if ((k & 31) == 31 || k == L - 1) {
+              hbits[k >> 5] = hw;
+              lbits[k >> 5] = lw;
+              hw = lw = 0;
+            }
+          }
+        }
+        __syncwarp();
+      }
+#pragma unroll
+      for (int p = 0; p < NW; ++p) {
+        const int wi = p * 32 + lane;
+        if (wi * 32 >= P.o) continue;
+        // part 0: literal k = 32*wi + b; part 1: literal k = o + 32*wi + b.
+        const int k1 = P.o + wi * 32;
+        const uint32_t h0 = hbits[wi], l0 = lbits[wi];
+        const uint32_t h1 = __funnelshift_r(hbits[k1 >> 5], hbits[(k1 >> 5) + 1], k1 & 31);
+        const uint32_t l1 = __funnelshift_r(lbits[k1 >> 5], lbits[(k1 >> 5) + 1], k1 & 31);
+        if (before) {
+          // c=1: lit=1 uses the p_high draw, lit=0 the p_low draw.
+          cl.type_i_word(0, p, x[p], 1, P.boost, (x[p] & h0) | (~x[p] & l0), P.lo, P.hi);
+          cl.type_i_word(1, p, n[p], 1, P.boost, (n[p] & h1) | (~n[p] & l1), P.lo, P.hi);
+        } else {
+          cl.type_i_word(0, p, x[p], 0, P.boost, l0, P.lo, P.hi);
+          cl.type_i_word(1, p, n[p], 0, P.boost, l1, P.lo, P.hi);
+        }
+      }
+      __syncwarp();
+    };
+    if (!forced) {
+      // Windows of 32 steps: the gate inputs (order, label, tally ->
+      // probability and feedback type) and the previous-output bit of each
+      // step's example are loaded by its own lane up front, and the new
+      // outputs are published at the window end. Exact for the replay: a
+      // pass visits each example once, so no step reads a tally or an output
+      // bit an earlier step of the same pass writes. Only the stream is
+      // serial: lane 0 draws each gate (trainer.cpp:121) and, on Type I, the
+      // 2o draws.
+      for (int64_t t0 = 0; t0 < job.batch; t0 += 32) {
+        const int64_t t = t0 + lane;
+        const int steps = static_cast<int>(job.batch - t0 < 32 ? job.batch - t0 : 32);
+        int64_t i = 0;
+        int target = 0;
+        double p = 0.0;
+        uint32_t prevbit = 0;
+        if (lane < steps) {
+          const int64_t pos = (job.offset + t) % q;
+          i = P.order ? P.order[pos] : pos;
+          const int v0 = __ldcg(P.tallies + i * P.m + c);
+          const int label = P.labels[i];
+          if (P.regress) {  // gate_probability, regression.cpp:46-48
+            const int v = v0 < 0 ? 0 : (v0 > T ? T : v0);
+            const int e = label > v ? label - v : v - label;
+            p = fmin(1.0, static_cast<double>(e) / (2.0 * static_cast<double>(T)));
+            target = v < label ? 1 : 0;
+          } else {  // clause_update_probability, feedback.cpp:24-28
+            const int y = label == c ? 1 : 0;
+            const int v = v0 < -T ? -T : (v0 > T ? T : v0);
+            const int e = y ? T - v : T + v;
+            p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
+            target = (y == 1) == positive ? 1 : 0;
+          }
+          prevbit = (__ldcg(prev_row + (i >> 5)) >> (i & 31)) & 1u;
+        }
+        unsigned gm = 0, outs = 0;
+        for (int sidx = 0; sidx < steps; ++sidx) {
+          const double ps = __shfl_sync(kFull, p, sidx);
+          int gated = 0;
+          if (lane == 0) gated = rng.uniform() < ps ? 1 : 0;  // skip iff u >= p (trainer.cpp:121)
+          gated = __shfl_sync(kFull, gated, 0);
+          if (!gated) continue;
+          ++events;
+          gm |= 1u << sidx;
+          const int64_t is = __shfl_sync(kFull, i, sidx);
+          const int ts = __shfl_sync(kFull, target, sidx);
+          uint32_t x[NW], n[NW];
+#pragma unroll
+          for (int pw = 0; pw < NW; ++pw) {
+            x[pw] = P.xplane[is * 2 * P.Wp + pw * 32 + lane];
+            n[pw] = P.nplane[is * 2 * P.Wp + pw * 32 + lane];
+          }
+          const int before = cl.eval_train(x, n);
+          int after = before;
+          if (ts == 0) {
+            if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
+          } else {
+            type_i(x, n, before);
+            after = cl.eval_train(x, n);
+          }
+          outs |= static_cast<unsigned>(after) << sidx;
+        }
+        if ((gm >> lane) & 1u) {  // record_output_and_tally (pool.cpp:93-106)
+          const uint32_t now = (outs >> lane) & 1u;
+          if (now != prevbit) {
+            red_xor_gpu(prev_row + (i >> 5), 1u << (i & 31));
+            int delta = now ? 1 : -1;
+            if (!positive) delta = -delta;
+            publish_tally(P, static_cast<size_t>(i) * P.m + c, delta);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    for (int64_t t = 0; forced && t < job.batch; ++t) {
       int64_t i = 0;
       int target = 0, gated = 1;  // target: 1 = Type I step, 0 = Type II
       if (lane == 0 && !forced) {
@@ -232,43 +347,7 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
       if (type2) {
         if (before && cl.type_ii(x, n)) after = cl.eval_train(x, n);
       } else {
-        if (M.jump_chunk) {
-          draw_type_i_bits(rng, L, M.chunk, M.p_high, M.p_low, jc, jl, hbits, lbits, refw, lane);
-        } else {
-          if (lane == 0) {
-            uint32_t hw = 0, lw = 0;
-            for (int k = 0; k < L; ++k) {
-              const double u = rng.uniform();
-              hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
-              lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
-              if ((k & 31) == 31 || k == L - 1) {
-                hbits[k >> 5] = hw;
-                lbits[k >> 5] = lw;
-                hw = lw = 0;
-              }
-            }
-          }
-          __syncwarp();
-        }
-#pragma unroll
-        for (int p = 0; p < NW; ++p) {
-          const int wi = p * 32 + lane;
-          if (wi * 32 >= P.o) continue;
-          // part 0: literal k = 32*wi + b; part 1: literal k = o + 32*wi + b.
-          const int k1 = P.o + wi * 32;
-          const uint32_t h0 = hbits[wi], l0 = lbits[wi];
-          const uint32_t h1 = __funnelshift_r(hbits[k1 >> 5], hbits[(k1 >> 5) + 1], k1 & 31);
-          const uint32_t l1 = __funnelshift_r(lbits[k1 >> 5], lbits[(k1 >> 5) + 1], k1 & 31);
-          if (before) {
-            // c=1: lit=1 uses the p_high draw, lit=0 the p_low draw.
-            cl.type_i_word(0, p, x[p], 1, P.boost, (x[p] & h0) | (~x[p] & l0), P.lo, P.hi);
-            cl.type_i_word(1, p, n[p], 1, P.boost, (n[p] & h1) | (~n[p] & l1), P.lo, P.hi);
-          } else {
-            cl.type_i_word(0, p, x[p], 0, P.boost, l0, P.lo, P.hi);
-            cl.type_i_word(1, p, n[p], 0, P.boost, l1, P.lo, P.hi);
-          }
-        }
-        __syncwarp();
+        type_i(x, n, before);
         after = cl.eval_train(x, n);
       }
       if (lane == 0 && !forced) {

@@ -13,6 +13,9 @@ for mode in ("0", "1"):
     tm = T.MultiClassTM(T.TMConfig(clauses=200, margin=50, specificity=10.0, seed=42), 784, 10)
     pool = T.ExamplePool(784, d.train_x, d.train_y, 10)
     t0 = time.perf_counter()
-    T.train_epoch_parallel(tm, pool, 1, 0, mode=T.MODE_SYNC_MIRROR)
+    rep = T.train_epoch_parallel(tm, pool, 1, 0, mode=T.MODE_SYNC_MIRROR)
     res[mode] = time.perf_counter() - t0
-print(json.dumps({"w1_mnist_q200_n200_jump_s": res["0"], "serial_s": res["1"], "speedup": res["1"] / res["0"]}))
+    res["dev" + mode] = rep.device_seconds
+    res["ev" + mode] = rep.total_feedback_events()
+print(json.dumps({"w1_mnist_q200_n200_jump_s": res["0"], "serial_s": res["1"], "speedup": res["1"] / res["0"],
+                  "device_s": [res["dev0"], res["dev1"]], "events": [res["ev0"], res["ev1"]]}))
