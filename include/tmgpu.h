@@ -118,6 +118,10 @@ int tmg_debug_counters(tmg_machine* tm, uint64_t* out, int32_t count, int32_t re
 int tmg_alias8_table(uint32_t threshold, uint32_t* out);
 /* Integer-pipe roofline probe: LOP3-only and LOP3+IMAD thread-ops per second. */
 int tmg_bench_int_peak(int32_t device, double* lop3_ops_per_s, double* mixed_ops_per_s);
+/* Host probe of the xoshiro256 jump-ahead used by the bit-exact replays
+ * (train_epoch_sequential, W = 1): state <- M^k state, M the GF(2) matrix of
+ * one state update of rng.hpp next(). Must equal k calls of next(). */
+int tmg_debug_xoshiro_jump(uint64_t* state, uint64_t k);
 
 /* Defaults of TMConfig (core.hpp:86-93). */
 void tmg_config_default(tmg_config* cfg);

@@ -49,6 +49,7 @@ SIGNATURES = {
     "tmg_kernel_launches": (C.c_ulonglong, []),
     "tmg_machine_stream": (C.c_int, [P, PP]),
     "tmg_bench_int_peak": (C.c_int, [I32, C.POINTER(D), C.POINTER(D)]),
+    "tmg_debug_xoshiro_jump": (C.c_int, [P, C.c_uint64]),
     "tmg_debug_feedback_rates": (C.c_int, [P, I32, I32, P, I32, C.c_uint32, P, P]),
     "tmg_debug_type_i_async": (C.c_int, [P, I32, I32, P, I32, C.c_uint32, I32]),
     "tmg_debug_counters": (C.c_int, [P, P, I32, I32]),

@@ -1015,6 +1015,22 @@ TMG_API int tmg_pool_reset_tallies(tmg_pool* pool) {
   });
 }
 
+// Host check of the jump-ahead matrices (sequential.cu / draw_type_i_bits):
+// state <- M^k state for the xoshiro256 state update.
+TMG_API int tmg_debug_xoshiro_jump(uint64_t* state, uint64_t k) {
+  return guarded([&] {
+    if (!state) fail(TMG_EINVAL, "null state");
+    const Gf2 m = gf2_pow(k);
+    uint64_t out[4] = {0, 0, 0, 0};
+    for (int i = 0; i < 256; ++i) {
+      uint64_t acc = 0;
+      for (int w = 0; w < 4; ++w) acc ^= m.r[i][w] & state[w];
+      if (__builtin_popcountll(acc) & 1) out[i >> 6] |= uint64_t(1) << (i & 63);
+    }
+    for (int w = 0; w < 4; ++w) state[w] = out[w];
+  });
+}
+
 TMG_API int tmg_pool_tally_ipc_handle(tmg_pool* pool, unsigned char* handle) {
   return guarded([&] {
     if (!pool || !handle) fail(TMG_EINVAL, "null argument");

@@ -159,3 +159,21 @@ def test_cli_host_part_matches_reference():
     tm = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "tm")
     assert os.path.exists(tm), "build first: make -C paper_2009_04861_b200/csrc"
     assert run(tm, "host") == _cli_golden("host")
+
+
+def test_xoshiro_jump_ahead_matches_stepping():
+    """The GF(2) jump matrices behind the bit-exact parallel replays
+    (engine.cu gf2_pow; applied on the GPU by sequential.cu / train.cu
+    draw_type_i_bits): M^k applied to a state equals k steps of rng.hpp
+    next() — for the chunk and 2o distances of the configs' shapes."""
+    import ctypes as C
+
+    import paper_2009_04861_b200 as T
+    from paper_2009_04861_b200._capi import check, lib
+    for k in (1, 2, 49, 147, 625, 1568, 4704, 20000):
+        r = T.Rng(2009, k)
+        jumped = r.state.copy()
+        check(lib().tmg_debug_xoshiro_jump(C.c_void_p(jumped.ctypes.data), k))
+        for _ in range(k):
+            r.next()
+        assert np.array_equal(jumped, r.state), k
