@@ -224,6 +224,9 @@ struct tmg_pool {
   uint32_t* xplane() const { return rows.ptr; }
   uint32_t* nplane() const { return rows.ptr + Wp; }
   DevBuf<int32_t> labels, tallies, delta, order;
+  // Feature-major example columns for evaluation (eval.cu), built on first
+  // use: the rows never change after creation.
+  mutable DevBuf<uint32_t> lit_t;
   std::vector<int32_t> host_labels;
   // Tally replicas of the other ranks (multi-GPU over peer memory): every
   // tally change is also added into each of them by the training kernels.
@@ -243,8 +246,10 @@ struct tmg_machine {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf<uint32_t> state, prev;
-  DevBuf<int32_t> inc_count, nentries, sums;
-  DevBuf<tmg::EvalEntry> entries;
+  DevBuf<int32_t> inc_count, lens, sums;
+  DevBuf<int64_t> offs;      // [clauses + 1] literal-list offsets
+  DevBuf<uint32_t> lists;    // included-literal lists (eval.cu)
+  DevBuf<uint32_t> lit_t;    // scratch: feature-major example columns of non-pool rows
   DevBuf<unsigned long long> events;
   DevBuf<unsigned long long> dbg;  // instrumentation counters (TMG_STATS builds)
   DevBuf<uint32_t> alias8;         // alias table of the clause-output-0 Type I draw
@@ -295,10 +300,19 @@ void bind(tmg_machine* tm, int64_t q) {  // core.cpp:117-126
   CK(cudaStreamSynchronize(tm->stream));
 }
 
+// Include counts and the per-clause included-literal lists of the current
+// state (rebuilt lazily after any state change).
 void rebuild_entries(tmg_machine* tm) {
   if (!tm->entries_dirty) return;
-  tmg::build_entries_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx, tm->entries.ptr,
-                            tm->nentries.ptr, tm->inc_count.ptr, tm->stream);
+  const int64_t total = tmg::build_lists_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx,
+                                                tm->inc_count.ptr, tm->lens.ptr, tm->offs.ptr, tm->stream);
+  if (total < 0) CK(cudaGetLastError());
+  if (tm->lists.count < static_cast<size_t>(total) + 8) {
+    // grow with headroom: lists get longer as clauses learn
+    tm->lists.alloc(static_cast<size_t>(total + total / 4) + 64);
+  }
+  tmg::fill_lists_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx, tm->o, tm->offs.ptr, tm->lists.ptr,
+                         tm->stream);
   CK(cudaGetLastError());
   tm->entries_dirty = false;
 }
@@ -347,8 +361,8 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     const size_t cl = static_cast<size_t>(tm->clauses());
     tm->state.alloc(cl * tm->B * 2 * tm->Wp);
     tm->inc_count.alloc(cl);
-    tm->nentries.alloc(cl);
-    tm->entries.alloc(cl * tm->Wx);
+    tm->lens.alloc(cl);
+    tm->offs.alloc(cl + 1);
     tm->events.alloc(2 * static_cast<size_t>(m));  // all events, then Type I events
     tm->dbg.alloc(tmg::kDebugCounters);
     CK(cudaMemsetAsync(tm->dbg.ptr, 0, tm->dbg.bytes(), tm->stream));
@@ -588,36 +602,56 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
   tm->entries_dirty = true;
 }
 
-std::vector<int32_t> class_sums_device(tmg_machine* tm, const uint32_t* xplane, const uint32_t* nplane,
-                                       int64_t q, bool train_mode, int32_t* d_out, uint32_t* prev) {
+// Class sums of q literal rows (x-plane words at xplane, row stride 2*Wp)
+// into d_out [q][m]; train mode writes previous-output bitmaps to prev when
+// given. lit_t: the rows' feature-major columns if already built (pools cache
+// theirs), else they are built into the machine's scratch.
+void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool train_mode, int32_t* d_out,
+                       uint32_t* prev, const uint32_t* lit_t = nullptr) {
   rebuild_entries(tm);
-  tmg::EvalParams e{};
-  e.entries = tm->entries.ptr;
-  e.nentries = tm->nentries.ptr;
+  const int64_t Gs = tmg::lit_t_stride(q);
+  if (!lit_t) {
+    const size_t need = static_cast<size_t>(tm->o + 1) * Gs;
+    if (tm->lit_t.count < need) tm->lit_t.alloc(need);
+    tmg::transpose_literals_launch(xplane, 2 * tm->Wp, q, tm->o, tm->lit_t.ptr, tm->stream);
+    lit_t = tm->lit_t.ptr;
+  }
+  tmg::BitsEvalParams e{};
+  e.lit_t = lit_t;
+  e.Gs = Gs;
+  e.lists = tm->lists.ptr;
+  e.offs = tm->offs.ptr;
   e.inc_count = tm->inc_count.ptr;
   e.prev = prev;
   e.n_loc = tm->n_loc;
   e.j_begin = tm->j_begin;
   e.m = tm->m;
-  e.Wx = tm->Wx;
-  e.Wp = tm->Wp;
   e.Wq = tm->Wq;
-  e.xplane = xplane;
-  e.nplane = nplane;
   e.q = q;
   e.sums = d_out;
   e.all_positive = tm->all_positive;
-  // Enough CTAs for several waves over 148 SMs (TMG_EVAL_WAVES resident
-  // grids of 8 CTAs per SM), so the last partial wave is a small tail.
-  const int64_t tiles = (q + 127) / 128;
-  int chunks = static_cast<int>(
-      std::max<int64_t>(1, (int64_t(148) * 8 * TMG_EVAL_WAVES + tiles * tm->m - 1) / (tiles * tm->m)));
-  chunks = std::min(chunks, std::max(1, tm->n_loc / 8));
-  e.chunk = (tm->n_loc + chunks - 1) / chunks;
+  // Enough CTAs for ~4 resident waves of 4 CTAs (32 warps) per SM; at most
+  // 2040 clauses per CTA (the bit-sliced counters' range), >= 4 per warp.
+  const int64_t blocks = (q + 1023) / 1024;
+  int64_t chunks = (int64_t(148) * 4 * 4 + blocks * tm->m - 1) / (blocks * tm->m);
+  chunks = std::max<int64_t>(chunks, (tm->n_loc + 2039) / 2040);
+  chunks = std::min<int64_t>(chunks, std::max(1, tm->n_loc / 32));
+  chunks = std::max<int64_t>(chunks, (tm->n_loc + 2039) / 2040);
+  chunks = std::min<int64_t>(chunks, 65535 / tm->m);
+  e.cta_clauses = static_cast<int32_t>((tm->n_loc + chunks - 1) / chunks);
+  e.chunks = static_cast<int32_t>((tm->n_loc + e.cta_clauses - 1) / e.cta_clauses);
   CK(cudaMemsetAsync(d_out, 0, static_cast<size_t>(q) * tm->m * 4, tm->stream));
-  tmg::eval_sums_launch(e, train_mode, tm->stream);
+  tmg::eval_bits_launch(e, train_mode, tm->stream);
   CK(cudaGetLastError());
-  return {};
+}
+
+const uint32_t* pool_lit_t(tmg_machine* tm, const tmg_pool* pool) {
+  if (!pool->lit_t.ptr) {
+    pool->lit_t.alloc(static_cast<size_t>(pool->o + 1) * tmg::lit_t_stride(pool->q));
+    tmg::transpose_literals_launch(pool->xplane(), 2 * pool->Wp, pool->q, pool->o, pool->lit_t.ptr, tm->stream);
+    CK(cudaGetLastError());
+  }
+  return pool->lit_t.ptr;
 }
 
 void ensure_sums(tmg_machine* tm, int64_t q) {
@@ -737,9 +771,11 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   tm->state.release();
   tm->prev.release();
   tm->inc_count.release();
-  tm->nentries.release();
+  tm->lens.release();
+  tm->offs.release();
+  tm->lit_t.release();
   tm->sums.release();
-  tm->entries.release();
+  tm->lists.release();
   tm->events.release();
   tm->dbg.release();
   tm->alias8.release();
@@ -765,8 +801,8 @@ TMG_API int tmg_machine_info_get(const tmg_machine* tm, tmg_machine_info* info) 
     info->words_per_lane = tm->NW;
     info->bound_examples = static_cast<int32_t>(tm->q_bound);
     info->device = tm->device;
-    info->device_bytes = tm->state.bytes() + tm->prev.bytes() + tm->inc_count.bytes() + tm->entries.bytes() +
-                         tm->nentries.bytes() + tm->sums.bytes();
+    info->device_bytes = tm->state.bytes() + tm->prev.bytes() + tm->inc_count.bytes() + tm->lists.bytes() +
+                         tm->lens.bytes() + tm->offs.bytes() + tm->lit_t.bytes() + tm->sums.bytes();
   });
 }
 
@@ -1594,7 +1630,7 @@ TMG_API int tmg_refresh_tallies(tmg_machine* tm, tmg_pool* pool) {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
     if (tm->q_bound != pool->q) bind(tm, pool->q);  // pool.cpp:113
-    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, true, pool->tallies.ptr, tm->prev.ptr);
+    class_sums_device(tm, pool->xplane(), pool->q, true, pool->tallies.ptr, tm->prev.ptr, pool_lit_t(tm, pool));
     CK(cudaStreamSynchronize(tm->stream));
   });
 }
@@ -1603,7 +1639,7 @@ TMG_API int tmg_class_sums_device(tmg_machine* tm, const tmg_pool* pool, int32_t
   return guarded([&] {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
-    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, mode == TMG_EVAL_TRAIN, d_sums, nullptr);
+    class_sums_device(tm, pool->xplane(), pool->q, mode == TMG_EVAL_TRAIN, d_sums, nullptr, pool_lit_t(tm, pool));
     CK(cudaStreamSynchronize(tm->stream));
   });
 }
@@ -1613,8 +1649,8 @@ TMG_API int tmg_class_sums(tmg_machine* tm, const tmg_pool* pool, int32_t mode, 
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
     ensure_sums(tm, pool->q);
-    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, mode == TMG_EVAL_TRAIN, tm->sums.ptr,
-                      nullptr);
+    class_sums_device(tm, pool->xplane(), pool->q, mode == TMG_EVAL_TRAIN, tm->sums.ptr, nullptr,
+                      pool_lit_t(tm, pool));
     CK(cudaMemcpyAsync(out, tm->sums.ptr, static_cast<size_t>(pool->q) * tm->m * 4, cudaMemcpyDeviceToHost,
                        tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
@@ -1627,7 +1663,7 @@ TMG_API int tmg_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
     DeviceGuard dg(tm->device);
     if (tm->n_loc != tm->n) fail(TMG_EINVAL, "predict on a clause shard: reduce class sums across shards first");
     ensure_sums(tm, pool->q + (pool->q + tm->m - 1) / tm->m + 1);
-    class_sums_device(tm, pool->xplane(), pool->nplane(), pool->q, false, tm->sums.ptr, nullptr);
+    class_sums_device(tm, pool->xplane(), pool->q, false, tm->sums.ptr, nullptr, pool_lit_t(tm, pool));
     int32_t* pred = tm->sums.ptr + static_cast<size_t>(pool->q) * tm->m;
     tmg::argmax_launch(tm->sums.ptr, pred, pool->q, tm->m, tm->stream);
     CK(cudaGetLastError());
@@ -1657,7 +1693,7 @@ TMG_API int tmg_class_sums_literals(tmg_machine* tm, const uint64_t* lits, int64
     DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
     literals_to_planes(tm, lits, q, xs);
     ensure_sums(tm, q);
-    class_sums_device(tm, xs.ptr, xs.ptr + tm->Wp, q, mode == TMG_EVAL_TRAIN, tm->sums.ptr, nullptr);
+    class_sums_device(tm, xs.ptr, q, mode == TMG_EVAL_TRAIN, tm->sums.ptr, nullptr);
     CK(cudaMemcpyAsync(out, tm->sums.ptr, static_cast<size_t>(q) * tm->m * 4, cudaMemcpyDeviceToHost, tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
   });
@@ -1672,7 +1708,7 @@ TMG_API int tmg_predict_literals(tmg_machine* tm, const uint64_t* lits, int64_t 
     DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
     literals_to_planes(tm, lits, q, xs);
     ensure_sums(tm, q + (q + tm->m - 1) / tm->m + 1);
-    class_sums_device(tm, xs.ptr, xs.ptr + tm->Wp, q, false, tm->sums.ptr, nullptr);
+    class_sums_device(tm, xs.ptr, q, false, tm->sums.ptr, nullptr);
     int32_t* pred = tm->sums.ptr + static_cast<size_t>(q) * tm->m;
     tmg::argmax_launch(tm->sums.ptr, pred, q, tm->m, tm->stream);
     CK(cudaGetLastError());
@@ -1689,11 +1725,12 @@ TMG_API int tmg_machine_create_regress(const tmg_config* cfg, int32_t o, int32_t
 }
 
 namespace {
-void regress_predict_planes(tmg_machine* tm, const uint32_t* xs, const uint32_t* ns, int64_t q, int32_t* out) {
+void regress_predict_planes(tmg_machine* tm, const uint32_t* xs, int64_t q, int32_t* out,
+                            const uint32_t* lit_t = nullptr) {
   if (!tm->all_positive) fail(TMG_EINVAL, "not a regression machine");
   if (tm->n_loc != tm->n) fail(TMG_EINVAL, "predict on a clause shard: reduce clause counts across shards first");
   ensure_sums(tm, 2 * q);
-  class_sums_device(tm, xs, ns, q, false, tm->sums.ptr, nullptr);
+  class_sums_device(tm, xs, q, false, tm->sums.ptr, nullptr, lit_t);
   tmg::clamp_launch(tm->sums.ptr, tm->sums.ptr + q, q, tm->cfg.margin, tm->stream);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, tm->sums.ptr + q, static_cast<size_t>(q) * 4, cudaMemcpyDeviceToHost, tm->stream));
@@ -1706,7 +1743,7 @@ TMG_API int tmg_regress_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* 
   return guarded([&] {
     if (!M(tm) || !pool || tm->o != pool->o) fail(TMG_EINVAL, "head/pool feature count mismatch");
     DeviceGuard dg(tm->device);
-    regress_predict_planes(tm, pool->xplane(), pool->nplane(), pool->q, out);
+    regress_predict_planes(tm, pool->xplane(), pool->q, out, pool_lit_t(tm, pool));
   });
 }
 
@@ -1717,7 +1754,7 @@ TMG_API int tmg_regress_predict_literals(tmg_machine* tm, const uint64_t* lits, 
     DeviceGuard dg(tm->device);
     DevBuf<uint32_t> xs;  // literal rows [q][2][Wp]
     literals_to_planes(tm, lits, q, xs);
-    regress_predict_planes(tm, xs.ptr, xs.ptr + tm->Wp, q, out);
+    regress_predict_planes(tm, xs.ptr, q, out);
   });
 }
 

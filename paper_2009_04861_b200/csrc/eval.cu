@@ -6,142 +6,219 @@
 // variant with previous-output bitmaps replaces refresh_tallies
 // (proj/src/pool.cpp:108-124).
 //
-// Trained clauses are very sparse (tens of included literals out of 2o), so
-// each clause is first compacted to the list of its nonzero include words
-// (build_entries). A CTA owns a tile of 128 examples staged in shared memory
-// word-major (conflict-free: lane = example) and a chunk of clauses of one
-// class; every thread evaluates its example against each clause's word list
-// (a warp-uniform loop over broadcast loads) with a warp-wide early exit.
+// Example-sliced evaluation. A clause is a conjunction of its included
+// literals, so for 32 examples at once its output word is the AND of the
+// included literals' 32-example bit columns. The examples are therefore
+// transposed once per call into feature-major bit columns (lit_t: row f =
+// bit e of word g is x_f of example 32g+e, plus one all-ones row), and each
+// clause is compacted to the list of its included literals (feature index,
+// negation flag). A warp takes one clause at a time over 1024 examples:
+// per included literal ONE coalesced 128-byte load and ONE LOP3
+// (acc &= col ^ neg) cover 1024 (clause, example) pairs, with a warp-wide
+// exit once every example is falsified. Clause outputs are summed per
+// example in bit-sliced signed counters (one carry/borrow chain per clause
+// word), reduced across the CTA's warps with bit-sliced adders in shared
+// memory and turned into integers once per CTA.
 #include <algorithm>
 
 #include "kernels.h"
 #include "tm_device.cuh"
 
-#ifndef TMG_EVAL_STAGE
-#define TMG_EVAL_STAGE 4  // (r1au: 4 -> 1.22 ms, 32 -> 1.48, unstaged 1.33) clauses whose include lists a CTA stages in shared memory at a time
-#endif
-
 namespace tmg {
 
 namespace {
 
-// Examples per CTA in eval_sums: 128 (one thread each), or 32 for very wide
-// rows (IMDb) so the staged tile fits in shared memory. Rows are padded to
-// TILE+1 words: conflict-free staging and reads.
+constexpr int kEvalWarps = 8;   // warps per eval CTA (same example block, disjoint clause ranges)
+constexpr int kSumPlanes = 12;  // bit-sliced two's-complement counters: |sum| <= 2040 per CTA
 
-// One warp per clause: list its nonzero include words and count includes.
-__global__ void build_entries_kernel(const uint32_t* __restrict__ state, int clauses, int B, int Wp,
-                                     int Wx, EvalEntry* __restrict__ entries,
-                                     int32_t* __restrict__ nentries, int32_t* __restrict__ inc_count) {
+// One warp per clause: count the included literals (top plane) -> inc_count
+// and the list length padded to a multiple of 8 (lens).
+__global__ void count_literals_kernel(const uint32_t* __restrict__ state, int clauses, int B, int Wp, int Wx,
+                                      int32_t* __restrict__ inc_count, int32_t* __restrict__ lens) {
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= clauses) return;
   const uint32_t* top = state + (static_cast<size_t>(lc) * B + (B - 1)) * 2 * Wp;
-  EvalEntry* out = entries + static_cast<size_t>(lc) * Wx;
-  int base = 0, cnt = 0;
-  for (int w0 = 0; w0 < Wx; w0 += 32) {
-    const int w = w0 + lane;
-    uint32_t ix = 0, in = 0;
-    if (w < Wx) {
-      ix = top[w];
-      in = top[Wp + w];
-    }
-    cnt += __popc(ix) + __popc(in);
-    const bool nz = (ix | in) != 0;
-    const unsigned bal = __ballot_sync(kFull, nz);
-    if (nz) out[base + __popc(bal & ((1u << lane) - 1u))] = EvalEntry{static_cast<uint32_t>(w), ix, in, 0u};
-    base += __popc(bal);
-  }
+  int cnt = 0;
+  for (int w = lane; w < Wx; w += 32) cnt += __popc(top[w]) + __popc(top[Wp + w]);
 #pragma unroll
   for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
   if (lane == 0) {
-    nentries[lc] = base;
     inc_count[lc] = cnt;
+    lens[lc] = (cnt + 7) & ~7;
   }
 }
 
-template <bool TRAIN, int kTile>
-__global__ void __launch_bounds__(kTile) eval_sums_kernel(EvalParams P) {
-  constexpr int kTS = kTile + 1;
-  extern __shared__ uint32_t tile[];  // [2][Wx][kTS], then P.stage staged clauses' entries
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * kTile;
-  const int64_t i = i0 + tid;
-  const bool live = i < P.q;
-  // Stage the literal planes of the example tile, transposed to word-major.
-  for (int idx = tid; idx < P.Wx * kTile; idx += kTile) {
-    const int e = idx / P.Wx, w = idx % P.Wx;
-    const int64_t ie = i0 + e;
-    uint32_t xv = 0, nv = 0;
-    if (ie < P.q) {
-      xv = __ldg(P.xplane + ie * 2 * P.Wp + w);
-      nv = __ldg(P.nplane + ie * 2 * P.Wp + w);
+// Exclusive prefix sum of lens -> offs (one CTA; clause counts are small).
+// offs[clauses] = total.
+__global__ void __launch_bounds__(1024) scan_lengths_kernel(const int32_t* __restrict__ lens, int clauses,
+                                                            int64_t* __restrict__ offs) {
+  __shared__ int64_t part[1024];
+  const int t = threadIdx.x;
+  const int per = (clauses + 1023) / 1024;
+  const int a = min(clauses, t * per), b = min(clauses, a + per);
+  int64_t s = 0;
+  for (int k = a; k < b; ++k) s += lens[k];
+  part[t] = s;
+  __syncthreads();
+  for (int d = 1; d < 1024; d <<= 1) {  // Hillis-Steele inclusive scan
+    const int64_t v = t >= d ? part[t - d] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  int64_t run = part[t] - s;
+  for (int k = a; k < b; ++k) {
+    offs[k] = run;
+    run += lens[k];
+  }
+  if (t == 1023) offs[clauses] = part[1023];
+}
+
+// One warp per clause: write its included literals as (f << 1 | negated),
+// padded to the list length with (o << 1), the all-ones row of lit_t.
+__global__ void fill_literals_kernel(const uint32_t* __restrict__ state, int clauses, int B, int Wp, int Wx,
+                                     int o, const int64_t* __restrict__ offs, uint32_t* __restrict__ lists) {
+  const int lane = threadIdx.x & 31;
+  const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (lc >= clauses) return;
+  const uint32_t* top = state + (static_cast<size_t>(lc) * B + (B - 1)) * 2 * Wp;
+  uint32_t* out = lists + offs[lc];
+  const int len = static_cast<int>(offs[lc + 1] - offs[lc]);
+  int base = 0;
+  for (int part = 0; part < 2; ++part) {
+    for (int w0 = 0; w0 < Wx; w0 += 32) {
+      const int w = w0 + lane;
+      uint32_t bits = w < Wx ? top[part * Wp + w] : 0u;
+      const int cnt = __popc(bits);
+      int incl = cnt;  // inclusive warp scan of the counts
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int v = __shfl_up_sync(kFull, incl, d);
+        if (lane >= d) incl += v;
+      }
+      int pos = base + incl - cnt;
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        out[pos++] = (static_cast<uint32_t>(w * 32 + b) << 1) | static_cast<uint32_t>(part);
+      }
+      base += __shfl_sync(kFull, incl, 31);
     }
-    tile[w * kTS + e] = xv;
-    tile[(P.Wx + w) * kTS + e] = nv;
+  }
+  for (int k = base + lane; k < len; k += 32) out[k] = static_cast<uint32_t>(o) << 1;
+}
+
+// Literal rows [q][2][Wp] (x-plane words first) -> feature-major bit columns
+// lit_t[f][Gs]: bit e of word g = x_f of example 32g + e (0 beyond q). One
+// CTA: one row word w (32 features) x 32 column words (1024 examples); each
+// warp transposes 32 x 32 bit blocks with ballots, rows leave coalesced.
+__global__ void __launch_bounds__(256) transpose_literals_kernel(const uint32_t* __restrict__ xplane,
+                                                                 int64_t row_stride, int64_t q, int o,
+                                                                 int64_t Gs, uint32_t* __restrict__ lit_t) {
+  __shared__ uint32_t tile[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = blockIdx.y;
+  const int64_t g0 = static_cast<int64_t>(blockIdx.x) * 32;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int gl = warp * 4 + r;
+    const int64_t i = (g0 + gl) * 32 + lane;
+    const uint32_t v = i < q ? __ldg(xplane + i * row_stride + w) : 0u;
+    uint32_t mine = 0;
+#pragma unroll
+    for (int b = 0; b < 32; ++b) {
+      const uint32_t col = __ballot_sync(kFull, (v >> b) & 1u);
+      if (lane == b) mine = col;
+    }
+    tile[lane][gl] = mine;  // feature 32w + lane, column word g0 + gl
   }
   __syncthreads();
+  for (int fl = warp; fl < 32; fl += kEvalWarps) {
+    const int f = w * 32 + fl;
+    if (f < o) lit_t[static_cast<int64_t>(f) * Gs + g0 + lane] = tile[fl][lane];
+  }
+}
 
-  const int chunks = (P.n_loc + P.chunk - 1) / P.chunk;
-  const int c = blockIdx.y / chunks;
-  const int jl0 = (blockIdx.y % chunks) * P.chunk;
-  const int jl1 = min(jl0 + P.chunk, P.n_loc);
-  // Clause include-word lists are staged P.stage clauses at a time (every
-  // warp copies whole lists, coalesced), so the evaluation loop reads them
-  // from shared memory instead of a dependent global load per clause.
-  uint4* sent = reinterpret_cast<uint4*>(tile + ((2 * P.Wx * kTS + 3) & ~3));
-  int* sne = reinterpret_cast<int*>(sent + static_cast<size_t>(P.stage) * P.Wx);
-  const int warp = tid >> 5, nwarps = kTile >> 5;
-  int sum = 0;
-  for (int jb = jl0; jb < jl1; jb += P.stage) {
-    const int nb = min(P.stage, jl1 - jb);
-    __syncthreads();  // the previous block's lists are consumed
-    for (int cs = warp; cs < nb; cs += nwarps) {
-      const int lc = c * P.n_loc + jb + cs;
-      const int ne = __ldg(P.nentries + lc);
-      const uint4* src = reinterpret_cast<const uint4*>(P.entries + static_cast<size_t>(lc) * P.Wx);
-      for (int k = lane; k < ne; k += 32) {
-        uint4 en = __ldg(src + k);
-        en.w = (P.Wx + en.x) * kTS;  // !x-plane row of word w in the tile
-        en.x *= kTS;                 // x-plane row
-        sent[cs * P.Wx + k] = en;
+// counter += x (ADD) or -= x, bit-sliced two's complement, per bit lane.
+template <bool ADD>
+__device__ __forceinline__ void count_word(uint32_t (&P)[kSumPlanes], uint32_t x) {
+#pragma unroll
+  for (int b = 0; b < kSumPlanes; ++b) {
+    if (x == 0u) break;
+    const uint32_t p = P[b];
+    P[b] = p ^ x;
+    x = ADD ? (p & x) : (~p & x);
+  }
+}
+
+template <bool TRAIN>
+__global__ void __launch_bounds__(kEvalWarps * 32) eval_bits_kernel(BitsEvalParams P) {
+  __shared__ uint32_t red[kEvalWarps][kSumPlanes][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * 32 + lane;  // this lane's column word
+  const int64_t e0 = gw * 32;
+  const uint32_t valid = e0 >= P.q ? 0u : (P.q - e0 >= 32 ? kFull : ((1u << (P.q - e0)) - 1u));
+  const int c = blockIdx.y / P.chunks;
+  const int jc0 = (blockIdx.y % P.chunks) * P.cta_clauses;
+  const int jc1 = min(jc0 + P.cta_clauses, P.n_loc);
+  const int per = (P.cta_clauses + kEvalWarps - 1) / kEvalWarps;
+  const int ja = min(jc1, jc0 + warp * per), jb = min(jc1, ja + per);
+  const uint32_t* __restrict__ col = P.lit_t + gw;
+  uint32_t cnt[kSumPlanes];
+#pragma unroll
+  for (int b = 0; b < kSumPlanes; ++b) cnt[b] = 0u;
+  for (int jl = ja; jl < jb; ++jl) {
+    const int lc = c * P.n_loc + jl;
+    const int inc = __ldg(P.inc_count + lc);
+    if (!TRAIN && inc == 0) continue;  // empty clause: Predict 0 (core.hpp:211-213)
+    const int64_t off = __ldg(P.offs + lc);
+    const int len = static_cast<int>(__ldg(P.offs + lc + 1) - off);
+    const uint4* lst = reinterpret_cast<const uint4*>(P.lists + off);
+    uint32_t acc = valid;  // empty clause: Train 1
+    for (int k = 0; k < len; k += 8) {
+      const uint4 a = __ldg(lst + (k >> 2)), b = __ldg(lst + (k >> 2) + 1);
+      const uint32_t e[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(col + static_cast<int64_t>(e[u] >> 1) * P.Gs);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc &= v[u] ^ (0u - (e[u] & 1u));
+      if (!__any_sync(kFull, acc != 0u)) break;
+    }
+    if (TRAIN && P.prev != nullptr && gw < P.Wq) P.prev[static_cast<size_t>(lc) * P.Wq + gw] = acc;
+    const int j = P.j_begin + jl;
+    if (P.all_positive || !(j & 1)) count_word<true>(cnt, acc);
+    else count_word<false>(cnt, acc);
+  }
+  // CTA reduction of the warps' counters: bit-sliced ripple adds in shared memory.
+#pragma unroll
+  for (int b = 0; b < kSumPlanes; ++b) red[warp][b][lane] = cnt[b];
+  __syncthreads();
+  for (int half = kEvalWarps / 2; half >= 1; half >>= 1) {
+    if (warp < half) {
+      uint32_t carry = 0u;
+#pragma unroll
+      for (int b = 0; b < kSumPlanes; ++b) {
+        const uint32_t x = red[warp][b][lane], y = red[warp + half][b][lane];
+        red[warp][b][lane] = x ^ y ^ carry;
+        carry = (x & y) | (carry & (x ^ y));
       }
-      if (lane == 0) sne[cs] = ne;
     }
     __syncthreads();
-    for (int cs = 0; cs < nb; ++cs) {
-      const int jl = jb + cs;
-      const int lc = c * P.n_loc + jl;
-      const int ne = sne[cs];
-      int out;
-      if (ne == 0) {
-        out = TRAIN ? 1 : 0;  // empty-clause convention (core.hpp:211-213)
-      } else {
-        const uint4* en = sent + cs * P.Wx;
-        const uint32_t* xt = tile + tid;  // this example's column of the tile
-        uint32_t viol = 0;
-        for (int k = 0; k < ne; k += 4) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (k + u < ne) {
-              const uint4 ent = en[k + u];
-              viol |= (ent.y & ~xt[ent.x]) | (ent.z & ~xt[ent.w]);
-            }
-          }
-          if (__all_sync(kFull, viol != 0 || !live)) break;
-        }
-        out = viol == 0 ? 1 : 0;
-      }
-      const int j = P.j_begin + jl;
-      sum += (!P.all_positive && (j & 1)) ? -out : out;
-      if (TRAIN && P.prev != nullptr) {  // refresh_tallies also rewrites previous outputs
-        const unsigned bits = __ballot_sync(kFull, live && out);
-        if (lane == 0 && i < P.q) P.prev[static_cast<size_t>(lc) * P.Wq + (i >> 5)] = bits;
-      }
-    }
   }
-  if (live) atomicAdd(P.sums + i * P.m + c, sum);
+  // Per example: the K-bit two's-complement sum -> atomicAdd into sums[i][c].
+  const int64_t ib = static_cast<int64_t>(blockIdx.x) * 1024;
+  for (int x = threadIdx.x; x < 1024; x += kEvalWarps * 32) {
+    const int64_t i = ib + x;
+    if (i >= P.q) break;
+    const int wd = x >> 5, bit = x & 31;
+    int v = 0;
+#pragma unroll
+    for (int b = 0; b < kSumPlanes; ++b) v |= static_cast<int>((red[0][b][wd] >> bit) & 1u) << b;
+    v = (v ^ (1 << (kSumPlanes - 1))) - (1 << (kSumPlanes - 1));
+    if (v != 0) atomicAdd(P.sums + i * P.m + c, v);
+  }
 }
 
 __global__ void counters_to_planes_kernel(const uint16_t* __restrict__ counters,
@@ -302,89 +379,50 @@ __global__ void init_state_kernel(uint32_t* __restrict__ state, int64_t words, i
   state[idx] = b < B - 1 ? kFull : 0u;
 }
 
-// Rows too wide for even a 32-example staged tile (beyond ~26k features):
-// each thread reads its example's literal words straight from HBM/L2 at the
-// clause's include-list positions, and the lists are read from global memory.
-template <bool TRAIN>
-__global__ void __launch_bounds__(128) eval_sums_direct_kernel(EvalParams P) {
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * 128 + tid;
-  const bool live = i < P.q;
-  const uint32_t* xr = P.xplane + (live ? i : 0) * 2 * P.Wp;
-  const int chunks = (P.n_loc + P.chunk - 1) / P.chunk;
-  const int c = blockIdx.y / chunks;
-  const int jl0 = (blockIdx.y % chunks) * P.chunk;
-  const int jl1 = min(jl0 + P.chunk, P.n_loc);
-  int sum = 0;
-  for (int jl = jl0; jl < jl1; ++jl) {
-    const int lc = c * P.n_loc + jl;
-    const int ne = __ldg(P.nentries + lc);
-    int out;
-    if (ne == 0) {
-      out = TRAIN ? 1 : 0;  // empty-clause convention (core.hpp:211-213)
-    } else {
-      const uint4* en = reinterpret_cast<const uint4*>(P.entries + static_cast<size_t>(lc) * P.Wx);
-      uint32_t viol = 0;
-      for (int k = 0; k < ne; ++k) {
-        const uint4 ent = __ldg(en + k);
-        viol |= (ent.y & ~__ldg(xr + ent.x)) | (ent.z & ~__ldg(xr + P.Wp + ent.x));
-        if (__all_sync(kFull, viol != 0 || !live)) break;
-      }
-      out = viol == 0 ? 1 : 0;
-    }
-    const int j = P.j_begin + jl;
-    sum += (!P.all_positive && (j & 1)) ? -out : out;
-    if (TRAIN && P.prev != nullptr) {
-      const unsigned bits = __ballot_sync(kFull, live && out);
-      if (lane == 0 && i < P.q) P.prev[static_cast<size_t>(lc) * P.Wq + (i >> 5)] = bits;
-    }
-  }
-  if (live) atomicAdd(P.sums + i * P.m + c, sum);
-}
-
 inline unsigned blocks_for(int64_t n, int per) { return static_cast<unsigned>((n + per - 1) / per); }
 
 }  // namespace
 
-void build_entries_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, EvalEntry* e,
-                          int32_t* ne, int32_t* inc_count, cudaStream_t s) {
-  if (clauses <= 0) return;
+int64_t build_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int32_t* inc_count,
+                           int32_t* lens, int64_t* offs, cudaStream_t s) {
+  if (clauses <= 0) return 0;
   count_launch();
-  build_entries_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, e, ne, inc_count);
+  count_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, inc_count, lens);
+  count_launch();
+  scan_lengths_kernel<<<1, 1024, 0, s>>>(lens, clauses, offs);
+  int64_t total = 0;
+  if (cudaMemcpyAsync(&total, offs + clauses, sizeof total, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return -1;
+  return total;
 }
 
-void eval_sums_launch(const EvalParams& p, bool train_mode, cudaStream_t s) {
+void fill_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int o, const int64_t* offs,
+                       uint32_t* lists, cudaStream_t s) {
+  if (clauses <= 0) return;
+  count_launch();
+  fill_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, o, offs, lists);
+}
+
+int64_t lit_t_stride(int64_t q) { return ((q + 31) / 32 + 31) / 32 * 32; }
+
+void transpose_literals_launch(const uint32_t* xplane, int64_t row_stride, int64_t q, int o, uint32_t* lit_t,
+                               cudaStream_t s) {
+  const int64_t Gs = lit_t_stride(q);
+  const int Wx = (o + 31) / 32;
+  // row o: all ones (the padding literal of every clause list)
+  cudaMemsetAsync(lit_t + static_cast<int64_t>(o) * Gs, 0xFF, Gs * sizeof(uint32_t), s);
+  count_launch();
+  transpose_literals_kernel<<<dim3(static_cast<unsigned>(Gs / 32), Wx), 256, 0, s>>>(xplane, row_stride, q, o, Gs,
+                                                                                      lit_t);
+}
+
+void eval_bits_launch(const BitsEvalParams& p, bool train_mode, cudaStream_t s) {
   if (p.q <= 0 || p.n_loc <= 0) return;
-  const int chunks = (p.n_loc + p.chunk - 1) / p.chunk;
-  auto go = [&](auto kern, int tile) {
-    dim3 grid(blocks_for(p.q, tile), p.m * chunks);
-    EvalParams q = p;
-    // ~16 KB of staged include lists per CTA (at least one clause).
-    q.stage = std::max(1, std::min(TMG_EVAL_STAGE, static_cast<int>((16 * 1024) / (16 * std::max(1, p.Wx)))));
-    const size_t shm = sizeof(uint32_t) * ((2 * p.Wx * (tile + 1) + 3) & ~3) +
-                       sizeof(uint4) * static_cast<size_t>(q.stage) * p.Wx + sizeof(int) * q.stage;
-    if (shm > 48 * 1024)
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
-    count_launch();
-    kern<<<grid, tile, shm, s>>>(q);
-  };
-  const bool wide = sizeof(uint32_t) * 2 * p.Wx * 129 > 200 * 1024;
-  const bool direct = sizeof(uint32_t) * 2 * p.Wx * 33 + 16 * p.Wx + 16 > 200 * 1024;
-  if (direct) {
-    dim3 grid(blocks_for(p.q, 128), p.m * chunks);
-    count_launch();
-    if (train_mode) eval_sums_direct_kernel<true><<<grid, 128, 0, s>>>(p);
-    else eval_sums_direct_kernel<false><<<grid, 128, 0, s>>>(p);
-    return;
-  }
-  if (train_mode) {
-    if (wide) go(eval_sums_kernel<true, 32>, 32);
-    else go(eval_sums_kernel<true, 128>, 128);
-  } else {
-    if (wide) go(eval_sums_kernel<false, 32>, 32);
-    else go(eval_sums_kernel<false, 128>, 128);
-  }
+  dim3 grid(static_cast<unsigned>((p.q + 1023) / 1024), static_cast<unsigned>(p.m * p.chunks));
+  count_launch();
+  if (train_mode) eval_bits_kernel<true><<<grid, kEvalWarps * 32, 0, s>>>(p);
+  else eval_bits_kernel<false><<<grid, kEvalWarps * 32, 0, s>>>(p);
 }
 
 void counters_to_planes_launch(const uint16_t* counters, uint32_t* state, int clauses, int o, int B,

@@ -113,20 +113,18 @@ struct SeqParams {  // classic sequential trainer mirror (trainer.cpp:138-179)
 };
 bool train_sequential_launch(const TrainParams& p, const SeqParams& sp, int B, cudaStream_t s);
 
-struct EvalEntry {  // one nonzero include word of a clause
-  uint32_t w, inc_x, inc_n, pad;
-};
-
-struct EvalParams {
-  const EvalEntry* entries;  // [m*n_loc][Wx]
-  const int32_t* nentries;   // [m*n_loc]
+// Example-sliced class sums (eval.cu): included-literal lists per clause
+// against feature-major bit columns of the examples.
+struct BitsEvalParams {
+  const uint32_t* lit_t;     // [o + 1][Gs]: bit e of word g = x_f of example 32g + e; row o all ones
+  int64_t Gs;                // words per lit_t row (lit_t_stride(q))
+  const uint32_t* lists;     // concatenated literal lists, entry = f << 1 | negated, padded to 8 with o << 1
+  const int64_t* offs;       // [m*n_loc + 1] list offsets (multiples of 8)
   const int32_t* inc_count;  // [m*n_loc]
   uint32_t* prev;            // refresh mode: [m*n_loc][Wq]
-  int32_t n_loc, j_begin, m, Wx, Wp, Wq, chunk;
-  int32_t stage;  // clauses whose include lists are staged in shared memory at a time (set at launch)
-  int32_t all_positive;  // regression head: every clause votes +1
-  const uint32_t* xplane;
-  const uint32_t* nplane;
+  int32_t n_loc, j_begin, m, Wq;
+  int32_t cta_clauses, chunks;  // clauses per CTA (<= 2040), CTAs per class
+  int32_t all_positive;         // regression head: every clause votes +1
   int64_t q;
   int32_t* sums;  // [q][m], accumulated with atomics
 };
@@ -141,9 +139,15 @@ bool type_i_smem_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, 
                              cudaStream_t s);
 bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out, uint32_t trials, int B, int NW,
                            unsigned long long* inc, unsigned long long* dec, cudaStream_t s);
-void build_entries_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, EvalEntry* e,
-                          int32_t* ne, int32_t* inc_count, cudaStream_t s);
-void eval_sums_launch(const EvalParams& p, bool train_mode, cudaStream_t s);
+// Include counts, padded list lengths and offsets; returns the total list length (-1 on a CUDA error; syncs).
+int64_t build_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int32_t* inc_count,
+                           int32_t* lens, int64_t* offs, cudaStream_t s);
+void fill_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int o, const int64_t* offs,
+                       uint32_t* lists, cudaStream_t s);
+int64_t lit_t_stride(int64_t q);
+void transpose_literals_launch(const uint32_t* xplane, int64_t row_stride, int64_t q, int o, uint32_t* lit_t,
+                               cudaStream_t s);
+void eval_bits_launch(const BitsEvalParams& p, bool train_mode, cudaStream_t s);
 void counters_to_planes_launch(const uint16_t* counters, uint32_t* state, int clauses, int o, int B,
                                int Wp, int N, cudaStream_t s);
 void planes_to_counters_launch(const uint32_t* state, uint16_t* counters, int clauses, int o, int B,

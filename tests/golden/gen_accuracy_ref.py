@@ -29,6 +29,17 @@ CASES = {
                          noise=0.0, data_seed=2352),
     "imdb_q4000": dict(data="imdb", q=4000, qtest=2000, clauses=10000, T=100, s=15.0, epochs=2,
                        noise=0.0, data_seed=10000),
+    # The configuration bench.py times (BASELINE.json configs[1]) at its full
+    # size: q = 60 000 training rows, 10 000 test rows, 3 epochs.
+    "mnist_q60000": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
+                         noise=0.0, data_seed=2009),
+    # The reference's own worker-count spread at that configuration.
+    "mnist_q60000_w1": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
+                            noise=0.0, data_seed=2009, workers=1, seeds=1),
+    "mnist_q60000_w2": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
+                            noise=0.0, data_seed=2009, workers=2, seeds=2),
+    "mnist_q60000_w4": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
+                            noise=0.0, data_seed=2009, workers=4, seeds=2),
 }
 
 
@@ -49,15 +60,20 @@ def main():
     workers = os.cpu_count() or 1
     for name in names:
         case = CASES[name]
-        per_seed = {}
-        for seed in range(1, 6):
+        per_seed, seconds, events = {}, {}, {}
+        for seed in range(1, case.get("seeds", 5) + 1):
             rows = run(case, seed, workers)
             per_seed[str(seed)] = [r["test_accuracy"] for r in rows]
-            print(name, seed, per_seed[str(seed)][-1], flush=True)
-        final = [v[-1] for v in per_seed.values()]
-        res[name] = dict(config=case, workers=case.get("workers", workers), per_seed=per_seed,
-                         mean_final=sum(final) / len(final))
-        json.dump(res, open(path, "w"), indent=1)
+            seconds[str(seed)] = [r["seconds"] for r in rows]
+            events[str(seed)] = [r["feedback_events"] for r in rows]
+            print(name, seed, per_seed[str(seed)], seconds[str(seed)], flush=True)
+            final = [v[-1] for v in per_seed.values()]
+            # re-read: other cases may be running concurrently into the same file
+            res = json.load(open(path)) if os.path.exists(path) else {}
+            res[name] = dict(config=case, workers=case.get("workers", workers), per_seed=per_seed,
+                             mean_final=sum(final) / len(final), epoch_seconds=seconds,
+                             feedback_events=events)
+            json.dump(res, open(path, "w"), indent=1)
 
 
 if __name__ == "__main__":
