@@ -48,6 +48,11 @@ extern "C" {
 #define TMG_MODE_ASYNC 0       /* Algorithm 1, every clause concurrently (GPU) */
 #define TMG_MODE_SYNC_MIRROR 1 /* bit-exact replay of train_epoch_parallel's
                                   W-worker schedule (exact reference for W=1) */
+#define TMG_MODE_AUTO 2        /* what the drop-in train_epoch_parallel uses (C++
+                                  facade and Python alike): TMG_MODE_ASYNC for any
+                                  `workers`, unless workers == 1 and the environment
+                                  sets TSETLIN_DETERMINISTIC=1, which selects the
+                                  bit-exact single-worker replay */
 
 /* Evaluation modes (core.hpp:33-35). */
 #define TMG_EVAL_TRAIN 0
@@ -83,7 +88,8 @@ typedef struct tmg_machine_info {
   int32_t clause_begin, clause_end; /* this shard's slice of every class */
   int32_t planes;                   /* bit planes per automaton (B) */
   int32_t words_per_lane;           /* NW: 32-bit words per lane per part */
-  int32_t bound_examples;           /* ClassBank::bound_examples (core.hpp:183) */
+  int32_t bound_examples;           /* ClassBank::bound_examples (core.hpp:183) shared by every
+                                       bank; -1 when the banks are bound to different counts */
   int32_t device;
   uint64_t device_bytes;
 } tmg_machine_info;
@@ -152,10 +158,16 @@ int tmg_set_counters(tmg_machine* tm, int32_t bank, const uint16_t* in);
 /* ClassBank::include_mask / include_count (core.hpp:147-156): n x W64 u64, n i32. */
 int tmg_get_include_masks(const tmg_machine* tm, int32_t bank, uint64_t* out);
 int tmg_get_include_counts(const tmg_machine* tm, int32_t bank, int32_t* out);
-/* ClassBank::bind_examples (core.cpp:117-126): zeroes all previous outputs. */
+/* ClassBank::bind_examples (core.cpp:117-126) on every bank of the machine:
+ * zeroes all previous outputs. */
 int tmg_bind_examples(tmg_machine* tm, int64_t example_count);
+/* ClassBank::bind_examples (core.cpp:117-126) on ONE bank: zeroes that bank's
+ * previous outputs only; the other banks keep theirs. */
+int tmg_bind_bank(tmg_machine* tm, int32_t bank, int64_t example_count);
+/* ClassBank::bound_examples (core.hpp:183) of one bank. */
+int tmg_bank_bound_examples(const tmg_machine* tm, int32_t bank, int64_t* example_count);
 /* ClassBank::prev_output / set_prev_output (core.hpp:184-191):
- * n x ceil(q/64) uint64 per bank. */
+ * n x ceil(bound/64) uint64 per bank (bound = that bank's bound_examples). */
 int tmg_get_prev_outputs(const tmg_machine* tm, int32_t bank, uint64_t* out);
 int tmg_set_prev_outputs(tmg_machine* tm, int32_t bank, const uint64_t* in);
 

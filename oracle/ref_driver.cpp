@@ -257,6 +257,10 @@ void golden_update_clause(const std::string& dir) {
       {20, 3, 6, 5, 50, 4, 2.5, 1, 1, 17, 100, 2, 3},
       {784, 10, 4, 128, 40, 50, 10.0, 0, 1, 3, 40, 7, 1},
       {70, 2, 2, 64, 130, 8, 5.0, 0, 0, 129, 260, 1, 0},
+      // q < 32 with batch > q: the (offset + t) % q walk revisits examples
+      // inside one 32-step window of the GPU replay
+      {12, 2, 4, 128, 20, 15, 3.9, 0, 1, 7, 70, 0, 1},
+      {12, 2, 4, 128, 5, 15, 3.9, 0, 0, 3, 23, 1, 0},
   };
   int idx = 0;
   std::string manifest = "[\n";

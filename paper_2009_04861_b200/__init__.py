@@ -14,7 +14,7 @@ from . import _capi as _capi_mod
 _capi_mod.lib()  # fail loudly at import when the CUDA engine is missing
 
 from .model_io import load_model_file, save_model_file  # noqa: E402
-from .tsetlin import (MODE_ASYNC, MODE_SYNC_MIRROR, PREDICT, TRAIN, ClassBank, EpochReport,  # noqa: E402
+from .tsetlin import (MODE_ASYNC, MODE_AUTO, MODE_SYNC_MIRROR, PREDICT, TRAIN, ClassBank, EpochReport,  # noqa: E402
                       ExamplePool, MultiClassTM, RegressionHead, Rng, TMConfig, class_sums, classify,
                       device_count, epoch_order, evaluate_accuracy, evaluate_clause, evaluate_scaled_mae,
                       export_vote_sums, feedback_rates, literal_words, predict_all, predict_literals,
@@ -24,7 +24,7 @@ from .tsetlin import (MODE_ASYNC, MODE_SYNC_MIRROR, PREDICT, TRAIN, ClassBank, E
                       update_regress, vote_sum)
 
 __all__ = [
-    "MODE_ASYNC", "MODE_SYNC_MIRROR", "PREDICT", "TRAIN", "ClassBank", "EpochReport",
+    "MODE_ASYNC", "MODE_AUTO", "MODE_SYNC_MIRROR", "PREDICT", "TRAIN", "ClassBank", "EpochReport",
     "ExamplePool", "MultiClassTM", "RegressionHead", "Rng", "TMConfig", "class_sums", "classify",
     "device_count", "epoch_order", "evaluate_accuracy", "evaluate_clause", "evaluate_scaled_mae",
     "export_vote_sums", "feedback_rates", "literal_words", "load_model_file", "predict_all",

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TMG_LIB") or os.path.join(HERE, "_lib", "libtmgpu.so")
 
 TMG_OK, TMG_EINVAL, TMG_ERANGE, TMG_ERUNTIME = 0, 1, 2, 3
-MODE_ASYNC, MODE_SYNC_MIRROR = 0, 1
+MODE_ASYNC, MODE_SYNC_MIRROR, MODE_AUTO = 0, 1, 2
 EVAL_TRAIN, EVAL_PREDICT = 0, 1
 
 
@@ -72,6 +72,8 @@ SIGNATURES = {
     "tmg_get_include_masks": (C.c_int, [P, I32, P]),
     "tmg_get_include_counts": (C.c_int, [P, I32, P]),
     "tmg_bind_examples": (C.c_int, [P, I64]),
+    "tmg_bind_bank": (C.c_int, [P, I32, I64]),
+    "tmg_bank_bound_examples": (C.c_int, [P, I32, P]),
     "tmg_get_prev_outputs": (C.c_int, [P, I32, P]),
     "tmg_set_prev_outputs": (C.c_int, [P, I32, P]),
     "tmg_pool_create": (C.c_int, [I32, I32, P, P, I64, I32, PP]),

@@ -3,8 +3,9 @@ row f4; reference: proj/src/bench.cpp:45-142, bench.hpp:28-58), so GPU rows
 line up with the CPU reference's `tm bench` output.
 
 Modes: "seq" = train_epoch_sequential (GPU mirror), "par" =
-train_epoch_parallel (asynchronous all-clause GPU trainer when workers > 1,
-the bit-exact one-worker replay when workers == 1). `seconds` is the epoch
+train_epoch_parallel in TMG_MODE_AUTO, like the C++ facade (the asynchronous
+all-clause GPU trainer; the bit-exact one-worker replay when workers == 1 and
+TSETLIN_DETERMINISTIC=1). `seconds` is the epoch
 only (EpochReport.seconds); the metric is test accuracy (or MAE for
 regression) after each measured epoch.
 """
@@ -63,9 +64,7 @@ def bench_sweep(train_x, train_y, test_x, test_y, base: T.TMConfig, options: Ben
                 test = T.ExamplePool(o, test_x, np.asarray(test_y, np.int32), 1)
                 for e in range(total_epochs):
                     rep = (T.train_epoch_regress_sequential(head, pool, e) if mode == "seq"
-                           else T.train_epoch_regress_parallel(head, pool, workers, e,
-                                                               mode=T.MODE_ASYNC if workers > 1
-                                                               else T.MODE_SYNC_MIRROR))
+                           else T.train_epoch_regress_parallel(head, pool, workers, e, mode=T.MODE_AUTO))
                     if e < options.warmup_epochs:
                         continue
                     v = T.predict_scaled_all(head, test).astype(np.float64)
@@ -82,8 +81,7 @@ def bench_sweep(train_x, train_y, test_x, test_y, base: T.TMConfig, options: Ben
                 if mode == "seq":
                     rep = T.train_epoch_sequential(tm, pool, e)
                 else:
-                    rep = T.train_epoch_parallel(tm, pool, workers, e,
-                                                 mode=T.MODE_ASYNC if workers > 1 else T.MODE_SYNC_MIRROR)
+                    rep = T.train_epoch_parallel(tm, pool, workers, e, mode=T.MODE_AUTO)
                 if e < options.warmup_epochs:
                     continue
                 records.append(BenchRecord(mode, 1 if mode == "seq" else workers, clauses,

@@ -14,66 +14,18 @@
 
 #include <cuda_runtime.h>
 
+#include "engine.h"
 #include "kernels.h"
 #include "tmgpu.h"
 #include "tmgpu_rng.h"
-
-#define TMG_API extern "C" __attribute__((visibility("default")))
-
-#ifndef TMG_EVAL_WAVES
-#define TMG_EVAL_WAVES 8  // 1.77 -> 1.34 ms for MNIST-2000 predict on 10k rows (r1ae)
-#endif
 
 namespace tmg {
 unsigned long long g_launches = 0;
 }
 
-namespace {
-
-struct Error {
-  int code;
-  std::string msg;
-};
+namespace tmgx {
 
 thread_local std::string g_last_error;
-
-[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
-
-void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) fail(TMG_ERUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
-}
-#define CK(x) cuda_check((x), #x)
-
-template <typename F>
-int guarded(F&& f) {
-  try {
-    f();
-    return TMG_OK;
-  } catch (const Error& e) {
-    g_last_error = e.msg;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    g_last_error = "out of host memory";
-    return TMG_ERUNTIME;
-  } catch (const std::exception& e) {
-    g_last_error = e.what();
-    return TMG_ERUNTIME;
-  }
-}
-
-// Restores the caller's current device on scope exit.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) CK(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 // Keeps the current device's default memory pool from returning freed memory
 // to the driver at every synchronisation (once per device).
@@ -90,57 +42,6 @@ void pool_init() {
   done[dev].store(true, std::memory_order_release);
 }
 
-template <typename T>
-struct DevBuf {
-  T* ptr = nullptr;
-  size_t count = 0;
-  DevBuf() = default;
-  DevBuf(const DevBuf&) = delete;
-  DevBuf& operator=(const DevBuf&) = delete;
-  ~DevBuf() { release(); }
-  // Device memory comes from the device's stream-ordered pool, which keeps
-  // freed blocks mapped (release threshold raised in pool_init): creating and
-  // dropping example pools per call stays cheap. alloc/release keep
-  // cudaMalloc/cudaFree's synchronous semantics.
-  void alloc(size_t n) {
-    release();
-    if (n) {
-      pool_init();
-      CK(cudaMallocAsync(reinterpret_cast<void**>(&ptr), n * sizeof(T), cudaStreamPerThread));
-      CK(cudaStreamSynchronize(cudaStreamPerThread));
-    }
-    count = n;
-  }
-  // Plain cudaMalloc memory instead (IPC-exportable: the stream-ordered
-  // pool's blocks cannot be shared with cudaIpcGetMemHandle).
-  void alloc_plain(size_t n) {
-    release();
-    if (n) CK(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
-    count = n;
-    plain = n != 0;
-  }
-  void release() {
-    if (ptr) {
-      cudaDeviceSynchronize();
-      if (plain) {
-        cudaFree(ptr);
-      } else {
-        cudaFreeAsync(ptr, cudaStreamPerThread);
-        cudaStreamSynchronize(cudaStreamPerThread);
-      }
-    }
-    ptr = nullptr;
-    count = 0;
-    plain = false;
-  }
-  void swap(DevBuf& o) {
-    std::swap(ptr, o.ptr);
-    std::swap(count, o.count);
-    std::swap(plain, o.plain);
-  }
-  bool plain = false;
-  size_t bytes() const { return count * sizeof(T); }
-};
 
 // Supported words-per-lane instantiations of the training kernels.
 int round_nw(int nw) {
@@ -213,61 +114,12 @@ void build_alias8(uint32_t P, uint32_t out[256]) {
                                                : (static_cast<uint32_t>(thr[i]) << 8) | static_cast<uint32_t>(alias[i]);
 }
 
-}  // namespace
 
-struct tmg_pool {
-  int device = 0;
-  int o = 0, m = 0, Wp = 0;
-  int64_t q = 0;
-  cudaStream_t stream = nullptr;
-  DevBuf<uint32_t> rows;  // [q][2][Wp]: x-plane words, then !x-plane words
-  uint32_t* xplane() const { return rows.ptr; }
-  uint32_t* nplane() const { return rows.ptr + Wp; }
-  DevBuf<int32_t> labels, tallies, delta, order;
-  // Feature-major example columns for evaluation (eval.cu), built on first
-  // use: the rows never change after creation.
-  mutable DevBuf<uint32_t> lit_t;
-  std::vector<int32_t> host_labels;
-  // Tally replicas of the other ranks (multi-GPU over peer memory): every
-  // tally change is also added into each of them by the training kernels.
-  std::vector<int32_t*> peers;
-  void close_peers() {
-    for (int32_t* p : peers) cudaIpcCloseMemHandle(p);
-    peers.clear();
-  }
-};
+}  // namespace tmgx
 
-struct tmg_machine {
-  tmg_config cfg{};
-  int o = 0, m = 0, n = 0, j_begin = 0, j_end = 0, n_loc = 0;
-  int N = 0, B = 0, NW = 0, Wx = 0, Wp = 0, Wq = 0;
-  int device = 0;
-  int64_t q_bound = 0;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  DevBuf<uint32_t> state, prev;
-  DevBuf<int32_t> inc_count, lens, sums;
-  DevBuf<int64_t> offs;      // [clauses + 1] literal-list offsets
-  DevBuf<uint32_t> lists;    // included-literal lists (eval.cu)
-  DevBuf<uint32_t> lit_t;    // scratch: feature-major example columns of non-pool rows
-  DevBuf<unsigned long long> events;
-  DevBuf<unsigned long long> dbg;  // instrumentation counters (TMG_STATS builds)
-  DevBuf<uint32_t> alias8;         // alias table of the clause-output-0 Type I draw
-  DevBuf<uint16_t> scratch16;
-  // sequential-trainer jump matrices (M^chunk, M^(2o)) and per-clause states
-  DevBuf<uint32_t> seq_jump;
-  DevBuf<uint64_t> seq_tstate;
-  DevBuf<uint32_t> seq_scratch;  // grid-wide replay: output / gated bits, votes, negative class
-  bool entries_dirty = true;
-  // current async epoch
-  int32_t cur_epoch = -1;
-  uint32_t key0 = 0, key1 = 0;
-  int all_positive = 0;  // regression head bank (PolarityScheme::AllPositive)
-  bool regress_mode = false;  // current call trains the regression head
-  int clauses() const { return m * n_loc; }
-};
+using namespace tmgx;
 
-namespace {
+namespace tmgx {
 
 void validate_config(const tmg_config& c) {  // core.cpp:48-74
   if (c.clauses < 2 || c.clauses % 2 != 0)
@@ -290,14 +142,58 @@ void check_compatible(const tmg_machine* tm, const tmg_pool* pool) {  // trainer
   if (tm->device != pool->device) fail(TMG_EINVAL, "model and pool live on different devices");
 }
 
-void bind(tmg_machine* tm, int64_t q) {  // core.cpp:117-126
+void check_bind_count(int64_t q) {
   if (q < 0) fail(TMG_EINVAL, "example count must be >= 0");
   if (q > (int64_t(1) << 31) - 64) fail(TMG_EINVAL, "example count too large");
+}
+
+// bind_examples on every bank (core.cpp:117-126): all bitmaps cleared.
+void bind(tmg_machine* tm, int64_t q) {
+  check_bind_count(q);
   tm->q_bound = q;
+  tm->bank_q.assign(static_cast<size_t>(tm->m), q);
   tm->Wq = static_cast<int>(2 * ((q + 63) / 64));
   tm->prev.alloc(static_cast<size_t>(tm->clauses()) * tm->Wq);
   if (tm->prev.bytes()) CK(cudaMemsetAsync(tm->prev.ptr, 0, tm->prev.bytes(), tm->stream));
   CK(cudaStreamSynchronize(tm->stream));
+}
+
+// bind_examples on ONE bank: only its bitmap is cleared, the other banks keep
+// theirs (the buffer's row stride grows to the widest binding).
+void bind_bank(tmg_machine* tm, int c, int64_t q) {
+  check_bind_count(q);
+  const int need = static_cast<int>(2 * ((q + 63) / 64));
+  const size_t rows = static_cast<size_t>(tm->clauses());
+  if (need > tm->Wq) {
+    DevBuf<uint32_t> grown;
+    grown.alloc(rows * need);
+    CK(cudaMemsetAsync(grown.ptr, 0, grown.bytes(), tm->stream));
+    if (tm->Wq > 0 && rows)
+      CK(cudaMemcpy2DAsync(grown.ptr, static_cast<size_t>(need) * 4, tm->prev.ptr, static_cast<size_t>(tm->Wq) * 4,
+                           static_cast<size_t>(tm->Wq) * 4, rows, cudaMemcpyDeviceToDevice, tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+    tm->prev.swap(grown);
+    tm->Wq = need;
+  }
+  const size_t bank_words = static_cast<size_t>(tm->n_loc) * tm->Wq;
+  if (bank_words)
+    CK(cudaMemsetAsync(tm->prev.ptr + static_cast<size_t>(c) * bank_words, 0, bank_words * 4, tm->stream));
+  tm->bank_q[static_cast<size_t>(c)] = q;
+  tm->q_bound = q;
+  for (int64_t b : tm->bank_q)
+    if (b != q) tm->q_bound = -1;
+  CK(cudaStreamSynchronize(tm->stream));
+}
+
+// What every trainer does first (trainer.cpp:150,192-194; pool.cpp:113):
+// rebind only the banks whose bound count differs from the pool's.
+void bind_for(tmg_machine* tm, int64_t q) {
+  if (tm->q_bound == q) return;
+  bool none = true;
+  for (int64_t b : tm->bank_q) none = none && b != q;
+  if (none) return bind(tm, q);
+  for (int c = 0; c < tm->m; ++c)
+    if (tm->bank_q[static_cast<size_t>(c)] != q) bind_bank(tm, c, q);
 }
 
 // Include counts and the per-clause included-literal lists of the current
@@ -305,14 +201,16 @@ void bind(tmg_machine* tm, int64_t q) {  // core.cpp:117-126
 void rebuild_entries(tmg_machine* tm) {
   if (!tm->entries_dirty) return;
   const int64_t total = tmg::build_lists_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx,
-                                                tm->inc_count.ptr, tm->lens.ptr, tm->offs.ptr, tm->stream);
+                                                tm->inc_count.ptr, tm->lens.ptr, tm->npos.ptr, tm->offs.ptr,
+                                                tm->stream);
   if (total < 0) CK(cudaGetLastError());
+  tm->lists_total = total;
   if (tm->lists.count < static_cast<size_t>(total) + 8) {
     // grow with headroom: lists get longer as clauses learn
     tm->lists.alloc(static_cast<size_t>(total + total / 4) + 64);
   }
-  tmg::fill_lists_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx, tm->o, tm->offs.ptr, tm->lists.ptr,
-                         tm->stream);
+  tmg::fill_lists_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx, tm->o, tm->offs.ptr, tm->npos.ptr,
+                         tm->lists.ptr, tm->stream);
   CK(cudaGetLastError());
   tm->entries_dirty = false;
 }
@@ -326,7 +224,7 @@ void reset_state(tmg_machine* tm) {  // ClassBank ctor: counters = N (core.cpp:9
   CK(cudaStreamSynchronize(tm->stream));
 }
 
-tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int jb, int je, int all_positive = 0) {
+tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int jb, int je, int all_positive) {
   if (!cfg) fail(TMG_EINVAL, "null config");
   validate_config(*cfg);
   if (m < 1) fail(TMG_EINVAL, "class count must be >= 1");
@@ -362,6 +260,7 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->state.alloc(cl * tm->B * 2 * tm->Wp);
     tm->inc_count.alloc(cl);
     tm->lens.alloc(cl);
+    tm->npos.alloc(cl);
     tm->offs.alloc(cl + 1);
     tm->events.alloc(2 * static_cast<size_t>(m));  // all events, then Type I events
     tm->dbg.alloc(tmg::kDebugCounters);
@@ -607,20 +506,21 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
 // given. lit_t: the rows' feature-major columns if already built (pools cache
 // theirs), else they are built into the machine's scratch.
 void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool train_mode, int32_t* d_out,
-                       uint32_t* prev, const uint32_t* lit_t = nullptr) {
+                       uint32_t* prev, const uint32_t* lit_t) {
   rebuild_entries(tm);
   const int64_t Gs = tmg::lit_t_stride(q);
   if (!lit_t) {
-    const size_t need = static_cast<size_t>(tm->o + 1) * Gs;
+    const size_t need = static_cast<size_t>(tm->o + 2) * Gs;
     if (tm->lit_t.count < need) tm->lit_t.alloc(need);
     tmg::transpose_literals_launch(xplane, 2 * tm->Wp, q, tm->o, tm->lit_t.ptr, tm->stream);
     lit_t = tm->lit_t.ptr;
   }
   tmg::BitsEvalParams e{};
   e.lit_t = lit_t;
-  e.Gs = Gs;
+  e.Gs = static_cast<uint32_t>(Gs);
   e.lists = tm->lists.ptr;
   e.offs = tm->offs.ptr;
+  e.npos = tm->npos.ptr;
   e.inc_count = tm->inc_count.ptr;
   e.prev = prev;
   e.n_loc = tm->n_loc;
@@ -630,10 +530,14 @@ void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool 
   e.q = q;
   e.sums = d_out;
   e.all_positive = tm->all_positive;
-  // Enough CTAs for ~4 resident waves of 4 CTAs (32 warps) per SM; at most
-  // 2040 clauses per CTA (the bit-sliced counters' range), >= 4 per warp.
+  // 2 to 6 resident waves of 5 CTAs (40 warps) per SM, by the literal loads
+  // to do (~1k per warp and wave); at most 2040 clauses per CTA (the
+  // bit-sliced counters' range), >= 4 per warp.
   const int64_t blocks = (q + 1023) / 1024;
-  int64_t chunks = (int64_t(148) * 4 * 4 + blocks * tm->m - 1) / (blocks * tm->m);
+  const int64_t resident = int64_t(148) * 5;
+  const int64_t steps = blocks * tm->lists_total;  // warp-level literal loads
+  const int64_t waves = std::min<int64_t>(6, std::max<int64_t>(2, steps / (resident * 8 * 1024)));
+  int64_t chunks = (resident * waves + blocks * tm->m - 1) / (blocks * tm->m);
   chunks = std::max<int64_t>(chunks, (tm->n_loc + 2039) / 2040);
   chunks = std::min<int64_t>(chunks, std::max(1, tm->n_loc / 32));
   chunks = std::max<int64_t>(chunks, (tm->n_loc + 2039) / 2040);
@@ -647,7 +551,7 @@ void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool 
 
 const uint32_t* pool_lit_t(tmg_machine* tm, const tmg_pool* pool) {
   if (!pool->lit_t.ptr) {
-    pool->lit_t.alloc(static_cast<size_t>(pool->o + 1) * tmg::lit_t_stride(pool->q));
+    pool->lit_t.alloc(static_cast<size_t>(pool->o + 2) * tmg::lit_t_stride(pool->q));
     tmg::transpose_literals_launch(pool->xplane(), 2 * pool->Wp, pool->q, pool->o, pool->lit_t.ptr, tm->stream);
     CK(cudaGetLastError());
   }
@@ -715,7 +619,7 @@ void check_bank(const tmg_machine* tm, int32_t bank) {
   if (bank < 0 || bank >= tm->m) fail(TMG_ERANGE, "bank index out of range");
 }
 
-}  // namespace
+}  // namespace tmgx
 
 // ===================================================================== ABI ===
 
@@ -772,6 +676,7 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   tm->prev.release();
   tm->inc_count.release();
   tm->lens.release();
+  tm->npos.release();
   tm->offs.release();
   tm->lit_t.release();
   tm->sums.release();
@@ -802,7 +707,7 @@ TMG_API int tmg_machine_info_get(const tmg_machine* tm, tmg_machine_info* info) 
     info->bound_examples = static_cast<int32_t>(tm->q_bound);
     info->device = tm->device;
     info->device_bytes = tm->state.bytes() + tm->prev.bytes() + tm->inc_count.bytes() + tm->lists.bytes() +
-                         tm->lens.bytes() + tm->offs.bytes() + tm->lit_t.bytes() + tm->sums.bytes();
+                         tm->lens.bytes() + tm->npos.bytes() + tm->offs.bytes() + tm->lit_t.bytes() + tm->sums.bytes();
   });
 }
 
@@ -908,15 +813,33 @@ TMG_API int tmg_bind_examples(tmg_machine* tm, int64_t q) {
   });
 }
 
+TMG_API int tmg_bind_bank(tmg_machine* tm, int32_t bank, int64_t q) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    DeviceGuard dg(tm->device);
+    bind_bank(tm, bank, q);
+  });
+}
+
+TMG_API int tmg_bank_bound_examples(const tmg_machine* tm, int32_t bank, int64_t* q) {
+  return guarded([&] {
+    check_bank(M(tm), bank);
+    *q = tm->bank_q[static_cast<size_t>(bank)];
+  });
+}
+
+// Previous outputs of one bank in the reference layout: per clause
+// ceil(bound/64) u64 words (the device rows are Wq u32 words apart).
 TMG_API int tmg_get_prev_outputs(const tmg_machine* ctm, int32_t bank, uint64_t* out) {
   return guarded([&] {
     auto tm = const_cast<tmg_machine*>(M(ctm));
     check_bank(tm, bank);
     DeviceGuard dg(tm->device);
-    const size_t words = static_cast<size_t>(tm->n_loc) * tm->Wq;
-    if (words)
-      CK(cudaMemcpyAsync(out, tm->prev.ptr + static_cast<size_t>(bank) * words, words * 4, cudaMemcpyDeviceToHost,
-                         tm->stream));
+    const size_t w = 2 * static_cast<size_t>((tm->bank_q[static_cast<size_t>(bank)] + 63) / 64);
+    const size_t rows = static_cast<size_t>(tm->n_loc);
+    if (w && rows)
+      CK(cudaMemcpy2DAsync(out, w * 4, tm->prev.ptr + static_cast<size_t>(bank) * rows * tm->Wq,
+                           static_cast<size_t>(tm->Wq) * 4, w * 4, rows, cudaMemcpyDeviceToHost, tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
   });
 }
@@ -925,10 +848,11 @@ TMG_API int tmg_set_prev_outputs(tmg_machine* tm, int32_t bank, const uint64_t* 
   return guarded([&] {
     check_bank(M(tm), bank);
     DeviceGuard dg(tm->device);
-    const size_t words = static_cast<size_t>(tm->n_loc) * tm->Wq;
-    if (words)
-      CK(cudaMemcpyAsync(tm->prev.ptr + static_cast<size_t>(bank) * words, in, words * 4, cudaMemcpyHostToDevice,
-                         tm->stream));
+    const size_t w = 2 * static_cast<size_t>((tm->bank_q[static_cast<size_t>(bank)] + 63) / 64);
+    const size_t rows = static_cast<size_t>(tm->n_loc);
+    if (w && rows)
+      CK(cudaMemcpy2DAsync(tm->prev.ptr + static_cast<size_t>(bank) * rows * tm->Wq, static_cast<size_t>(tm->Wq) * 4,
+                           in, w * 4, w * 4, rows, cudaMemcpyHostToDevice, tm->stream));
     CK(cudaStreamSynchronize(tm->stream));
   });
 }
@@ -1138,7 +1062,7 @@ TMG_API int tmg_epoch_begin(tmg_machine* tm, tmg_pool* pool, int32_t epoch) {
   return guarded([&] {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
-    if (tm->q_bound != pool->q) bind(tm, pool->q);
+    bind_for(tm, pool->q);
     upload_order(tm, pool, epoch);
     epoch_keys(tm, epoch);
     CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
@@ -1233,14 +1157,23 @@ TMG_API int tmg_train_epoch_regress(tmg_machine* tm, tmg_pool* pool, int32_t mod
   return rc;
 }
 
+// TMG_MODE_AUTO (include/tmgpu.h): one rule for every drop-in caller.
+int32_t tmgx::resolve_mode(int32_t mode, int32_t workers) {
+  if (mode != TMG_MODE_AUTO) return mode;
+  const char* det = std::getenv("TSETLIN_DETERMINISTIC");
+  return workers == 1 && det && det[0] == '1' ? TMG_MODE_SYNC_MIRROR : TMG_MODE_ASYNC;
+}
+
 static int train_epoch_impl(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
                             tmg_epoch_report* report) {
   return guarded([&] {
     check_compatible(M(tm), pool);
     if (workers < 1) fail(TMG_EINVAL, "workers must be >= 1");  // trainer.cpp:184
+    mode = resolve_mode(mode, workers);
+    if (mode != TMG_MODE_ASYNC && mode != TMG_MODE_SYNC_MIRROR) fail(TMG_EINVAL, "unknown training mode");
     DeviceGuard dg(tm->device);
     const auto wall0 = std::chrono::steady_clock::now();
-    if (tm->q_bound != pool->q) bind(tm, pool->q);  // trainer.cpp:192-194
+    bind_for(tm, pool->q);  // trainer.cpp:192-194
     upload_order(tm, pool, epoch);
     CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
     CK(cudaEventRecord(tm->ev0, tm->stream));
@@ -1497,8 +1430,12 @@ TMG_API int tmg_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t c, int32_
     if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
     if (offset < 0) fail(TMG_EINVAL, "offset must be >= 0");
     DeviceGuard dg(tm->device);
-    if (tm->q_bound != pool->q) bind(tm, pool->q);
+    if (tm->bank_q[static_cast<size_t>(c)] != pool->q) bind_bank(tm, c, pool->q);  // trainer.cpp:107
     const bool use_order = order && order_len == pool->q;
+    if (use_order)  // record_output_and_tally's bounds check (pool.cpp:95-98), before any device write
+      for (int64_t k = 0; k < pool->q; ++k)
+        if (order[k] < 0 || order[k] >= pool->q)
+          fail(TMG_ERANGE, "example index " + std::to_string(order[k]) + " out of range");
     if (use_order)
       CK(cudaMemcpyAsync(pool->order.ptr, order, pool->q * 4, cudaMemcpyHostToDevice, tm->stream));
     tmg::MirrorJob jb{};
@@ -1628,8 +1565,10 @@ TMG_API int tmg_evaluate_clause(tmg_machine* tm, int32_t bank, int32_t j, const 
 TMG_API int tmg_refresh_tallies(tmg_machine* tm, tmg_pool* pool) {
   return guarded([&] {
     check_compatible(M(tm), pool);
+    if (tm->n_loc != tm->n)  // a shard's sums are partial: the pool's replicated tallies would be wrong
+      fail(TMG_EINVAL, "refresh_tallies on a clause shard: use tmg_class_sums_device per shard and all-reduce");
     DeviceGuard dg(tm->device);
-    if (tm->q_bound != pool->q) bind(tm, pool->q);  // pool.cpp:113
+    bind_for(tm, pool->q);  // pool.cpp:113
     class_sums_device(tm, pool->xplane(), pool->q, true, pool->tallies.ptr, tm->prev.ptr, pool_lit_t(tm, pool));
     CK(cudaStreamSynchronize(tm->stream));
   });

@@ -10,12 +10,13 @@
 // literals, so for 32 examples at once its output word is the AND of the
 // included literals' 32-example bit columns. The examples are therefore
 // transposed once per call into feature-major bit columns (lit_t: row f =
-// bit e of word g is x_f of example 32g+e, plus one all-ones row), and each
-// clause is compacted to the list of its included literals (feature index,
-// negation flag). A warp takes one clause at a time over 1024 examples:
-// per included literal ONE coalesced 128-byte load and ONE LOP3
-// (acc &= col ^ neg) cover 1024 (clause, example) pairs, with a warp-wide
-// exit once every example is falsified. Clause outputs are summed per
+// bit e of word g is x_f of example 32g+e, plus an all-ones and an all-zeros
+// row), and each clause is compacted to the feature indices of its included
+// positive literals and of its included negated literals. A warp takes one
+// clause at a time over 1024 examples: output = AND(positive columns) &
+// ~OR(negated columns), per included literal ONE address IMAD and ONE
+// coalesced 128-byte load (half a LOP3) for 1024 (clause, example) pairs,
+// with a warp-wide exit once every example is falsified. Clause outputs are summed per
 // example in bit-sliced signed counters (one carry/borrow chain per clause
 // word), reduced across the CTA's warps with bit-sliced adders in shared
 // memory and turned into integers once per CTA.
@@ -31,21 +32,30 @@ namespace {
 constexpr int kEvalWarps = 8;   // warps per eval CTA (same example block, disjoint clause ranges)
 constexpr int kSumPlanes = 12;  // bit-sliced two's-complement counters: |sum| <= 2040 per CTA
 
-// One warp per clause: count the included literals (top plane) -> inc_count
-// and the list length padded to a multiple of 8 (lens).
+// One warp per clause: count the included literals (top plane) -> inc_count,
+// npos = its positive-literal list length padded to 4, lens = npos + its
+// negated-literal list length padded to 4.
 __global__ void count_literals_kernel(const uint32_t* __restrict__ state, int clauses, int B, int Wp, int Wx,
-                                      int32_t* __restrict__ inc_count, int32_t* __restrict__ lens) {
+                                      int32_t* __restrict__ inc_count, int32_t* __restrict__ lens,
+                                      int32_t* __restrict__ npos) {
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= clauses) return;
   const uint32_t* top = state + (static_cast<size_t>(lc) * B + (B - 1)) * 2 * Wp;
-  int cnt = 0;
-  for (int w = lane; w < Wx; w += 32) cnt += __popc(top[w]) + __popc(top[Wp + w]);
+  int cp = 0, cn = 0;
+  for (int w = lane; w < Wx; w += 32) {
+    cp += __popc(top[w]);
+    cn += __popc(top[Wp + w]);
+  }
 #pragma unroll
-  for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+  for (int off = 16; off; off >>= 1) {
+    cp += __shfl_xor_sync(kFull, cp, off);
+    cn += __shfl_xor_sync(kFull, cn, off);
+  }
   if (lane == 0) {
-    inc_count[lc] = cnt;
-    lens[lc] = (cnt + 7) & ~7;
+    inc_count[lc] = cp + cn;
+    npos[lc] = (cp + 3) & ~3;
+    lens[lc] = ((cp + 3) & ~3) + ((cn + 3) & ~3);
   }
 }
 
@@ -75,18 +85,23 @@ __global__ void __launch_bounds__(1024) scan_lengths_kernel(const int32_t* __res
   if (t == 1023) offs[clauses] = part[1023];
 }
 
-// One warp per clause: write its included literals as (f << 1 | negated),
-// padded to the list length with (o << 1), the all-ones row of lit_t.
+// One warp per clause: its included positive literals' feature indices, padded
+// to 4 with o (the all-ones row of lit_t), then its included negated
+// literals' feature indices, padded to 4 with o + 1 (the all-zeros row).
 __global__ void fill_literals_kernel(const uint32_t* __restrict__ state, int clauses, int B, int Wp, int Wx,
-                                     int o, const int64_t* __restrict__ offs, uint32_t* __restrict__ lists) {
+                                     int o, const int64_t* __restrict__ offs, const int32_t* __restrict__ npos,
+                                     uint32_t* __restrict__ lists) {
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= clauses) return;
   const uint32_t* top = state + (static_cast<size_t>(lc) * B + (B - 1)) * 2 * Wp;
   uint32_t* out = lists + offs[lc];
+  const int split = npos[lc];
   const int len = static_cast<int>(offs[lc + 1] - offs[lc]);
-  int base = 0;
   for (int part = 0; part < 2; ++part) {
+    uint32_t* dst = out + (part ? split : 0);
+    const int end = part ? len - split : split;
+    int base = 0;
     for (int w0 = 0; w0 < Wx; w0 += 32) {
       const int w = w0 + lane;
       uint32_t bits = w < Wx ? top[part * Wp + w] : 0u;
@@ -101,12 +116,12 @@ __global__ void fill_literals_kernel(const uint32_t* __restrict__ state, int cla
       while (bits) {
         const int b = __ffs(bits) - 1;
         bits &= bits - 1;
-        out[pos++] = (static_cast<uint32_t>(w * 32 + b) << 1) | static_cast<uint32_t>(part);
+        dst[pos++] = static_cast<uint32_t>(w * 32 + b);
       }
       base += __shfl_sync(kFull, incl, 31);
     }
+    for (int k = base + lane; k < end; k += 32) dst[k] = static_cast<uint32_t>(o + part);
   }
-  for (int k = base + lane; k < len; k += 32) out[k] = static_cast<uint32_t>(o) << 1;
 }
 
 // Literal rows [q][2][Wp] (x-plane words first) -> feature-major bit columns
@@ -152,9 +167,50 @@ __device__ __forceinline__ void count_word(uint32_t (&P)[kSumPlanes], uint32_t x
   }
 }
 
+// Column word of feature f for this lane: col + f * row_bytes, one
+// IMAD.WIDE.U32 with the 64-bit base as addend.
+__device__ __forceinline__ uint32_t column(const char* __restrict__ col, uint32_t f, uint32_t row_bytes) {
+  return __ldg(reinterpret_cast<const uint32_t*>(col + static_cast<uint64_t>(f) * row_bytes));
+}
+
+// AND (positive list) or OR (negated list) of the listed feature columns:
+// per literal one IMAD.WIDE (address) + one coalesced load, half a LOP3;
+// 16 loads in flight per warp between early-exit votes.
+template <bool POS>
+__device__ __forceinline__ uint32_t fold_columns(const uint32_t* __restrict__ lst, int len,
+                                                 const char* __restrict__ col, uint32_t row_bytes, uint32_t acc,
+                                                 uint32_t other) {
+  const uint4* p = reinterpret_cast<const uint4*>(lst);
+  const uint4* const end = p + (len >> 2);  // lengths are multiples of 4
+  for (; p + 4 <= end; p += 4) {
+    const uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2), d = __ldg(p + 3);
+    const uint32_t v0 = column(col, a.x, row_bytes), v1 = column(col, a.y, row_bytes);
+    const uint32_t v2 = column(col, a.z, row_bytes), v3 = column(col, a.w, row_bytes);
+    const uint32_t v4 = column(col, b.x, row_bytes), v5 = column(col, b.y, row_bytes);
+    const uint32_t v6 = column(col, b.z, row_bytes), v7 = column(col, b.w, row_bytes);
+    const uint32_t v8 = column(col, c.x, row_bytes), v9 = column(col, c.y, row_bytes);
+    const uint32_t va = column(col, c.z, row_bytes), vb = column(col, c.w, row_bytes);
+    const uint32_t vc = column(col, d.x, row_bytes), vd = column(col, d.y, row_bytes);
+    const uint32_t ve = column(col, d.z, row_bytes), vf = column(col, d.w, row_bytes);
+    if (POS) acc &= v0 & v1 & v2 & v3 & v4 & v5 & v6 & v7 & v8 & v9 & va & vb & vc & vd & ve & vf;
+    else acc |= v0 | v1 | v2 | v3 | v4 | v5 | v6 | v7 | v8 | v9 | va | vb | vc | vd | ve | vf;
+    const uint32_t live = POS ? (acc & ~other) : (other & ~acc);
+    if (!__any_sync(kFull, live != 0u)) return POS ? 0u : kFull;  // every example falsified
+  }
+  for (; p < end; ++p) {
+    const uint4 a = __ldg(p);
+    const uint32_t v0 = column(col, a.x, row_bytes), v1 = column(col, a.y, row_bytes);
+    const uint32_t v2 = column(col, a.z, row_bytes), v3 = column(col, a.w, row_bytes);
+    if (POS) acc &= v0 & v1 & v2 & v3;
+    else acc |= v0 | v1 | v2 | v3;
+  }
+  return acc;
+}
+
 template <bool TRAIN>
-__global__ void __launch_bounds__(kEvalWarps * 32) eval_bits_kernel(BitsEvalParams P) {
+__global__ void __launch_bounds__(kEvalWarps * 32, 5) eval_bits_kernel(BitsEvalParams P) {
   __shared__ uint32_t red[kEvalWarps][kSumPlanes][32];
+  __shared__ int next_clause;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * 32 + lane;  // this lane's column word
   const int64_t e0 = gw * 32;
@@ -162,34 +218,34 @@ __global__ void __launch_bounds__(kEvalWarps * 32) eval_bits_kernel(BitsEvalPara
   const int c = blockIdx.y / P.chunks;
   const int jc0 = (blockIdx.y % P.chunks) * P.cta_clauses;
   const int jc1 = min(jc0 + P.cta_clauses, P.n_loc);
-  const int per = (P.cta_clauses + kEvalWarps - 1) / kEvalWarps;
-  const int ja = min(jc1, jc0 + warp * per), jb = min(jc1, ja + per);
-  const uint32_t* __restrict__ col = P.lit_t + gw;
+  const char* __restrict__ col = reinterpret_cast<const char*>(P.lit_t + gw);
+  const uint32_t row_bytes = P.Gs * 4u;
+  if (threadIdx.x == 0) next_clause = jc0 + kEvalWarps;
+  __syncthreads();
   uint32_t cnt[kSumPlanes];
 #pragma unroll
   for (int b = 0; b < kSumPlanes; ++b) cnt[b] = 0u;
-  for (int jl = ja; jl < jb; ++jl) {
+  // Clauses are handed out one at a time (lists differ in length): warps
+  // finish together at the CTA reduction below.
+  for (int jl = jc0 + warp; jl < jc1;) {
     const int lc = c * P.n_loc + jl;
     const int inc = __ldg(P.inc_count + lc);
-    if (!TRAIN && inc == 0) continue;  // empty clause: Predict 0 (core.hpp:211-213)
-    const int64_t off = __ldg(P.offs + lc);
-    const int len = static_cast<int>(__ldg(P.offs + lc + 1) - off);
-    const uint4* lst = reinterpret_cast<const uint4*>(P.lists + off);
     uint32_t acc = valid;  // empty clause: Train 1
-    for (int k = 0; k < len; k += 8) {
-      const uint4 a = __ldg(lst + (k >> 2)), b = __ldg(lst + (k >> 2) + 1);
-      const uint32_t e[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      uint32_t v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(col + static_cast<int64_t>(e[u] >> 1) * P.Gs);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc &= v[u] ^ (0u - (e[u] & 1u));
-      if (!__any_sync(kFull, acc != 0u)) break;
+    if (TRAIN || inc != 0) {  // empty clause: Predict 0 (core.hpp:211-213)
+      const int64_t off = __ldg(P.offs + lc);
+      const int len = static_cast<int>(__ldg(P.offs + lc + 1) - off);
+      const int np = __ldg(P.npos + lc);
+      const uint32_t* lst = P.lists + off;
+      acc = fold_columns<true>(lst, np, col, row_bytes, acc, 0u);
+      if (__any_sync(kFull, acc != 0u) && len > np) acc &= ~fold_columns<false>(lst + np, len - np, col, row_bytes, 0u, acc);
+      if (TRAIN && P.prev != nullptr && gw < P.Wq) P.prev[static_cast<size_t>(lc) * P.Wq + gw] = acc;
+      const int j = P.j_begin + jl;
+      if (P.all_positive || !(j & 1)) count_word<true>(cnt, acc);
+      else count_word<false>(cnt, acc);
     }
-    if (TRAIN && P.prev != nullptr && gw < P.Wq) P.prev[static_cast<size_t>(lc) * P.Wq + gw] = acc;
-    const int j = P.j_begin + jl;
-    if (P.all_positive || !(j & 1)) count_word<true>(cnt, acc);
-    else count_word<false>(cnt, acc);
+    int nj = 0;
+    if (lane == 0) nj = atomicAdd(&next_clause, 1);
+    jl = __shfl_sync(kFull, nj, 0);
   }
   // CTA reduction of the warps' counters: bit-sliced ripple adds in shared memory.
 #pragma unroll
@@ -384,10 +440,10 @@ inline unsigned blocks_for(int64_t n, int per) { return static_cast<unsigned>((n
 }  // namespace
 
 int64_t build_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int32_t* inc_count,
-                           int32_t* lens, int64_t* offs, cudaStream_t s) {
+                           int32_t* lens, int32_t* npos, int64_t* offs, cudaStream_t s) {
   if (clauses <= 0) return 0;
   count_launch();
-  count_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, inc_count, lens);
+  count_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, inc_count, lens, npos);
   count_launch();
   scan_lengths_kernel<<<1, 1024, 0, s>>>(lens, clauses, offs);
   int64_t total = 0;
@@ -398,10 +454,10 @@ int64_t build_lists_launch(const uint32_t* state, int clauses, int B, int Wp, in
 }
 
 void fill_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int o, const int64_t* offs,
-                       uint32_t* lists, cudaStream_t s) {
+                       const int32_t* npos, uint32_t* lists, cudaStream_t s) {
   if (clauses <= 0) return;
   count_launch();
-  fill_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, o, offs, lists);
+  fill_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, o, offs, npos, lists);
 }
 
 int64_t lit_t_stride(int64_t q) { return ((q + 31) / 32 + 31) / 32 * 32; }
@@ -410,8 +466,10 @@ void transpose_literals_launch(const uint32_t* xplane, int64_t row_stride, int64
                                cudaStream_t s) {
   const int64_t Gs = lit_t_stride(q);
   const int Wx = (o + 31) / 32;
-  // row o: all ones (the padding literal of every clause list)
+  // rows o (all ones) and o + 1 (all zeros): the padding of the positive and
+  // the negated clause lists
   cudaMemsetAsync(lit_t + static_cast<int64_t>(o) * Gs, 0xFF, Gs * sizeof(uint32_t), s);
+  cudaMemsetAsync(lit_t + static_cast<int64_t>(o + 1) * Gs, 0, Gs * sizeof(uint32_t), s);
   count_launch();
   transpose_literals_kernel<<<dim3(static_cast<unsigned>(Gs / 32), Wx), 256, 0, s>>>(xplane, row_stride, q, o, Gs,
                                                                                       lit_t);

@@ -45,7 +45,6 @@ namespace detail {
 struct DeviceMachine {
   tmg_machine* h = nullptr;
   int device = 0;
-  int64_t bound = 0;
   std::vector<ClassBank::Link*> links;  // bank index -> host mirror
   ~DeviceMachine() {
     if (h) tmg_machine_destroy(h);
@@ -87,7 +86,9 @@ void download(const ClassBank& b, Link& l) {
   check(tmg_get_counters(dm.h, l.bank, l.counters.data()));
   check(tmg_get_include_masks(dm.h, l.bank, l.masks.data()));
   check(tmg_get_include_counts(dm.h, l.bank, l.counts.data()));
-  l.bound = static_cast<int>(dm.bound);
+  int64_t bound = 0;
+  check(tmg_bank_bound_examples(dm.h, l.bank, &bound));
+  l.bound = static_cast<int>(bound);
   l.prev.assign(static_cast<std::size_t>(b.clause_count()) * ((l.bound + 63) / 64), 0);
   if (!l.prev.empty()) check(tmg_get_prev_outputs(dm.h, l.bank, l.prev.data()));
   l.host_stale = false;
@@ -121,15 +122,6 @@ void make_device_cfg(const ClassBank& b, Link& l, const TMConfig& cfg) {
 
 // Pushes every dirty bank mirror of the machine to the device.
 void push_machine(detail::DeviceMachine& dm, const std::vector<const ClassBank*>& banks) {
-  int64_t want = dm.bound;
-  for (auto* l : dm.links)
-    if (l->prev_dirty) want = l->bound;
-  if (want != dm.bound) {
-    check(tmg_bind_examples(dm.h, want));  // machine-wide, zeroes every bank's bits
-    dm.bound = want;
-    for (auto* l : dm.links)
-      if (!l->host_stale && l->bound == want) l->prev_dirty = true;
-  }
   for (std::size_t k = 0; k < dm.links.size(); ++k) {
     Link* l = dm.links[k];
     (void)banks;
@@ -137,8 +129,11 @@ void push_machine(detail::DeviceMachine& dm, const std::vector<const ClassBank*>
       check(tmg_set_counters(dm.h, l->bank, l->counters.data()));
       l->counters_dirty = false;
     }
-    if (l->prev_dirty) {
-      if (l->bound == dm.bound && !l->prev.empty()) check(tmg_set_prev_outputs(dm.h, l->bank, l->prev.data()));
+    if (l->prev_dirty) {  // bind_examples is per bank (core.cpp:117-126): only this bank is rebound
+      int64_t bound = 0;
+      check(tmg_bank_bound_examples(dm.h, l->bank, &bound));
+      if (bound != l->bound) check(tmg_bind_bank(dm.h, l->bank, l->bound));
+      if (!l->prev.empty()) check(tmg_set_prev_outputs(dm.h, l->bank, l->prev.data()));
       l->prev_dirty = false;
     }
   }
@@ -160,11 +155,6 @@ detail::DeviceMachine& device_of(const MultiClassTM& tm) {
   return dm;
 }
 
-void sync_bound_after(detail::DeviceMachine& dm) {
-  tmg_machine_info info{};
-  check(tmg_machine_info_get(dm.h, &info));
-  dm.bound = info.bound_examples;
-}
 
 void push_pool(const ExamplePool& pool) {
   auto* dp = pool.device();
@@ -432,7 +422,6 @@ void refresh_tallies(ExamplePool& pool, std::span<ClassBank> banks) {  // pool.c
     throw std::invalid_argument("refresh_tallies expects all banks of one machine");
   push_pool(pool);
   check(tmg_refresh_tallies(dm.h, pool.device()->h));
-  sync_bound_after(dm);
   mark_stale(dm);
   pool_changed(pool);
 }
@@ -530,13 +519,16 @@ std::uint64_t update_clause(ClassBank& bank, int j, ExamplePool& pool, int class
                             std::span<const std::int32_t> order, std::int64_t offset, std::int64_t batch, int margin,
                             double s, bool boost_true_positive, Rng& rng) {
   auto& dm = device_of(bank);
+  // The engine keys the tally column and the target on the bank's own class
+  // (as every reference caller does, trainer.cpp:220); a different class_idx
+  // is rejected instead of silently ignored (tsetlin.py does the same).
+  if (class_idx != bank.link_->bank)
+    throw std::invalid_argument("update_clause: class_idx must be the bank's own class index");
   push_pool(pool);
   std::uint64_t events = 0;
   check(tmg_update_clause(dm.h, pool.device()->h, bank.link_->bank, j, order.empty() ? nullptr : order.data(),
                           static_cast<std::int64_t>(order.size()), offset, batch, margin, s,
                           boost_true_positive ? 1 : 0, rng.raw_state(), &events));
-  (void)class_idx;
-  sync_bound_after(dm);
   mark_stale(dm);
   pool_changed(pool);
   return events;
@@ -566,10 +558,10 @@ EpochReport train_epoch_parallel(MultiClassTM& tm, ExamplePool& pool, int worker
   rep.feedback_events.assign(static_cast<std::size_t>(tm.num_banks()), 0);
   tmg_epoch_report r{};
   r.feedback_events = rep.feedback_events.data();
-  check(tmg_train_epoch(dm.h, pool.device()->h, workers == 1 ? TMG_MODE_SYNC_MIRROR : TMG_MODE_ASYNC, workers, epoch,
-                        &r));
+  // TMG_MODE_AUTO: asynchronous for every `workers`; TSETLIN_DETERMINISTIC=1
+  // with workers == 1 selects the bit-exact single-worker replay.
+  check(tmg_train_epoch(dm.h, pool.device()->h, TMG_MODE_AUTO, workers, epoch, &r));
   rep.seconds = r.seconds;
-  sync_bound_after(dm);
   mark_stale(dm);
   pool_changed(pool);
   return rep;
@@ -677,10 +669,8 @@ EpochReport train_epoch_regress_parallel(RegressionHead& head, ExamplePool& pool
   rep.feedback_events.assign(1, 0);
   tmg_epoch_report r{};
   r.feedback_events = rep.feedback_events.data();
-  check(tmg_train_epoch_regress(dm.h, pool.device()->h, workers == 1 ? TMG_MODE_SYNC_MIRROR : TMG_MODE_ASYNC,
-                                workers, epoch, &r));
+  check(tmg_train_epoch_regress(dm.h, pool.device()->h, TMG_MODE_AUTO, workers, epoch, &r));
   rep.seconds = r.seconds;
-  sync_bound_after(dm);
   mark_stale(dm);
   pool_changed(pool);
   return rep;

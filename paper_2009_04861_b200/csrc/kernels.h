@@ -116,10 +116,12 @@ bool train_sequential_launch(const TrainParams& p, const SeqParams& sp, int B, c
 // Example-sliced class sums (eval.cu): included-literal lists per clause
 // against feature-major bit columns of the examples.
 struct BitsEvalParams {
-  const uint32_t* lit_t;     // [o + 1][Gs]: bit e of word g = x_f of example 32g + e; row o all ones
-  int64_t Gs;                // words per lit_t row (lit_t_stride(q))
-  const uint32_t* lists;     // concatenated literal lists, entry = f << 1 | negated, padded to 8 with o << 1
-  const int64_t* offs;       // [m*n_loc + 1] list offsets (multiples of 8)
+  const uint32_t* lit_t;     // [o + 2][Gs]: bit e of word g = x_f of example 32g + e; row o ones, o + 1 zeros
+  uint32_t Gs;               // words per lit_t row (lit_t_stride(q))
+  const uint32_t* lists;     // per clause: positive-literal features (padded to 4 with o), then
+                             // negated-literal features (padded to 4 with o + 1)
+  const int64_t* offs;       // [m*n_loc + 1] list offsets (multiples of 4)
+  const int32_t* npos;       // [m*n_loc] padded length of the positive part
   const int32_t* inc_count;  // [m*n_loc]
   uint32_t* prev;            // refresh mode: [m*n_loc][Wq]
   int32_t n_loc, j_begin, m, Wq;
@@ -141,9 +143,9 @@ bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out
                            unsigned long long* inc, unsigned long long* dec, cudaStream_t s);
 // Include counts, padded list lengths and offsets; returns the total list length (-1 on a CUDA error; syncs).
 int64_t build_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int32_t* inc_count,
-                           int32_t* lens, int64_t* offs, cudaStream_t s);
+                           int32_t* lens, int32_t* npos, int64_t* offs, cudaStream_t s);
 void fill_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int o, const int64_t* offs,
-                       uint32_t* lists, cudaStream_t s);
+                       const int32_t* npos, uint32_t* lists, cudaStream_t s);
 int64_t lit_t_stride(int64_t q);
 void transpose_literals_launch(const uint32_t* xplane, int64_t row_stride, int64_t q, int o, uint32_t* lit_t,
                                cudaStream_t s);

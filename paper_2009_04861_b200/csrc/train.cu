@@ -241,9 +241,13 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
       // bit an earlier step of the same pass writes. Only the stream is
       // serial: lane 0 draws each gate (trainer.cpp:121) and, on Type I, the
       // 2o draws.
-      for (int64_t t0 = 0; t0 < job.batch; t0 += 32) {
+      // A window never spans more than q steps: with batch > q (the
+      // reference's (offset + t) % q wraps) an example would otherwise meet
+      // two lanes of one window and both would see its stale tally and bit.
+      const int64_t win = q < 32 ? q : 32;
+      for (int64_t t0 = 0; t0 < job.batch; t0 += win) {
         const int64_t t = t0 + lane;
-        const int steps = static_cast<int>(job.batch - t0 < 32 ? job.batch - t0 : 32);
+        const int steps = static_cast<int>(job.batch - t0 < win ? job.batch - t0 : win);
         int64_t i = 0;
         int target = 0;
         double p = 0.0;

@@ -20,6 +20,7 @@ from ._capi import check, lib
 
 MODE_ASYNC = _capi.MODE_ASYNC
 MODE_SYNC_MIRROR = _capi.MODE_SYNC_MIRROR
+MODE_AUTO = _capi.MODE_AUTO
 TRAIN, PREDICT = _capi.EVAL_TRAIN, _capi.EVAL_PREDICT  # EvalMode (core.hpp:33-35)
 
 
@@ -236,7 +237,13 @@ class ClassBank:
         return int(self.include_counts()[j - self._tm.clause_begin])
 
     def bound_examples(self) -> int:
-        return self._tm.info().bound_examples
+        q = C.c_int64()
+        check(lib().tmg_bank_bound_examples(self._tm.handle, self._c, C.byref(q)))
+        return q.value
+
+    def bind_examples(self, q: int):
+        """ClassBank::bind_examples (core.cpp:117-126): this bank only."""
+        check(lib().tmg_bind_bank(self._tm.handle, self._c, q))
 
     def prev_outputs(self) -> np.ndarray:
         q = self.bound_examples()
@@ -321,12 +328,14 @@ class EpochReport:
 
 
 def train_epoch_parallel(tm: MultiClassTM, pool: ExamplePool, workers: int, epoch: int,
-                         mode: int = MODE_ASYNC) -> EpochReport:
+                         mode: int = MODE_AUTO) -> EpochReport:
     """train_epoch_parallel (trainer.cpp:181-242) on the GPU.
 
     mode=MODE_ASYNC runs Algorithm 1 over all clauses concurrently;
     mode=MODE_SYNC_MIRROR replays the reference's W-worker schedule with its
-    xoshiro streams (bit-exact for workers=1)."""
+    xoshiro streams (bit-exact for workers=1); MODE_AUTO (the default, as in
+    the C++ facade) is MODE_ASYNC unless workers == 1 and the environment sets
+    TSETLIN_DETERMINISTIC=1."""
     ev = np.zeros(tm.num_banks(), np.uint64)
     ev1 = np.zeros(tm.num_banks(), np.uint64)
     rep = _capi.EpochReportC(0, 0.0, 0.0, ev.ctypes.data_as(C.POINTER(C.c_uint64)),
@@ -595,7 +604,7 @@ def train_epoch_regress_sequential(head: RegressionHead, pool: ExamplePool, epoc
 
 
 def train_epoch_regress_parallel(head: RegressionHead, pool: ExamplePool, workers: int, epoch: int,
-                                 mode: int = MODE_ASYNC) -> EpochReport:
+                                 mode: int = MODE_AUTO) -> EpochReport:
     ev = np.zeros(1, np.uint64)
     ev1 = np.zeros(1, np.uint64)
     rep = _capi.EpochReportC(0, 0.0, 0.0, ev.ctypes.data_as(C.POINTER(C.c_uint64)),

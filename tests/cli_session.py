@@ -119,6 +119,9 @@ def run(binary, part="all", workdir=None):
         for cmd in cmds:
             env = dict(os.environ)
             env.pop("TM_THREADS", None)
+            # one-worker `--mode par` runs replay the reference schedule bit-exactly
+            # (TMG_MODE_AUTO); the reference binary ignores the variable
+            env["TSETLIN_DETERMINISTIC"] = "1"
             args = list(cmd)
             while args and args[0].startswith("@"):
                 k, v = args.pop(0)[1:].split("=", 1)

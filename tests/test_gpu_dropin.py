@@ -17,13 +17,18 @@ GPU_DRIVER = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "api_driver_gpu
 REF_DRIVER = os.path.join(REPO, "oracle", "_ref", "api_driver_ref")
 
 
+DET_ENV = dict(os.environ, TSETLIN_DETERMINISTIC="1")
+
+
 def _lines(text):
     return [l for l in text.splitlines() if l.strip()]
 
 
 def test_same_source_driver_matches_reference():
     assert os.path.exists(GPU_DRIVER), "build first (make -C paper_2009_04861_b200/csrc)"
-    gpu = subprocess.run([GPU_DRIVER], capture_output=True, text=True, timeout=600)
+    # the transcript includes one-worker train_epoch_parallel epochs: the
+    # bit-exact replay is selected by TSETLIN_DETERMINISTIC=1 (TMG_MODE_AUTO)
+    gpu = subprocess.run([GPU_DRIVER], capture_output=True, text=True, timeout=600, env=DET_ENV)
     assert gpu.returncode == 0, gpu.stderr
     want = _lines(open(os.path.join(GOLDEN, "api_driver_ref.txt")).read())
     if os.path.exists(REF_DRIVER):  # the live reference binary, when it travelled
@@ -38,7 +43,7 @@ def test_same_source_bench_sweep_matches_reference():
     "bench" (seq and one-worker par, classification and regression) prints the
     reference's records (seconds excluded) line for line."""
     drv = os.path.join(REPO, "paper_2009_04861_b200", "_lib", "data_driver_gpu")
-    out = subprocess.run([drv, "bench"], capture_output=True, text=True, timeout=600)
+    out = subprocess.run([drv, "bench"], capture_output=True, text=True, timeout=600, env=DET_ENV)
     assert out.returncode == 0, out.stderr
     want = _lines(open(os.path.join(GOLDEN, "data_driver_bench_ref.txt")).read())
     got = _lines(out.stdout)

@@ -128,6 +128,33 @@ def test_sync_mirror_epochs_bit_exact(name):
     _check_state(d, "refreshed", tm, pool, man["m"])
 
 
+def test_auto_mode_rule(monkeypatch):
+    """TMG_MODE_AUTO, the mode of the drop-in train_epoch_parallel in Python
+    and in the C++ facade: asynchronous for any worker count; the bit-exact
+    one-worker replay only with TSETLIN_DETERMINISTIC=1."""
+    name = EPOCH_CASES[0]
+    d = ("epoch_par_w1", name)
+    man = manifest(*d)
+    ep = man["epochs"][0]
+
+    def run():
+        pool = T.ExamplePool(man["o"], load(*d, "train_x.npy"), load(*d, "train_y.npy"), man["m"])
+        cfg = T.TMConfig(clauses=man["n"], margin=man["margin"], specificity=man["s"], state_depth=man["N"],
+                         boost_true_positive=bool(man["boost"]), seed=man["seed"])
+        tm = T.MultiClassTM(cfg, man["o"], man["m"])
+        return T.train_epoch_parallel(tm, pool, 1, ep["epoch"]), tm
+
+    monkeypatch.delenv("TSETLIN_DETERMINISTIC", raising=False)
+    rep, _ = run()
+    assert sum(rep.type_i_events) > 0  # only the asynchronous engine reports Type I counts
+    monkeypatch.setenv("TSETLIN_DETERMINISTIC", "1")
+    rep, tm = run()
+    assert rep.feedback_events == ep["feedback_events"] and sum(rep.type_i_events) == 0
+    counters = load(*d, f"epoch{ep['epoch']}_counters.npy")
+    for c in range(man["m"]):
+        assert np.array_equal(tm.banks[c].counters(), counters[c])
+
+
 @pytest.mark.parametrize("name,o,m,n", [("mnist_rand", 784, 10, 50), ("single_bank", 30, 1, 8),
                                         ("dense_o64", 64, 3, 12)])
 def test_inference_random_states(name, o, m, n):
@@ -185,6 +212,38 @@ def test_errors_follow_reference():
     with pytest.raises(IndexError):
         tm.banks[0].set_counters  # accessor exists
         T.update_clause(tm.banks[1], 9, pool2, 1, None, 0, 1, 15, 3.0, False, T.Rng(1))
+
+
+def test_update_clause_rejects_order_entries_out_of_range():
+    """record_output_and_tally's bounds check (pool.cpp:95-98) -> out_of_range,
+    raised before anything is written on the device."""
+    tm = T.MultiClassTM(T.TMConfig(clauses=4), 12, 2)
+    pool = T.ExamplePool(12, np.ones((4, 12), np.uint8), np.zeros(4, np.int32), 2)
+    before = tm.banks[0].counters()
+    for bad in ([0, 1, 2, 4], [0, -1, 2, 3]):
+        with pytest.raises(IndexError, match="out of range"):
+            T.update_clause(tm.banks[0], 0, pool, 0, bad, 0, 4, 15, 3.0, False, T.Rng(1))
+    assert np.array_equal(tm.banks[0].counters(), before)
+    assert not pool.tallies().any()
+
+
+def test_update_clause_rebinds_only_its_bank():
+    """update_clause rebinds the bank it updates (trainer.cpp:107); the other
+    banks keep their bound count and previous outputs (core.cpp:117-126)."""
+    tm = T.MultiClassTM(T.TMConfig(clauses=4, margin=15, specificity=3.0), 12, 2)
+    small = T.ExamplePool(12, np.ones((10, 12), np.uint8), np.zeros(10, np.int32), 2)
+    T.train_epoch_parallel(tm, small, 1, 0, mode=T.MODE_SYNC_MIRROR)
+    prev0 = tm.banks[0].prev_outputs()
+    assert tm.banks[0].bound_examples() == 10 and tm.banks[1].bound_examples() == 10
+    big = T.ExamplePool(12, np.ones((100, 12), np.uint8), np.ones(100, np.int32), 2)
+    T.update_clause(tm.banks[1], 1, big, 1, None, 0, 5, 15, 3.0, False, T.Rng(3))
+    assert tm.banks[0].bound_examples() == 10 and tm.banks[1].bound_examples() == 100
+    assert np.array_equal(tm.banks[0].prev_outputs(), prev0)
+    assert tm.banks[1].prev_outputs().shape == (4, 2)
+    assert tm.info().bound_examples == -1
+    tm.banks[0].bind_examples(100)  # per bank again
+    assert tm.banks[0].bound_examples() == 100 and not tm.banks[0].prev_outputs().any()
+    assert tm.info().bound_examples == 100
 
 
 @pytest.mark.parametrize("kind,q,n", [("mnist", 60, 200), ("imdb", 12, 60), ("xor", 300, 20), ("fmnist", 20, 100)])
