@@ -219,6 +219,48 @@ int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t worke
  * xoshiro stream serial). feedback_events: num_classes entries. */
 int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, double* seconds,
                                uint64_t* feedback_events);
+/* ---- clause-sharded machines (the reference's W worker
+ * threads sharing atomic tallies inside one train_epoch_parallel call,
+ * trainer.cpp:210-231, pool.hpp:57-59, spread over GPUs).
+ *
+ * One process, several GPUs: tmg_machine_create_devices splits the clause
+ * pairs of every class evenly over `devices` (repeats allowed: several shards
+ * on one GPU). The handle is used like any machine: counters, include masks,
+ * previous outputs, binding, tmg_train_epoch (TMG_MODE_ASYNC / AUTO),
+ * tmg_refresh_tallies, class sums and predictions cover the whole machine;
+ * calls that replay the reference's serial streams (sequential trainer,
+ * update_clause, feedback, the W = 1 replay, regression) need one device and
+ * fail with TMG_EINVAL. An epoch runs every shard's kernel on its own device
+ * and exchanges tally deltas every window (tmg_machine_set_windows, default
+ * 16) on side streams, overlapped with the next window: NCCL all-reduce when
+ * the devices are distinct and libnccl.so.2 loads (TSETLIN_EXCHANGE=peer
+ * forces the other path), else a peer-memory reduction kernel. Pools are
+ * replicated to the shards' devices on first use. ndev == 1 creates a plain
+ * machine. */
+int tmg_machine_create_devices(const tmg_config* cfg, int32_t o, int32_t m, const int32_t* devices, int32_t ndev,
+                               tmg_machine** out);
+int tmg_machine_set_windows(tmg_machine* tm, int32_t windows);
+/* Tallies of the pool's replica for shard k of the last sharded machine that
+ * used it (q x m int32; test hook: every replica holds the same tallies). */
+int tmg_pool_replica_tallies(const tmg_pool* pool, int32_t k, int32_t* out);
+/* shards held (group) or ranks (communicator); whether the exchange uses NCCL. */
+int tmg_machine_exchange_info(const tmg_machine* tm, int32_t* shards, int32_t* uses_nccl);
+/* 1 when libnccl.so.2 could be loaded; else 0 and the reason in `why`. */
+int tmg_nccl_available(char* why, int32_t len);
+/* One process per GPU: rank 0 makes a 128-byte NCCL id, the caller sends it
+ * to every rank, each rank creates its communicator on its device and
+ * attaches it to its shard (tmg_machine_create_shard with the even-aligned
+ * slice of its rank). tmg_train_epoch then trains this rank's clauses with
+ * the windowed exchange over NCCL and reports every rank's feedback events;
+ * tmg_class_sums / tmg_predict / tmg_refresh_tallies return whole-machine
+ * results on every rank. These calls are collective: every rank makes them
+ * in the same order with the same arguments. Attach NULL to detach. */
+typedef struct tmg_comm tmg_comm;
+int tmg_comm_unique_id(unsigned char* id128);
+int tmg_comm_create(const unsigned char* id128, int32_t nranks, int32_t rank, int32_t device, tmg_comm** out);
+int tmg_comm_destroy(tmg_comm* comm);
+int tmg_machine_attach_comm(tmg_machine* tm, tmg_comm* comm);
+
 /* Multi-GPU building blocks: one asynchronous window [t_begin, t_end) of every
  * clause's pass of `epoch`. Deltas are also accumulated in the pool's delta
  * buffer; after an allreduce of that buffer call tmg_pool_apply_reduced. */

@@ -14,9 +14,9 @@ from . import _capi as _capi_mod
 _capi_mod.lib()  # fail loudly at import when the CUDA engine is missing
 
 from .model_io import load_model_file, save_model_file  # noqa: E402
-from .tsetlin import (MODE_ASYNC, MODE_AUTO, MODE_SYNC_MIRROR, PREDICT, TRAIN, ClassBank, EpochReport,  # noqa: E402
+from .tsetlin import (MODE_ASYNC, MODE_AUTO, MODE_SYNC_MIRROR, PREDICT, TRAIN, ClassBank, Comm, EpochReport,  # noqa: E402
                       ExamplePool, MultiClassTM, RegressionHead, Rng, TMConfig, class_sums, classify,
-                      device_count, epoch_order, evaluate_accuracy, evaluate_clause, evaluate_scaled_mae,
+                      device_count, epoch_order, evaluate_accuracy, nccl_available, evaluate_clause, evaluate_scaled_mae,
                       export_vote_sums, feedback_rates, literal_words, predict_all, predict_literals,
                       predict_regress, predict_scaled, predict_scaled_all, refresh_tallies,
                       train_epoch_parallel, train_epoch_regress_parallel, train_epoch_regress_sequential,
@@ -24,9 +24,9 @@ from .tsetlin import (MODE_ASYNC, MODE_AUTO, MODE_SYNC_MIRROR, PREDICT, TRAIN, C
                       update_regress, vote_sum)
 
 __all__ = [
-    "MODE_ASYNC", "MODE_AUTO", "MODE_SYNC_MIRROR", "PREDICT", "TRAIN", "ClassBank", "EpochReport",
+    "MODE_ASYNC", "MODE_AUTO", "MODE_SYNC_MIRROR", "PREDICT", "TRAIN", "ClassBank", "Comm", "EpochReport",
     "ExamplePool", "MultiClassTM", "RegressionHead", "Rng", "TMConfig", "class_sums", "classify",
-    "device_count", "epoch_order", "evaluate_accuracy", "evaluate_clause", "evaluate_scaled_mae",
+    "device_count", "epoch_order", "evaluate_accuracy", "nccl_available", "evaluate_clause", "evaluate_scaled_mae",
     "export_vote_sums", "feedback_rates", "literal_words", "load_model_file", "predict_all",
     "predict_literals", "predict_regress", "predict_scaled", "predict_scaled_all", "refresh_tallies",
     "save_model_file", "train_epoch_parallel", "train_epoch_regress_parallel",

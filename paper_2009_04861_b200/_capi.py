@@ -73,6 +73,15 @@ SIGNATURES = {
     "tmg_get_include_counts": (C.c_int, [P, I32, P]),
     "tmg_bind_examples": (C.c_int, [P, I64]),
     "tmg_bind_bank": (C.c_int, [P, I32, I64]),
+    "tmg_machine_create_devices": (C.c_int, [P, I32, I32, P, I32, P]),
+    "tmg_machine_set_windows": (C.c_int, [P, I32]),
+    "tmg_pool_replica_tallies": (C.c_int, [P, I32, P]),
+    "tmg_machine_exchange_info": (C.c_int, [P, P, P]),
+    "tmg_nccl_available": (C.c_int, [P, I32]),
+    "tmg_comm_unique_id": (C.c_int, [P]),
+    "tmg_comm_create": (C.c_int, [P, I32, I32, I32, P]),
+    "tmg_comm_destroy": (C.c_int, [P]),
+    "tmg_machine_attach_comm": (C.c_int, [P, P]),
     "tmg_bank_bound_examples": (C.c_int, [P, I32, P]),
     "tmg_get_prev_outputs": (C.c_int, [P, I32, P]),
     "tmg_set_prev_outputs": (C.c_int, [P, I32, P]),

@@ -668,6 +668,7 @@ TMG_API int tmg_machine_create_shard(const tmg_config* cfg, int32_t o, int32_t m
 
 TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   if (!tm) return TMG_OK;
+  if (is_group(tm) || tm->owns_xchg) destroy_group(tm);
   int prev = -1;
   cudaGetDevice(&prev);
   cudaSetDevice(tm->device);
@@ -694,6 +695,7 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
 }
 
 TMG_API int tmg_machine_info_get(const tmg_machine* tm, tmg_machine_info* info) {
+  if (is_group(tm)) return group_info(tm, info);
   return guarded([&] {
     M(tm);
     info->feature_count = tm->o;
@@ -716,6 +718,7 @@ TMG_API int tmg_machine_config(const tmg_machine* tm, tmg_config* cfg) {
 }
 
 TMG_API int tmg_machine_reset(tmg_machine* tm) {
+  if (is_group(tm)) return group_reset(tm);
   return guarded([&] {
     DeviceGuard dg(M(tm)->device);
     reset_state(tm);
@@ -723,6 +726,7 @@ TMG_API int tmg_machine_reset(tmg_machine* tm) {
 }
 
 TMG_API int tmg_get_counters(const tmg_machine* ctm, int32_t bank, uint16_t* out) {
+  if (is_group(ctm)) return group_counters(ctm, bank, out, nullptr);
   return guarded([&] {
     auto tm = const_cast<tmg_machine*>(M(ctm));
     check_bank(tm, bank);
@@ -738,6 +742,7 @@ TMG_API int tmg_get_counters(const tmg_machine* ctm, int32_t bank, uint16_t* out
 }
 
 TMG_API int tmg_set_counters(tmg_machine* tm, int32_t bank, const uint16_t* in) {
+  if (is_group(tm)) return group_counters(tm, bank, nullptr, in);
   return guarded([&] {
     check_bank(M(tm), bank);
     DeviceGuard dg(tm->device);
@@ -774,6 +779,7 @@ std::vector<uint32_t> top_planes(tmg_machine* tm, int32_t bank) {
 }  // namespace
 
 TMG_API int tmg_get_include_masks(const tmg_machine* ctm, int32_t bank, uint64_t* out) {
+  if (is_group(ctm)) return group_include(ctm, bank, out, nullptr);
   return guarded([&] {
     auto tm = const_cast<tmg_machine*>(M(ctm));
     check_bank(tm, bank);
@@ -795,6 +801,7 @@ TMG_API int tmg_get_include_masks(const tmg_machine* ctm, int32_t bank, uint64_t
 }
 
 TMG_API int tmg_get_include_counts(const tmg_machine* ctm, int32_t bank, int32_t* out) {
+  if (is_group(ctm)) return group_include(ctm, bank, nullptr, out);
   return guarded([&] {
     auto tm = const_cast<tmg_machine*>(M(ctm));
     check_bank(tm, bank);
@@ -807,6 +814,7 @@ TMG_API int tmg_get_include_counts(const tmg_machine* ctm, int32_t bank, int32_t
 }
 
 TMG_API int tmg_bind_examples(tmg_machine* tm, int64_t q) {
+  if (is_group(tm)) return group_bind(tm, -1, q);
   return guarded([&] {
     DeviceGuard dg(M(tm)->device);
     bind(tm, q);
@@ -814,6 +822,7 @@ TMG_API int tmg_bind_examples(tmg_machine* tm, int64_t q) {
 }
 
 TMG_API int tmg_bind_bank(tmg_machine* tm, int32_t bank, int64_t q) {
+  if (is_group(tm)) return group_bind(tm, bank, q);
   return guarded([&] {
     check_bank(M(tm), bank);
     DeviceGuard dg(tm->device);
@@ -822,6 +831,7 @@ TMG_API int tmg_bind_bank(tmg_machine* tm, int32_t bank, int64_t q) {
 }
 
 TMG_API int tmg_bank_bound_examples(const tmg_machine* tm, int32_t bank, int64_t* q) {
+  if (is_group(tm)) return tmg_bank_bound_examples(tm->parts[0], bank, q);
   return guarded([&] {
     check_bank(M(tm), bank);
     *q = tm->bank_q[static_cast<size_t>(bank)];
@@ -831,6 +841,7 @@ TMG_API int tmg_bank_bound_examples(const tmg_machine* tm, int32_t bank, int64_t
 // Previous outputs of one bank in the reference layout: per clause
 // ceil(bound/64) u64 words (the device rows are Wq u32 words apart).
 TMG_API int tmg_get_prev_outputs(const tmg_machine* ctm, int32_t bank, uint64_t* out) {
+  if (is_group(ctm)) return group_prev(ctm, bank, out, nullptr);
   return guarded([&] {
     auto tm = const_cast<tmg_machine*>(M(ctm));
     check_bank(tm, bank);
@@ -845,6 +856,7 @@ TMG_API int tmg_get_prev_outputs(const tmg_machine* ctm, int32_t bank, uint64_t*
 }
 
 TMG_API int tmg_set_prev_outputs(tmg_machine* tm, int32_t bank, const uint64_t* in) {
+  if (is_group(tm)) return group_prev(tm, bank, nullptr, in);
   return guarded([&] {
     check_bank(M(tm), bank);
     DeviceGuard dg(tm->device);
@@ -907,6 +919,7 @@ TMG_API int tmg_pool_destroy(tmg_pool* pool) {
   cudaSetDevice(pool->device);
   if (pool->stream) cudaStreamSynchronize(pool->stream);
   pool->close_peers();
+  destroy_replicas(pool);
   pool->rows.release();
   pool->labels.release();
   pool->tallies.release();
@@ -1060,6 +1073,7 @@ TMG_API int tmg_pool_apply_reduced(tmg_pool* pool, const void* d_reduced) {
 
 TMG_API int tmg_epoch_begin(tmg_machine* tm, tmg_pool* pool, int32_t epoch) {
   return guarded([&] {
+    need_single(tm, "tmg_epoch_begin");
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
     bind_for(tm, pool->q);
@@ -1071,6 +1085,7 @@ TMG_API int tmg_epoch_begin(tmg_machine* tm, tmg_pool* pool, int32_t epoch) {
 
 TMG_API int tmg_train_window_async(tmg_machine* tm, tmg_pool* pool, int32_t epoch, int64_t t0, int64_t t1) {
   return guarded([&] {
+    need_single(tm, "tmg_train_window_async");
     check_compatible(M(tm), pool);
     if (tm->cur_epoch != epoch || tm->q_bound != pool->q) fail(TMG_EINVAL, "call tmg_epoch_begin first");
     if (t0 < 0 || t1 > pool->q || t0 > t1) fail(TMG_ERANGE, "window outside [0, q]");
@@ -1081,6 +1096,7 @@ TMG_API int tmg_train_window_async(tmg_machine* tm, tmg_pool* pool, int32_t epoc
 
 TMG_API int tmg_window_delta_snapshot(tmg_machine* tm, tmg_pool* pool, void* d_snapshot) {
   return guarded([&] {
+    need_single(tm, "tmg_window_delta_snapshot");
     check_compatible(M(tm), pool);
     if (!d_snapshot) fail(TMG_EINVAL, "null snapshot buffer");
     DeviceGuard dg(tm->device);
@@ -1091,6 +1107,7 @@ TMG_API int tmg_window_delta_snapshot(tmg_machine* tm, tmg_pool* pool, void* d_s
 
 TMG_API int tmg_window_apply_remote(tmg_machine* tm, tmg_pool* pool, const void* d_reduced, const void* d_snapshot) {
   return guarded([&] {
+    need_single(tm, "tmg_window_apply_remote");
     check_compatible(M(tm), pool);
     if (!d_reduced || !d_snapshot) fail(TMG_EINVAL, "null buffer");
     DeviceGuard dg(tm->device);
@@ -1102,6 +1119,7 @@ TMG_API int tmg_window_apply_remote(tmg_machine* tm, tmg_pool* pool, const void*
 
 TMG_API int tmg_epoch_events(tmg_machine* tm, uint64_t* feedback_events) {
   return guarded([&] {
+    need_single(tm, "tmg_epoch_events");
     DeviceGuard dg(M(tm)->device);
     std::vector<unsigned long long> ev(2 * static_cast<size_t>(tm->m));
     CK(cudaMemcpyAsync(ev.data(), tm->events.ptr, tm->events.bytes(), cudaMemcpyDeviceToHost, tm->stream));
@@ -1114,6 +1132,7 @@ TMG_API int tmg_epoch_events(tmg_machine* tm, uint64_t* feedback_events) {
 TMG_API int tmg_train_window(tmg_machine* tm, tmg_pool* pool, int32_t epoch, int64_t t0, int64_t t1,
                              uint64_t* feedback_events) {
   return guarded([&] {
+    need_single(tm, "tmg_train_window");
     check_compatible(M(tm), pool);
     if (tm->cur_epoch != epoch || tm->q_bound != pool->q) fail(TMG_EINVAL, "call tmg_epoch_begin first");
     if (t0 < 0 || t1 > pool->q || t0 > t1) fail(TMG_ERANGE, "window outside [0, q]");
@@ -1133,6 +1152,7 @@ static int train_epoch_impl(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32
 
 TMG_API int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
                             tmg_epoch_report* report) {
+  if (is_sharded(tm)) return group_train_epoch(tm, pool, mode, workers, epoch, report);
   if (tm && tm->all_positive) {
     g_last_error = "regression machine: use tmg_train_epoch_regress";
     return TMG_EINVAL;
@@ -1142,6 +1162,10 @@ TMG_API int tmg_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32
 
 TMG_API int tmg_train_epoch_regress(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
                                     tmg_epoch_report* report) {
+  if (is_sharded(tm)) {
+    g_last_error = "train_epoch_regress_parallel needs a single-device machine";
+    return TMG_EINVAL;
+  }
   // train_epoch_regress_parallel (regression.cpp:163-227)
   if (!tm || !tm->all_positive) {
     g_last_error = "not a regression machine (create it with tmg_machine_create_regress)";
@@ -1247,6 +1271,10 @@ static int train_epoch_impl(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32
 
 TMG_API int tmg_train_epoch_regress_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, double* seconds,
                                                uint64_t* feedback_events) {
+  if (is_sharded(tm)) {
+    g_last_error = "train_epoch_regress_sequential needs a single-device machine";
+    return TMG_EINVAL;
+  }
   // train_epoch_regress_sequential (regression.cpp:125-161)
   if (!tm || !tm->all_positive) {
     g_last_error = "not a regression machine (create it with tmg_machine_create_regress)";
@@ -1261,6 +1289,7 @@ TMG_API int tmg_train_epoch_regress_sequential(tmg_machine* tm, tmg_pool* pool, 
 TMG_API int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, double* seconds,
                                        uint64_t* feedback_events) {
   return guarded([&] {
+    need_single(tm, "train_epoch_sequential");
     if (tm && tm->regress_mode) {
       if (!pool || tm->o != pool->o) fail(TMG_EINVAL, "head/pool feature count mismatch");
       if (tm->device != pool->device) fail(TMG_EINVAL, "model and pool live on different devices");
@@ -1309,6 +1338,7 @@ TMG_API int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t 
 TMG_API int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
                                      int32_t clause_output, uint32_t trials, uint64_t* inc, uint64_t* dec) {
   return guarded([&] {
+    need_single(tm, "tmg_debug_feedback_rates");
     check_bank(M(tm), bank);
     if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
     DeviceGuard dg(tm->device);
@@ -1348,6 +1378,7 @@ TMG_API int tmg_debug_feedback_rates(tmg_machine* tm, int32_t bank, int32_t j, c
 TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
                                    int32_t clause_output, uint32_t example, int32_t epoch) {
   return guarded([&] {
+    need_single(tm, "tmg_debug_type_i_async");
     check_bank(M(tm), bank);
     if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
     if (!literals) fail(TMG_EINVAL, "null literal row");
@@ -1384,6 +1415,7 @@ TMG_API int tmg_debug_type_i_async(tmg_machine* tm, int32_t bank, int32_t j, con
 
 TMG_API int tmg_debug_counters(tmg_machine* tm, uint64_t* out, int32_t count, int32_t reset) {
   return guarded([&] {
+    need_single(tm, "tmg_debug_counters");
     M(tm);
     if (count < 0 || count > tmg::kDebugCounters) fail(TMG_EINVAL, "counter count out of range");
     DeviceGuard dg(tm->device);
@@ -1405,6 +1437,7 @@ TMG_API unsigned long long tmg_kernel_launches(void) {
 }
 
 TMG_API int tmg_machine_stream(tmg_machine* tm, void** stream) {
+  if (is_group(tm)) return tmg_machine_stream(tm->parts[0], stream);
   return guarded([&] { *stream = M(tm)->stream; });
 }
 
@@ -1421,6 +1454,8 @@ TMG_API int tmg_bench_int_peak(int32_t device, double* lop3_ops_per_s, double* m
 TMG_API int tmg_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t c, int32_t j, const int32_t* order,
                               int64_t order_len, int64_t offset, int64_t batch, int32_t margin, double s,
                               int32_t boost, uint64_t* rng_state, uint64_t* events) {
+  if (is_group(tm))
+    return group_update_clause(tm, pool, c, j, order, order_len, offset, batch, margin, s, boost, rng_state, events);
   return guarded([&] {
     check_compatible(M(tm), pool);
     if (batch < 1) fail(TMG_EINVAL, "batch must be >= 1");  // trainer.cpp:106
@@ -1476,6 +1511,11 @@ TMG_API int tmg_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t c, int32_
 
 TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals, int32_t type,
                          double s, int32_t boost, int32_t clause_output, uint64_t* rng_state) {
+  if (is_group(tm)) {  // the shard that owns clause j
+    tmg_machine* part = group_owner(tm, j);
+    if (!part) return guarded([&] { fail(TMG_ERANGE, "clause index outside this machine"); });
+    return tmg_feedback(part, bank, j, literals, type, s, boost, clause_output, rng_state);
+  }
   return guarded([&] {
     check_bank(M(tm), bank);
     if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
@@ -1538,6 +1578,11 @@ TMG_API int tmg_feedback(tmg_machine* tm, int32_t bank, int32_t j, const uint64_
 
 TMG_API int tmg_evaluate_clause(tmg_machine* tm, int32_t bank, int32_t j, const uint64_t* literals,
                                 int32_t mode, int32_t* out) {
+  if (is_group(tm)) {
+    tmg_machine* part = group_owner(tm, j);
+    if (!part) return guarded([&] { fail(TMG_ERANGE, "clause index outside this machine"); });
+    return tmg_evaluate_clause(part, bank, j, literals, mode, out);
+  }
   return guarded([&] {
     check_bank(M(tm), bank);
     if (j < tm->j_begin || j >= tm->j_end) fail(TMG_ERANGE, "clause index outside this machine");
@@ -1563,6 +1608,11 @@ TMG_API int tmg_evaluate_clause(tmg_machine* tm, int32_t bank, int32_t j, const 
 // ------------------------------------------------------------- inference ---
 
 TMG_API int tmg_refresh_tallies(tmg_machine* tm, tmg_pool* pool) {
+  if (is_sharded(tm)) {  // sums over every shard; each shard rewrites its previous outputs
+    if (!pool || !tm) return guarded([&] { fail(TMG_EINVAL, "null handle"); });
+    std::vector<int32_t> sums(static_cast<size_t>(pool->q) * tm->m);
+    return group_class_sums(tm, pool, nullptr, 0, TMG_EVAL_TRAIN, sums.data(), true);
+  }
   return guarded([&] {
     check_compatible(M(tm), pool);
     if (tm->n_loc != tm->n)  // a shard's sums are partial: the pool's replicated tallies would be wrong
@@ -1575,6 +1625,16 @@ TMG_API int tmg_refresh_tallies(tmg_machine* tm, tmg_pool* pool) {
 }
 
 TMG_API int tmg_class_sums_device(tmg_machine* tm, const tmg_pool* pool, int32_t mode, int32_t* d_sums) {
+  if (is_sharded(tm)) {
+    if (!pool || !tm) return guarded([&] { fail(TMG_EINVAL, "null handle"); });
+    std::vector<int32_t> sums(static_cast<size_t>(pool->q) * tm->m);
+    const int rc = group_class_sums(tm, pool, nullptr, 0, mode, sums.data(), false);
+    if (rc != TMG_OK) return rc;
+    return guarded([&] {
+      DeviceGuard dg(tm->device);
+      CK(cudaMemcpy(d_sums, sums.data(), sums.size() * 4, cudaMemcpyHostToDevice));
+    });
+  }
   return guarded([&] {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
@@ -1584,6 +1644,7 @@ TMG_API int tmg_class_sums_device(tmg_machine* tm, const tmg_pool* pool, int32_t
 }
 
 TMG_API int tmg_class_sums(tmg_machine* tm, const tmg_pool* pool, int32_t mode, int32_t* out) {
+  if (is_sharded(tm)) return group_class_sums(tm, pool, nullptr, 0, mode, out, false);
   return guarded([&] {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
@@ -1596,7 +1657,30 @@ TMG_API int tmg_class_sums(tmg_machine* tm, const tmg_pool* pool, int32_t mode, 
   });
 }
 
+namespace {
+void argmax_host(const int32_t* sums, int64_t q, int m, int32_t* pred) {  // classify, trainer.cpp:244-260
+  for (int64_t i = 0; i < q; ++i) {
+    const int32_t* row = sums + i * m;
+    if (m == 1) {
+      pred[i] = row[0] >= 0 ? 1 : 0;
+      continue;
+    }
+    int best = 0;
+    for (int c = 1; c < m; ++c)
+      if (row[c] > row[best]) best = c;
+    pred[i] = best;
+  }
+}
+}  // namespace
+
 TMG_API int tmg_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
+  if (is_sharded(tm)) {
+    if (!pool || !tm) return guarded([&] { fail(TMG_EINVAL, "null handle"); });
+    std::vector<int32_t> sums(static_cast<size_t>(pool->q) * tm->m);
+    const int rc = group_class_sums(tm, pool, nullptr, 0, TMG_EVAL_PREDICT, sums.data(), false);
+    if (rc == TMG_OK) argmax_host(sums.data(), pool->q, tm->m, out);
+    return rc;
+  }
   return guarded([&] {
     check_compatible(M(tm), pool);
     DeviceGuard dg(tm->device);
@@ -1611,7 +1695,7 @@ TMG_API int tmg_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
   });
 }
 
-namespace {
+namespace tmgx {
 void literals_to_planes(tmg_machine* tm, const uint64_t* lits, int64_t q, DevBuf<uint32_t>& xs) {
   const int W64 = (2 * tm->o + 63) / 64;
   DevBuf<uint64_t> dl;
@@ -1622,9 +1706,10 @@ void literals_to_planes(tmg_machine* tm, const uint64_t* lits, int64_t q, DevBuf
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(tm->stream));
 }
-}  // namespace
+}  // namespace tmgx
 
 TMG_API int tmg_class_sums_literals(tmg_machine* tm, const uint64_t* lits, int64_t q, int32_t mode, int32_t* out) {
+  if (is_sharded(tm)) return group_class_sums(tm, nullptr, lits, q, mode, out, false);
   return guarded([&] {
     M(tm);
     if (q <= 0) return;
@@ -1639,6 +1724,13 @@ TMG_API int tmg_class_sums_literals(tmg_machine* tm, const uint64_t* lits, int64
 }
 
 TMG_API int tmg_predict_literals(tmg_machine* tm, const uint64_t* lits, int64_t q, int32_t* out) {
+  if (is_sharded(tm)) {
+    if (q <= 0) return TMG_OK;
+    std::vector<int32_t> sums(static_cast<size_t>(q) * tm->m);
+    const int rc = group_class_sums(tm, nullptr, lits, q, TMG_EVAL_PREDICT, sums.data(), false);
+    if (rc == TMG_OK) argmax_host(sums.data(), q, tm->m, out);
+    return rc;
+  }
   return guarded([&] {
     M(tm);
     if (q <= 0) return;
@@ -1680,6 +1772,7 @@ void regress_predict_planes(tmg_machine* tm, const uint32_t* xs, int64_t q, int3
 TMG_API int tmg_regress_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* out) {
   // predict_scaled over a pool (regression.cpp:86-93)
   return guarded([&] {
+    need_single(tm, "predict_scaled");
     if (!M(tm) || !pool || tm->o != pool->o) fail(TMG_EINVAL, "head/pool feature count mismatch");
     DeviceGuard dg(tm->device);
     regress_predict_planes(tm, pool->xplane(), pool->q, out, pool_lit_t(tm, pool));
@@ -1688,6 +1781,7 @@ TMG_API int tmg_regress_predict(tmg_machine* tm, const tmg_pool* pool, int32_t* 
 
 TMG_API int tmg_regress_predict_literals(tmg_machine* tm, const uint64_t* lits, int64_t q, int32_t* out) {
   return guarded([&] {
+    need_single(tm, "predict_scaled");
     M(tm);
     if (q <= 0) return;
     DeviceGuard dg(tm->device);

@@ -141,6 +141,10 @@ struct tmg_pool {
   // Tally replicas of the other ranks (multi-GPU over peer memory): every
   // tally change is also added into each of them by the training kernels.
   std::vector<int32_t*> peers;
+  // Sharded machines (group.cu): one tally replica per shard (replicas[k]
+  // may be this pool itself); a replica points back at its primary.
+  std::vector<tmg_pool*> replicas;
+  tmg_pool* primary = nullptr;
   void close_peers() {
     for (int32_t* p : peers) cudaIpcCloseMemHandle(p);
     peers.clear();
@@ -176,6 +180,13 @@ struct tmg_machine {
   uint32_t key0 = 0, key1 = 0;
   int all_positive = 0;  // regression head bank (PolarityScheme::AllPositive)
   bool regress_mode = false;  // current call trains the regression head
+  // Sharded machine (group.cu): clause shards on devices of this process
+  // (parts non-empty: this handle owns no device state itself), or a shard
+  // of a multi-process machine attached to a communicator (xchg, parts empty).
+  std::vector<tmg_machine*> parts;
+  tmgx::Exchange* xchg = nullptr;
+  bool owns_xchg = false;
+  int windows = 16;  // tally-exchange windows per sharded epoch
   int clauses() const { return m * n_loc; }
 };
 
@@ -196,7 +207,32 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
 void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool train_mode, int32_t* d_out,
                        uint32_t* prev, const uint32_t* lit_t = nullptr);
 const uint32_t* pool_lit_t(tmg_machine* tm, const tmg_pool* pool);
+void literals_to_planes(tmg_machine* tm, const uint64_t* lits, int64_t q, DevBuf<uint32_t>& xs);
 tmg_pool* create_pool_common(int device, int o, int64_t q, int m);
 int32_t resolve_mode(int32_t mode, int32_t workers);
+
+// group.cu — sharded machines. The group_* entry points implement the ABI
+// call of the same name for a machine with parts (or an attached comm).
+inline bool is_group(const tmg_machine* tm) { return tm && !tm->parts.empty(); }
+inline bool is_sharded(const tmg_machine* tm) { return tm && (!tm->parts.empty() || tm->xchg); }
+void need_single(const tmg_machine* tm, const char* what);
+void destroy_group(tmg_machine* tm);
+void destroy_replicas(tmg_pool* pool);
+int group_info(const tmg_machine* tm, tmg_machine_info* info);
+int group_reset(tmg_machine* tm);
+int group_counters(const tmg_machine* tm, int32_t bank, uint16_t* out, const uint16_t* in);
+int group_include(const tmg_machine* tm, int32_t bank, uint64_t* masks, int32_t* counts);
+int group_bind(tmg_machine* tm, int32_t bank, int64_t q);  // bank < 0: every bank
+int group_prev(const tmg_machine* tm, int32_t bank, uint64_t* out, const uint64_t* in);
+tmg_machine* group_owner(const tmg_machine* tm, int32_t j);  // shard holding clause j, or null
+int group_update_clause(tmg_machine* tm, tmg_pool* pool, int32_t c, int32_t j, const int32_t* order,
+                        int64_t order_len, int64_t offset, int64_t batch, int32_t margin, double s, int32_t boost,
+                        uint64_t* rng_state, uint64_t* events);
+int group_train_epoch(tmg_machine* tm, tmg_pool* pool, int32_t mode, int32_t workers, int32_t epoch,
+                      tmg_epoch_report* report);
+// Class sums over every shard into host memory (train mode also refreshes
+// the shards' previous outputs and, with set_tallies, the pool's tallies).
+int group_class_sums(tmg_machine* tm, const tmg_pool* pool, const uint64_t* lits, int64_t q, int32_t mode,
+                     int32_t* out, bool set_tallies);
 
 }  // namespace tmgx

@@ -21,8 +21,34 @@ void check(int rc) {
 }
 
 int default_device() {
-  const char* env = std::getenv("TSETLIN_DEVICE");
+  const char* env = std::getenv("TSETLIN_DEVICES");
+  if (env && *env) return std::atoi(env);  // the first listed device holds the pools
+  env = std::getenv("TSETLIN_DEVICE");
   return env ? std::atoi(env) : 0;
+}
+
+// $TSETLIN_DEVICES="0,1,2,3": every MultiClassTM spans these GPUs (clause
+// shards, tmg_machine_create_devices); unset or one entry: one GPU.
+std::vector<std::int32_t> machine_devices() {
+  std::vector<std::int32_t> out;
+  const char* env = std::getenv("TSETLIN_DEVICES");
+  for (const char* p = env; p && *p;) {
+    char* end = nullptr;
+    const long v = std::strtol(p, &end, 10);
+    if (end == p) throw std::invalid_argument("TSETLIN_DEVICES: expected a comma-separated device list");
+    out.push_back(static_cast<std::int32_t>(v));
+    p = *end == ',' ? end + 1 : end;
+    if (*end && *end != ',') throw std::invalid_argument("TSETLIN_DEVICES: expected a comma-separated device list");
+  }
+  if (out.empty()) out.push_back(default_device());
+  return out;
+}
+
+tmg_machine* create_multiclass(const tmg_config& cc, int o, int m) {
+  const std::vector<std::int32_t> devs = machine_devices();
+  tmg_machine* h = nullptr;
+  check(tmg_machine_create_devices(&cc, o, m, devs.data(), static_cast<std::int32_t>(devs.size()), &h));
+  return h;
 }
 
 tmg_config to_c(const TMConfig& c) {
@@ -472,7 +498,7 @@ MultiClassTM::MultiClassTM(TMConfig cfg, int feature_count, int num_classes) : c
   auto dm = std::make_shared<detail::DeviceMachine>();
   dm->device = default_device();
   const tmg_config cc = to_c(config);
-  check(tmg_machine_create(&cc, feature_count, num_classes, dm->device, &dm->h));
+  dm->h = create_multiclass(cc, feature_count, num_classes);
   banks.reserve(static_cast<std::size_t>(num_classes));
   for (int c = 0; c < num_classes; ++c) {
     banks.emplace_back(feature_count, config.clauses, config.state_depth, PolarityScheme::Alternating);
@@ -485,9 +511,9 @@ MultiClassTM::MultiClassTM(TMConfig cfg, int feature_count, int num_classes) : c
 
 MultiClassTM::MultiClassTM(const MultiClassTM& other) : config(other.config) {
   auto dm = std::make_shared<detail::DeviceMachine>();
-  dm->device = other.banks.empty() ? default_device() : other.banks.front().link_->dev->device;
+  dm->device = default_device();
   const tmg_config cc = to_c(config);
-  check(tmg_machine_create(&cc, other.feature_count(), other.num_banks(), dm->device, &dm->h));
+  dm->h = create_multiclass(cc, other.feature_count(), other.num_banks());
   banks.reserve(other.banks.size());
   for (int c = 0; c < other.num_banks(); ++c) {
     const ClassBank& src = other.banks[static_cast<std::size_t>(c)];

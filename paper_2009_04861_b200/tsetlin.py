@@ -266,11 +266,17 @@ class MultiClassTM:
     ``clause_range`` selects an even-aligned clause shard for multi-GPU."""
 
     def __init__(self, cfg: TMConfig, feature_count: int, num_classes: int, device: int = 0,
-                 clause_range: Optional[Sequence[int]] = None):
+                 clause_range: Optional[Sequence[int]] = None, devices: Optional[Sequence[int]] = None):
         self.config = cfg
         c = cfg._c()
         self._h = C.c_void_p()
-        if clause_range is None:
+        if devices is not None:  # clause shards over several GPUs (repeats: several shards on one GPU)
+            devs = (C.c_int32 * len(devices))(*[int(v) for v in devices])
+            check(lib().tmg_machine_create_devices(C.byref(c), feature_count, num_classes, devs, len(devices),
+                                                   C.byref(self._h)))
+            self.clause_begin, self.clause_end = 0, cfg.clauses
+            device = int(devices[0])
+        elif clause_range is None:
             check(lib().tmg_machine_create(C.byref(c), feature_count, num_classes, device,
                                            C.byref(self._h)))
             self.clause_begin, self.clause_end = 0, cfg.clauses
@@ -311,6 +317,55 @@ class MultiClassTM:
 
     def bind_examples(self, q: int):
         check(lib().tmg_bind_examples(self._h, q))
+
+    def set_windows(self, windows: int):
+        """Tally-exchange windows per epoch of a sharded machine (default 16)."""
+        check(lib().tmg_machine_set_windows(self._h, windows))
+
+    def exchange_info(self):
+        """(shards or ranks, whether the exchange runs over NCCL)."""
+        n, nccl = C.c_int32(), C.c_int32()
+        check(lib().tmg_machine_exchange_info(self._h, C.byref(n), C.byref(nccl)))
+        return n.value, bool(nccl.value)
+
+    def attach_comm(self, comm: Optional["Comm"]):
+        check(lib().tmg_machine_attach_comm(self._h, comm.handle if comm is not None else None))
+
+
+class Comm:
+    """One rank's NCCL communicator for a multi-process clause-sharded
+    machine (tmg_comm_create): rank 0 calls unique_id(), the caller sends the
+    128 bytes to every rank (e.g. torch.distributed.broadcast_object_list)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_ubyte * 128)()
+        check(lib().tmg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        buf = (C.c_ubyte * 128).from_buffer_copy(uid)
+        self._h = C.c_void_p()
+        check(lib().tmg_comm_create(buf, nranks, rank, device, C.byref(self._h)))
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().tmg_comm_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+def nccl_available():
+    why = C.create_string_buffer(256)
+    ok = lib().tmg_nccl_available(why, 256)
+    return bool(ok), why.value.decode()
 
 
 @dataclass
