@@ -16,12 +16,14 @@ q examples — the most expensive epoch, and identical work every step.
           reset, the epoch runs, the per-class feedback-event report is read
           back.
 Multi-GPU (torchrun): weak scaling in clauses — every rank owns 2000 clauses
-per class (global n = 2000 * world). Default exchange "peer": every rank's
-tally replica is mapped into every other rank (CUDA IPC over NVLink) and the
-training kernels add each tally change into all replicas as it happens;
-"overlapped"/"sync" all-reduce tally deltas with NCCL every window
-(paper_2009_04861_b200/distributed.py). "peer" falls back to "overlapped"
-(and says so in config.exchange_note) when the replicas cannot be mapped.
+per class (global n = 2000 * world). Default exchange "comm": the engine's own
+NCCL communicator (tmg_comm_create, id broadcast once through
+torch.distributed) attached to the rank's shard, and tmg_train_epoch runs the
+windowed tally exchange inside the library, overlapped on a side stream
+(paper_2009_04861_b200/csrc/group.cu). Alternatives: "peer" (every tally
+change also RED-added into the other ranks' replicas over CUDA IPC / NVLink
+by the training kernels), "overlapped"/"sync" (the same windows driven from
+Python with torch.distributed, paper_2009_04861_b200/distributed.py).
 
 --impl reference times the UNMODIFIED reference (oracle/_ref/ref_driver, the
 reference sources compiled with their own Release flags) on the host cores:
@@ -162,7 +164,7 @@ def algorithmic_ops(steps_per_epoch: int, events: int, type1: int) -> float:
     return 18.0 * steps_per_epoch + events * 2.0 * w32 + type1 * L * 18.0 + (events - type1) * L * 3.0
 
 
-def inference_line(args, tm, d, local, stream):
+def inference_line(args, tm, d, local, stream, clk=None):
     import numpy as np
     import torch
 
@@ -189,8 +191,12 @@ def inference_line(args, tm, d, local, stream):
     evals_per_s = M_CLS * N_CLAUSES * Q_TEST * 2 * O_FEAT / (t * 1e-3)
     out = {"metric": "clause-literal evals/s (predict, class sums of the test rows)", "value": evals_per_s,
            "unit": "clause-literal evals/s", "rows_per_s": Q_TEST / (t * 1e-3), "ms": t, "rows": Q_TEST,
-           "kernel": "eval_sums_kernel<0,128>", "model": "state after the last timed epoch",
-           "test_accuracy": float((pred == d.test_y).mean())}
+           "kernel": "eval_bits_kernel<0>", "model": "state after the last timed epoch",
+           "test_accuracy": float((pred == d.test_y).mean()),
+           "roofline": roofline_record("eval_bits_ncu.json", t * 1e-3, clk, "eval_bits_kernel<0>", t,
+                                       extra={"timing_note": "kernel_ms is the whole tmg_class_sums_device call "
+                                                             "(sums memset + kernel; lists and example columns "
+                                                             "cached), so frac is a lower bound"})}
     if not args.no_cpu and os.path.exists(REF_DRIVER):
         import tempfile
         rows = 500
@@ -270,6 +276,102 @@ def sequential_line(local, with_ref: bool) -> dict:
     return line
 
 
+SM_COUNT, SCHEDULERS_PER_SM = 148, 4
+
+
+def same_q_record(d, local, q_use: int, ref_row: dict, line: dict) -> dict:
+    """Like-for-like with the reference's sample: the GPU's fresh epoch 0 on
+    the SAME first q_use training rows (examples/s and feedback events/s of
+    both), beside the full-q events/s ratio. Per-example cost depends on q
+    (the tallies of a longer epoch saturate later), so the events-normalised
+    ratio is the fair one for the headline."""
+    import paper_2009_04861_b200 as T
+    tm = T.MultiClassTM(T.TMConfig(clauses=N_CLAUSES, margin=MARGIN, specificity=SPEC, state_depth=STATE_N,
+                                   seed=TM_SEED), O_FEAT, M_CLS, device=local)
+    pool = T.ExamplePool(O_FEAT, d.train_x[:q_use], d.train_y[:q_use], M_CLS, device=local)
+    secs, ev = [], []
+    for _ in range(4):  # first is warm-up
+        tm.reset()
+        pool.reset_tallies()
+        rep = T.train_epoch_parallel(tm, pool, 1, 0)
+        secs.append(rep.device_seconds)
+        ev.append(rep.total_feedback_events())
+    g_s, g_ev = statistics.mean(secs[1:]), statistics.mean(ev[1:])
+    r_s, r_ev = ref_row["seconds"], ref_row["feedback_events"]
+    return {"q": q_use, "gpu_ms": g_s * 1e3, "gpu_examples_per_s": q_use / g_s,
+            "gpu_feedback_events_per_s": g_ev / g_s, "gpu_feedback_events": g_ev,
+            "ref_examples_per_s": q_use / r_s, "ref_feedback_events_per_s": r_ev / r_s, "ref_feedback_events": r_ev,
+            "examples_ratio_same_q": (q_use / g_s) / (q_use / r_s),
+            "events_ratio_same_q": (g_ev / g_s) / (r_ev / r_s),
+            "events_ratio_full_q": line["feedback_events_per_s"] / (r_ev / r_s),
+            "examples_ratio_full_q_vs_prefix": line["examples_per_s"] / (q_use / r_s)}
+
+
+def time_to_accuracy(d, local, epochs: int = 5) -> dict:
+    """Test accuracy after every asynchronous epoch (q = 60 000, 10 000 test
+    rows, seed 42) and the device time to reach the reference's mean final
+    accuracy (tests/golden/accuracy_ref.json "mnist_q60000": 5 seeds x 3
+    epochs of the compiled reference, train_epoch_parallel on all 8 threads
+    of the build container; its epoch seconds are that machine's)."""
+    import paper_2009_04861_b200 as T
+    ref = json.load(open(os.path.join(REPO, "tests", "golden", "accuracy_ref.json"))).get("mnist_q60000")
+    tm = T.MultiClassTM(T.TMConfig(clauses=N_CLAUSES, margin=MARGIN, specificity=SPEC, state_depth=STATE_N,
+                                   seed=TM_SEED), O_FEAT, M_CLS, device=local)
+    pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M_CLS, device=local)
+    test = T.ExamplePool(O_FEAT, d.test_x, d.test_y, M_CLS, device=local)
+    acc, secs = [], []
+    for e in range(epochs):
+        rep = T.train_epoch_parallel(tm, pool, 1, e)
+        secs.append(rep.device_seconds)
+        acc.append(T.evaluate_accuracy(tm, test))
+    out = {"gpu_accuracy_per_epoch": [round(a, 4) for a in acc], "gpu_epoch_ms": [round(v * 1e3, 2) for v in secs]}
+    if ref:
+        seeds = sorted(ref["per_seed"])
+        ref_acc = [statistics.mean(ref["per_seed"][k][e] for k in seeds) for e in range(len(ref["per_seed"][seeds[0]]))]
+        ref_s = [statistics.mean(ref["epoch_seconds"][k][e] for k in seeds) for e in range(len(ref_acc))]
+        target = ref_acc[-1]
+        hit = next((e for e, a in enumerate(acc) if a >= target), None)
+        out.update({"target": round(target, 4), "target_source": "reference mean final accuracy, 5 seeds, "
+                                                                 f"{len(ref_acc)} epochs (W={ref['workers']})",
+                    "reference_accuracy_per_epoch": [round(a, 4) for a in ref_acc],
+                    "reference_epoch_s": [round(v, 1) for v in ref_s],
+                    "reference_seconds_to_target": round(sum(ref_s), 1),
+                    "gpu_epochs_to_target": None if hit is None else hit + 1,
+                    "gpu_seconds_to_target": None if hit is None else sum(secs[:hit + 1]),
+                    "speedup_to_target": None if hit is None else sum(ref_s) / sum(secs[:hit + 1])})
+    return out
+
+
+def roofline_record(profile: str, kernel_s: float, clk, kernel: str, step_ms: float, effective=None, extra=None):
+    """Issue-bound roofline of one kernel: ncu's executed warp instructions of
+    this workload (profiles/<profile>, an ncu --set full capture of the same
+    command) / the kernel's live duration, vs the issue peak at the measured
+    SM clock. frac is a hardware fraction (<= 1); the ncu pipe and memory
+    utilisations of the same capture ride along."""
+    path = os.path.join(REPO, "profiles", profile)
+    prof = json.load(open(path)) if os.path.exists(path) else {}
+    mhz = (clk or {}).get("sm_mhz") or (clk or {}).get("sm_max_mhz") or 1965.0
+    peak = SM_COUNT * SCHEDULERS_PER_SM * 32 * mhz * 1e6  # thread-instructions/s
+    instr = prof.get("warp_instructions")
+    achieved = instr * 32 / kernel_s if instr else None
+    rec = {"bound": "int-issue", "unit": "Tops/s (thread instructions)",
+           "achieved": achieved / 1e12 if achieved else None, "peak": peak / 1e12,
+           "frac": achieved / peak if achieved else None,
+           "traffic": prof.get("dram_bytes_per_launch"),
+           "kernel": kernel, "kernel_ms": kernel_s * 1e3, "kernel_share_of_step": kernel_s * 1e3 / step_ms,
+           "instructions_per_launch": instr, "ncu_duration_ms": prof.get("duration_ms"),
+           "ncu": {k: prof.get(k) for k in ("pipe_alu_pct", "pipe_fma_pct", "pipe_fmaheavy_pct", "pipe_lsu_inst_pct",
+                                            "issue_active_pct", "l1tex_throughput_pct", "l2_throughput_pct",
+                                            "occupancy_achieved_pct", "source") if k in prof},
+           "peak_source": f"issue peak {SM_COUNT} SMs x {SCHEDULERS_PER_SM} schedulers x 32 lanes at the sampled "
+                          f"SM clock ({mhz:.0f} MHz); MEASURED_PEAKS.json has no integer figure",
+           "profile": f"profiles/{profile}"}
+    if effective is not None:
+        rec["effective_frac"] = effective
+    rec.update(extra or {})
+    return rec
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -316,6 +418,15 @@ def run_ours(args):
     allreduce = D.nccl_allreduce(local) if world > 1 else None
     windows = args.windows
     exchange, exchange_note = (args.exchange if world > 1 else "none"), None
+    comm = None
+    if exchange == "comm" and (args.share_device or args.dist_backend != "nccl"):
+        exchange, exchange_note = "overlapped", "NCCL needs one GPU per rank; one-device protocol test"
+    if exchange == "comm":  # the library's own NCCL communicator, windows inside tmg_train_epoch
+        uid = [T.Comm.unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(uid, src=0)
+        comm = T.Comm(uid[0], world, rank, local)
+        tm.attach_comm(comm)
+        tm.set_windows(windows)
     if exchange == "peer":  # tally replicas over peer memory; NCCL windows if P2P is unavailable
         try:
             D.attach_peer_tallies(pool)
@@ -330,9 +441,9 @@ def run_ours(args):
     def one_epoch(p):
         tm.reset()
         p.reset_tallies()
-        if world == 1:
+        if world == 1 or exchange == "comm":
             rep = T.train_epoch_parallel(tm, p, 1, 0)
-            return rep.feedback_events, rep.type_i_events, rep.device_seconds
+            return rep.feedback_events, rep.type_i_events, (rep.device_seconds if world == 1 else None)
         if exchange == "peer":
             ev = D.train_epoch_peer(tm, p, 0)
         elif exchange == "overlapped":
@@ -370,6 +481,7 @@ def run_ours(args):
         events.append(sum(ev))
         if t1 is not None:
             type1.append(sum(t1))
+        if ks is not None:
             kern_s.append(ks)
     launches = kernel_launches() - launches0
     clk = clocks.stop() if clocks else None
@@ -428,29 +540,21 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk,
     }
-    # ---- roofline of the dominant kernel (train_async), INT issue bound
+    # ---- roofline of the dominant kernel (train_async): integer issue bound.
+    # Hardware fraction: the kernel's executed warp instructions per launch
+    # (ncu, committed profile of this exact workload) over its live CUDA-event
+    # time, against the SM issue peak (148 SMs x 4 schedulers x 1 warp
+    # instruction per cycle) at the SM clock sampled during the timed region.
     if kern_s:
-        ops = algorithmic_ops(M_CLS * N_CLAUSES * Q_TRAIN, int(statistics.mean(events)),
-                              int(statistics.mean(type1)))
         k = statistics.mean(kern_s)
-        traffic, hw = None, None
-        tpath = os.path.join(REPO, "profiles", "train_async_ncu.json")
-        if os.path.exists(tpath):  # the committed ncu --set full summary of this kernel
-            prof = json.load(open(tpath))
-            traffic = prof.get("dram_bytes_per_launch")
-            hw = {k: prof.get(k) for k in ("pipe_alu_pct", "pipe_fma_pct", "pipe_fmaheavy_pct", "pipe_lsu_inst_pct",
-                                           "issue_active_pct", "ipc_active", "duration_ms", "source")}
-        line["roofline"] = {"bound": "int-alu", "achieved": ops / k / 1e12, "peak": mixed_peak / 1e12,
-                            "unit": "Tops/s", "frac": ops / k / mixed_peak, "traffic": traffic,
-                            "frac_note": "algorithmic ops (SURVEY 8(d) model) / kernel time; >1 = the sampler "
-                                         "draws fewer random words than the model charges (effective). "
-                                         "Hardware view: ncu ALU-pipe utilisation in 'ncu'",
-                            "ncu": hw,
-                            "kernel": "train_async_kernel<1,8,P2>", "kernel_ms": k * 1e3,
-                            "kernel_share_of_step": k * 1e3 / ms,
-                            "peak_source": "measured on this GPU by tmg_bench_int_peak (LOP3+IMAD issue); "
-                                           f"LOP3-only {lop3_peak / 1e12:.2f} Tops/s",
-                            "ops_model": "SURVEY.md 8(d): gate 18, eval 2*ceil(2o/32), TypeI 2o*18, TypeII 2o*3"}
+        line["roofline"] = roofline_record(
+            "train_async_ncu.json", k, clk, "train_async_kernel<1,8,P2>", ms,
+            effective=algorithmic_ops(M_CLS * N_CLAUSES * Q_TRAIN, int(statistics.mean(events)),
+                                      int(statistics.mean(type1))) / k / mixed_peak,
+            extra={"effective_note": "SURVEY.md 8(d) ops model (gate 18, eval 2*ceil(2o/32), TypeI 2o*18, "
+                                     "TypeII 2o*3) / kernel time / measured LOP3+IMAD peak "
+                                     f"{mixed_peak / 1e12:.2f} Tops/s (LOP3-only {lop3_peak / 1e12:.2f}); "
+                                     ">1 because the alias sampler draws one 32-bit word per 8 literals"})
     line["e2e"] = {"value": e2e_val, "unit": UNIT, "ms_per_step": statistics.mean(e2e_ms),
                    "ms_all": [round(v, 3) for v in e2e_ms],
                    "phases_ms": {k: round(statistics.mean(ph[n] for ph in e2e_phases), 3)
@@ -462,7 +566,7 @@ def run_ours(args):
     # beside the reference's single-threaded predict_all on the SAME model
     # file for a bounded row sample, predictions compared row for row.
     if world == 1:
-        line["inference"] = inference_line(args, tm, d, local, stream)
+        line["inference"] = inference_line(args, tm, d, local, stream, clk)
         if not args.no_other_configs:
             line["other_configs"] = other_configs(local)
             line["sequential_trainer"] = sequential_line(local, not args.no_cpu)
@@ -478,6 +582,9 @@ def run_ours(args):
                                 "sample": f"fresh-model epoch 0 on the first {q_use} of {Q_TRAIN} rows, "
                                           f"reference train_epoch_parallel(workers={cores}), "
                                           f"{rows[0]['feedback_events']} feedback events"}
+        line["same_q"] = same_q_record(d, local, q_use, rows[0], line)
+    if world == 1 and not args.no_other_configs:
+        line["time_to_accuracy"] = time_to_accuracy(d, local)
     print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
@@ -494,10 +601,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-other-configs", action="store_true", help="skip the FMNIST/IMDb side measurements")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (tests: gloo)")
-    ap.add_argument("--exchange", choices=["peer", "overlapped", "sync"], default="peer",
-                    help="N>1 tally exchange: replicas updated by the training kernels over peer memory "
-                         "(NVLink), or windowed all-reduce double-buffered on a side stream, or "
-                         "host-synchronous per window")
+    ap.add_argument("--exchange", choices=["comm", "peer", "overlapped", "sync"], default="comm",
+                    help="N>1 tally exchange: the engine's NCCL communicator with the windowed exchange "
+                         "inside tmg_train_epoch (default); replicas updated by the training kernels over "
+                         "peer memory (NVLink); windowed all-reduce driven from Python, overlapped or "
+                         "host-synchronous")
     ap.add_argument("--share-device", action="store_true",
                     help="run every rank on cuda:0 (one-GPU test of the N>1 protocol; not a measurement)")
     args = ap.parse_args()

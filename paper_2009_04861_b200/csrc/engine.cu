@@ -319,6 +319,10 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   p.boost = tm->cfg.boost_true_positive ? 1 : 0;
   p.all_positive = tm->all_positive;
   p.regress = tm->regress_mode ? 1 : 0;
+  {  // clause order over the grid's waves (kernels.h TrainParams::interleave)
+    const char* o = std::getenv("TMG_CLAUSE_ORDER");
+    p.interleave = o && o[0] == 'c' ? 0 : 1;
+  }
   const double s = tm->cfg.specificity;
   p.thr_high = prob_threshold((s - 1.0) / s);
   p.thr_low = prob_threshold(1.0 / s);

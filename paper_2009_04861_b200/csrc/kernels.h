@@ -50,6 +50,10 @@ struct TrainParams {
   // are scaled targets t in [0, T], gate |t - v| / 2T with v = clamp(tally, 0,
   // T), Type I when v < t else Type II (regression.cpp:46-67).
   int32_t regress;
+  // Clause order over the grid: 0 = class-major (warp w -> class w / n_loc),
+  // 1 = interleaved (warp w -> class w % m, clause w / m), so each resident
+  // wave holds a slice of every class instead of all clauses of a few.
+  int32_t interleave;
   int32_t all_positive;
   uint32_t thr_high, thr_low;  // async: P(u < p) thresholds as 32-bit fixed point
   BernThresholds bern;         // the same, split for the sampler

@@ -42,8 +42,9 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   load_alias(P, atab);
   const int lane = static_cast<int>(lane_id());
   const AliasRef aref = lane_alias(atab, lane);
-  const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (lc >= P.m * P.n_loc) return;
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= P.m * P.n_loc) return;
+  const int lc = P.interleave ? (w % P.m) * P.n_loc + w / P.m : w;
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;

@@ -165,8 +165,9 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   const int lane = threadIdx.x & 31;
   const AliasRef aref = lane_alias(atab, lane);
   const int wib = threadIdx.x >> 5;
-  const int lc = blockIdx.x * cpb + wib;
-  if (lc >= P.m * P.n_loc) return;
+  const int w = blockIdx.x * cpb + wib;
+  if (w >= P.m * P.n_loc) return;
+  const int lc = P.interleave ? (w % P.m) * P.n_loc + w / P.m : w;
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;

@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Summarise an ncu --set full report of one kernel into profiles/ (markdown +
 json): duration, pipe utilisation, stall reasons, DRAM traffic, occupancy.
-Usage: python tools/summarize_ncu.py <report.ncu-rep> <out-prefix> [kernel-regex]"""
+Usage: python tools/summarize_ncu.py <report.ncu-rep> <out-prefix> [kernel-regex] [source-note]"""
 import csv
 import io
 import json
@@ -57,8 +57,13 @@ summary = {
     "registers_per_thread": num("launch__registers_per_thread"),
     "occupancy_achieved_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
     "l2_hit_pct": num("lts__t_sector_hit_rate.pct"),
+    "l1tex_throughput_pct": num("l1tex__throughput.avg.pct_of_peak_sustained_elapsed"),
+    "l2_throughput_pct": num("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+    "l1tex_hit_pct": num("l1tex__t_sector_hit_rate.pct"),
     "top_stalls_per_issue": top,
 }
+if len(sys.argv) > 4:
+    summary["source"] = sys.argv[4]
 json.dump(summary, open(prefix + ".json", "w"), indent=1)
 with open(prefix + ".md", "w") as f:
     f.write(f"# ncu --set full summary: {summary['kernel']}\n\n")
