@@ -284,6 +284,19 @@ __device__ __forceinline__ bool gate_step(const TrainParams& P, int c, bool posi
   return gate_decide(P, c, positive, g, i, __ldg(P.labels + i), __ldcg(P.tallies + i * P.m + c), target);
 }
 
+// The clause a warp trains (TrainParams::interleave): class-major (0), or
+// classes interleaved per warp (1) or per group of G warps (2, the CTA's
+// warps stay one class's consecutive clauses), so that each resident wave of
+// the grid holds a slice of every class.
+__device__ __forceinline__ int clause_of_warp(const TrainParams& P, int w, int G) {
+  if (P.interleave == 0) return w;
+  if (P.interleave == 2 && P.n_loc % G == 0) {
+    const int b = w / G;
+    return (b % P.m) * P.n_loc + (b / P.m) * G + w % G;
+  }
+  return (w % P.m) * P.n_loc + w / P.m;
+}
+
 // Per-clause starting position in the epoch order (trainer.cpp:41-44, 222-223).
 __device__ __forceinline__ int64_t clause_offset_dev(uint32_t g, int64_t q) {
   return static_cast<int64_t>(splitmix_dev(static_cast<uint64_t>(g) + 1) % static_cast<uint64_t>(q));

@@ -321,7 +321,7 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   p.regress = tm->regress_mode ? 1 : 0;
   {  // clause order over the grid's waves (kernels.h TrainParams::interleave)
     const char* o = std::getenv("TMG_CLAUSE_ORDER");
-    p.interleave = o && o[0] == 'c' ? 0 : 1;
+    p.interleave = o && o[0] == 'c' ? 0 : (o && o[0] == 'w' ? 1 : 2);
   }
   const double s = tm->cfg.specificity;
   p.thr_high = prob_threshold((s - 1.0) / s);

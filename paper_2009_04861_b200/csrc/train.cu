@@ -44,7 +44,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   const AliasRef aref = lane_alias(atab, lane);
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= P.m * P.n_loc) return;
-  const int lc = P.interleave ? (w % P.m) * P.n_loc + w / P.m : w;
+  const int lc = clause_of_warp(P, w, blockDim.x >> 5);
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;

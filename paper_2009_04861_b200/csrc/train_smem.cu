@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   const int wib = threadIdx.x >> 5;
   const int w = blockIdx.x * cpb + wib;
   if (w >= P.m * P.n_loc) return;
-  const int lc = P.interleave ? (w % P.m) * P.n_loc + w / P.m : w;
+  const int lc = clause_of_warp(P, w, cpb);
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
