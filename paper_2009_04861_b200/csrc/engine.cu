@@ -495,7 +495,8 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
   if (with_delta) p.tally_delta = pool->delta.ptr;
   int blocks = 0;
   // Register-resident clauses up to 4 words per lane per part (o <= 4096);
-  // wider rows keep the automata in shared memory. (A variant splitting each
+  // wider rows keep the automata in shared memory (FMNIST's 3-word rows on
+  // the shared-memory kernel: 1203 vs 627 ms, round 2). (A variant splitting each
   // wide clause over 2-4 warps with register-resident slices measured 3-11 %
   // slower at IMDb shape, round 1, and was dropped.)
   const bool ok = tm->NW <= 4 ? tmg::train_async_launch(p, tm->B, tm->NW, tm->stream, &blocks)

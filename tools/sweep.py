@@ -89,6 +89,12 @@ def run(kind, clauses_list, q, qt, T_, s, epochs=2):
             r = ref_point(kind, n, T_, s, q)
             line["reference"] = r
             line["x_reference_examples_per_s"] = line["examples_per_s_e0"] / r["examples_per_s"]
+            # per-example cost grows with the tallies' distance from T, which
+            # depends on q: the feedback-events/s ratio is the like-for-like one
+            gpu_eps = rows[0]["events"] / (rows[0]["kernel_ms"] * 1e-3)
+            line["x_reference_events_per_s"] = gpu_eps / (r["feedback_events"] / r["seconds"])
+            line["events_per_example"] = {"gpu_full_q": rows[0]["events"] / q,
+                                          "reference_prefix": r["feedback_events"] / r["q_sample"]}
         print(json.dumps(line), flush=True)
         del tm
 
