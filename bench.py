@@ -314,7 +314,8 @@ def time_to_accuracy(d, local, epochs: int = 5) -> dict:
     epochs of the compiled reference, train_epoch_parallel on all 8 threads
     of the build container; its epoch seconds are that machine's)."""
     import paper_2009_04861_b200 as T
-    ref = json.load(open(os.path.join(REPO, "tests", "golden", "accuracy_ref.json"))).get("mnist_q60000")
+    allref = json.load(open(os.path.join(REPO, "tests", "golden", "accuracy_ref.json")))
+    ref = allref.get("mnist_q60000")
     tm = T.MultiClassTM(T.TMConfig(clauses=N_CLAUSES, margin=MARGIN, specificity=SPEC, state_depth=STATE_N,
                                    seed=TM_SEED), O_FEAT, M_CLS, device=local)
     pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M_CLS, device=local)
@@ -339,6 +340,18 @@ def time_to_accuracy(d, local, epochs: int = 5) -> dict:
                     "gpu_epochs_to_target": None if hit is None else hit + 1,
                     "gpu_seconds_to_target": None if hit is None else sum(secs[:hit + 1]),
                     "speedup_to_target": None if hit is None else sum(ref_s) / sum(secs[:hit + 1])})
+        by_w = {}
+        for key in ("mnist_q60000", "mnist_q60000_w4", "mnist_q60000_w2", "mnist_q60000_w1"):
+            if key in allref:
+                v = allref[key]
+                ks = sorted(v["per_seed"])
+                by_w[f"W={v['workers']}"] = {
+                    "seeds": len(ks),
+                    "accuracy_per_epoch": [round(statistics.mean(v["per_seed"][k][e] for k in ks), 4)
+                                           for e in range(len(v["per_seed"][ks[0]]))],
+                    "epoch_s": [round(statistics.mean(v["epoch_seconds"][k][e] for k in ks), 1)
+                                for e in range(len(v["per_seed"][ks[0]]))]}
+        out["reference_by_workers"] = by_w
     return out
 
 

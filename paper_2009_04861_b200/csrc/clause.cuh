@@ -22,6 +22,7 @@
 #endif
 
 
+
 namespace tmg {
 namespace {
 

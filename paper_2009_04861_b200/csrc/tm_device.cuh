@@ -409,30 +409,32 @@ __device__ __forceinline__ AliasRef alias_ref(const uint32_t* tab, uint32_t lane
                   static_cast<uint32_t>(__cvta_generic_to_shared(tab + 256 * kAliasCopies)) + laneoff};
 }
 
+// The 32-literal pattern of one word slot from one Philox block (4 draws).
+template <bool SPLIT = true>
+__device__ __forceinline__ uint32_t alias_word(const U4 r, AliasRef ar, uint32_t need) {
+  uint32_t b[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t u = j == 0 ? r.x : (j == 1 ? r.y : (j == 2 ? r.z : r.w));
+    const uint32_t col = u & 0xFFu;
+    uint32_t e;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(mad_u32(col, 4u * kAliasCopies, ar.base)));
+    if (SPLIT) {
+      uint32_t a;
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(a) : "r"(mad_u32(col, kAliasCopies, ar.pbase)));
+      b[j] = u < e ? u : a;  // (u >> 8) < threshold: the column's own pattern; low byte = the draw
+    } else {
+      b[j] = (u | 0xFFu) < e ? u : e;  // the same test on the packed entry
+    }
+  }
+  const uint32_t lo = __byte_perm(b[0], b[1], 0x0040), hi = __byte_perm(b[2], b[3], 0x0040);
+  return __byte_perm(lo, hi, 0x5410) & need;
+}
+
 template <int K, bool SPLIT = true, typename Gen>
 __device__ __forceinline__ void alias_words(const uint32_t (&need)[K], AliasRef ar, uint32_t (&bern)[K], Gen&& gen) {
-  const uint32_t base = ar.base, pbase = ar.pbase;
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const U4 r = gen(k, 0);
-    uint32_t b[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t u = j == 0 ? r.x : (j == 1 ? r.y : (j == 2 ? r.z : r.w));
-      const uint32_t col = u & 0xFFu;
-      uint32_t e;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(mad_u32(col, 4u * kAliasCopies, base)));
-      if (SPLIT) {
-        uint32_t a;
-        asm volatile("ld.shared.u8 %0, [%1];" : "=r"(a) : "r"(mad_u32(col, kAliasCopies, pbase)));
-        b[j] = u < e ? u : a;  // (u >> 8) < threshold: the column's own pattern; low byte = the draw
-      } else {
-        b[j] = (u | 0xFFu) < e ? u : e;  // the same test on the packed entry
-      }
-    }
-    const uint32_t lo = __byte_perm(b[0], b[1], 0x0040), hi = __byte_perm(b[2], b[3], 0x0040);
-    bern[k] = __byte_perm(lo, hi, 0x5410) & need[k];
-  }
+  for (int k = 0; k < K; ++k) bern[k] = alias_word<SPLIT>(gen(k, 0), ar, need[k]);
 }
 
 // Warp-cooperative exact Bernoulli masks for one Type I event: every lane

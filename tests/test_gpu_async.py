@@ -429,11 +429,14 @@ def _band(case):
 def test_async_accuracy_parity_mnist_full():
     """The configuration bench.py times (BASELINE.json configs[1]): q = 60 000
     training rows, 10 000 test rows, 2000 clauses/class, T = 50, s = 10, three
-    epochs, five seeds. Two-sided: the GPU's 5-seed mean after every epoch
-    lies within 0.5 pt of the reference's (W = all threads) 5-seed mean for
-    that epoch, widened only by the reference's own spread over worker
-    counts (tests/golden/accuracy_ref.json, gen_accuracy_ref.py)."""
-    ref = _ref_acc().get("mnist_q60000")
+    epochs, five seeds. Two-sided after EVERY epoch: the GPU's 5-seed mean
+    lies within 0.5 pt of the band the reference's own asynchronous schedules
+    span at that epoch — its seed means over the worker counts measured (all
+    host threads, W = 4, W = 2, W = 1; tests/golden/accuracy_ref.json,
+    gen_accuracy_ref.py). The reference itself moves by 3.5 pt at epoch 0
+    between W = 8 (0.906) and W = 1 (0.941)."""
+    acc = _ref_acc()
+    ref = acc.get("mnist_q60000")
     if ref is None:
         pytest.skip("accuracy_ref.json lacks mnist_q60000")
     cfgd = ref["config"]
@@ -449,16 +452,11 @@ def test_async_accuracy_parity_mnist_full():
             T.train_epoch_parallel(tm, pool, 8, e)
             per_epoch[k, e] = T.evaluate_accuracy(tm, test)
     gpu = per_epoch.mean(axis=0)
-    cpu = np.mean([ref["per_seed"][str(s)] for s in range(1, 6)], axis=0)
-    lo, hi, spread = _band("mnist_q60000")
-    print(f"mnist_q60000 per-epoch gpu {np.round(gpu, 4)} vs reference {np.round(cpu, 4)}; "
-          f"reference final over W: {spread}; gpu per seed {per_epoch[:, -1]}")
-    # Final epoch (the configuration's defined length): two-sided, 0.5 pt
-    # widened by the reference's own spread over worker counts. Earlier
-    # epochs: not below the reference by more than 0.5 pt (the GPU's
-    # schedule — every class's clauses spread over each resident wave — is
-    # ahead after epoch 0; that is bench.py's time_to_accuracy, not a gap).
-    for e in range(cfgd["epochs"] - 1):
-        assert gpu[e] >= cpu[e] - 0.005, (e, gpu, cpu)
-    assert abs(gpu[-1] - cpu[-1]) <= 0.005 + (hi - lo), (gpu, cpu)
-    assert lo - 0.005 <= gpu[-1] <= hi + 0.005
+    curves = {k: np.mean([v for v in acc[k]["per_seed"].values()], axis=0)
+              for k in ("mnist_q60000", "mnist_q60000_w4", "mnist_q60000_w2", "mnist_q60000_w1") if k in acc}
+    lo = np.min(list(curves.values()), axis=0)
+    hi = np.max(list(curves.values()), axis=0)
+    print(f"mnist_q60000 per-epoch gpu {np.round(gpu, 4)}; reference per W "
+          f"{ {k: np.round(v, 4).tolist() for k, v in curves.items()} }; gpu per seed {per_epoch[:, -1]}")
+    for e in range(cfgd["epochs"]):
+        assert lo[e] - 0.005 <= gpu[e] <= hi[e] + 0.005, (e, gpu, lo, hi)
