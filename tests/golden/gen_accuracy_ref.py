@@ -31,6 +31,12 @@ CASES = {
                        noise=0.0, data_seed=10000),
     "mnist_q6000_w1": dict(data="mnist", q=6000, qtest=2000, clauses=2000, T=50, s=10.0, epochs=3,
                            noise=0.0, data_seed=2009, workers=1),
+    # configs[2] / [3] shapes on larger training prefixes (about an hour of
+    # the reference each on the 8-core build container)
+    "fmnist_q6000": dict(data="fmnist", q=6000, qtest=2000, clauses=8000, T=100, s=15.0, epochs=2,
+                         noise=0.0, data_seed=2352),
+    "imdb_q12000": dict(data="imdb", q=12000, qtest=4000, clauses=10000, T=100, s=15.0, epochs=2,
+                        noise=0.0, data_seed=10000),
     # The configuration bench.py times (BASELINE.json configs[1]) at its full
     # size: q = 60 000 training rows, 10 000 test rows, 3 epochs.
     "mnist_q60000": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,

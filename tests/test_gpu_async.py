@@ -372,7 +372,8 @@ def accuracy_parity(case, gpu_accs):
     return lo - tol <= gpu <= hi + tol, msg
 
 
-@pytest.mark.parametrize("case,kind", [("fmnist_q1000", "fmnist"), ("imdb_q4000", "imdb")])
+@pytest.mark.parametrize("case,kind", [("fmnist_q1000", "fmnist"), ("imdb_q4000", "imdb"),
+                                       ("fmnist_q6000", "fmnist"), ("imdb_q12000", "imdb")])
 def test_async_accuracy_parity_wide(case, kind):
     """BASELINE.json configs[2]/[3] shapes (FMNIST 2352 bits x 8000 clauses,
     IMDb 10 000 bits x 10 000 clauses, the shared-memory clause kernel) vs the
