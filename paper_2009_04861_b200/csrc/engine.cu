@@ -210,7 +210,7 @@ void rebuild_entries(tmg_machine* tm) {
     tm->lists.alloc(static_cast<size_t>(total + total / 4) + 64);
   }
   tmg::fill_lists_launch(tm->state.ptr, tm->clauses(), tm->B, tm->Wp, tm->Wx, tm->o, tm->offs.ptr, tm->npos.ptr,
-                         tm->lists.ptr, tm->stream);
+                         tm->lists.ptr, tm->meta.ptr, tm->stream);
   CK(cudaGetLastError());
   tm->entries_dirty = false;
 }
@@ -261,6 +261,7 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->inc_count.alloc(cl);
     tm->lens.alloc(cl);
     tm->npos.alloc(cl);
+    tm->meta.alloc(cl);
     tm->offs.alloc(cl + 1);
     tm->events.alloc(2 * static_cast<size_t>(m));  // all events, then Type I events
     tm->dbg.alloc(tmg::kDebugCounters);
@@ -524,9 +525,7 @@ void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool 
   e.lit_t = lit_t;
   e.Gs = static_cast<uint32_t>(Gs);
   e.lists = tm->lists.ptr;
-  e.offs = tm->offs.ptr;
-  e.npos = tm->npos.ptr;
-  e.inc_count = tm->inc_count.ptr;
+  e.meta = tm->meta.ptr;
   e.prev = prev;
   e.n_loc = tm->n_loc;
   e.j_begin = tm->j_begin;
@@ -683,6 +682,7 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   tm->inc_count.release();
   tm->lens.release();
   tm->npos.release();
+  tm->meta.release();
   tm->offs.release();
   tm->lit_t.release();
   tm->sums.release();

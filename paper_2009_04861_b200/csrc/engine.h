@@ -163,6 +163,7 @@ struct tmg_machine {
   tmgx::DevBuf<uint32_t> state, prev;
   tmgx::DevBuf<int32_t> inc_count, lens, npos, sums;
   tmgx::DevBuf<int64_t> offs;      // [clauses + 1] literal-list offsets
+  tmgx::DevBuf<int4> meta;         // [clauses] eval list descriptors
   tmgx::DevBuf<uint32_t> lists;    // included-literal lists (eval.cu)
   tmgx::DevBuf<uint32_t> lit_t;    // scratch: feature-major example columns of non-pool rows
   tmgx::DevBuf<unsigned long long> events;

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(1024) scan_lengths_kernel(const int32_t* __res
 // literals' feature indices, padded to 4 with o + 1 (the all-zeros row).
 __global__ void fill_literals_kernel(const uint32_t* __restrict__ state, int clauses, int B, int Wp, int Wx,
                                      int o, const int64_t* __restrict__ offs, const int32_t* __restrict__ npos,
-                                     uint32_t* __restrict__ lists) {
+                                     uint32_t* __restrict__ lists, int4* __restrict__ meta) {
   const int lane = threadIdx.x & 31;
   const int lc = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (lc >= clauses) return;
@@ -98,6 +98,7 @@ __global__ void fill_literals_kernel(const uint32_t* __restrict__ state, int cla
   uint32_t* out = lists + offs[lc];
   const int split = npos[lc];
   const int len = static_cast<int>(offs[lc + 1] - offs[lc]);
+  if (lane == 0) meta[lc] = make_int4(static_cast<int>(offs[lc] >> 2), len, split, 0);
   for (int part = 0; part < 2; ++part) {
     uint32_t* dst = out + (part ? split : 0);
     const int end = part ? len - split : split;
@@ -225,20 +226,21 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 5) eval_bits_kernel(BitsEvalP
   uint32_t cnt[kSumPlanes];
 #pragma unroll
   for (int b = 0; b < kSumPlanes; ++b) cnt[b] = 0u;
-  // Clauses are handed out one at a time (lists differ in length): warps
-  // finish together at the CTA reduction below.
+  // Clauses are handed out one at a time as warps finish (lists differ in
+  // length; claiming ahead measured worse: a busy warp sits on its claim), so
+  // the warps reach the CTA reduction below together. One 16-byte load per
+  // clause: {list offset / 4, list length, positive-part length}.
+  const int4* __restrict__ meta = P.meta + static_cast<size_t>(c) * P.n_loc;
   for (int jl = jc0 + warp; jl < jc1;) {
-    const int lc = c * P.n_loc + jl;
-    const int inc = __ldg(P.inc_count + lc);
+    const int4 mt = __ldg(meta + jl);
+    const int len = mt.y, np = mt.z;
     uint32_t acc = valid;  // empty clause: Train 1
-    if (TRAIN || inc != 0) {  // empty clause: Predict 0 (core.hpp:211-213)
-      const int64_t off = __ldg(P.offs + lc);
-      const int len = static_cast<int>(__ldg(P.offs + lc + 1) - off);
-      const int np = __ldg(P.npos + lc);
-      const uint32_t* lst = P.lists + off;
+    if (TRAIN || len != 0) {  // empty clause: Predict 0 (core.hpp:211-213)
+      const uint32_t* lst = P.lists + (static_cast<size_t>(static_cast<uint32_t>(mt.x)) << 2);
       acc = fold_columns<true>(lst, np, col, row_bytes, acc, 0u);
       if (__any_sync(kFull, acc != 0u) && len > np) acc &= ~fold_columns<false>(lst + np, len - np, col, row_bytes, 0u, acc);
-      if (TRAIN && P.prev != nullptr && gw < P.Wq) P.prev[static_cast<size_t>(lc) * P.Wq + gw] = acc;
+      if (TRAIN && P.prev != nullptr && gw < P.Wq)
+        P.prev[(static_cast<size_t>(c) * P.n_loc + jl) * P.Wq + gw] = acc;
       const int j = P.j_begin + jl;
       if (P.all_positive || !(j & 1)) count_word<true>(cnt, acc);
       else count_word<false>(cnt, acc);
@@ -454,10 +456,11 @@ int64_t build_lists_launch(const uint32_t* state, int clauses, int B, int Wp, in
 }
 
 void fill_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int o, const int64_t* offs,
-                       const int32_t* npos, uint32_t* lists, cudaStream_t s) {
+                       const int32_t* npos, uint32_t* lists, int4* meta, cudaStream_t s) {
   if (clauses <= 0) return;
   count_launch();
-  fill_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, o, offs, npos, lists);
+  fill_literals_kernel<<<blocks_for(clauses, 4), 128, 0, s>>>(state, clauses, B, Wp, Wx, o, offs, npos, lists,
+                                                              meta);
 }
 
 int64_t lit_t_stride(int64_t q) { return ((q + 31) / 32 + 31) / 32 * 32; }

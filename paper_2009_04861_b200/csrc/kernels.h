@@ -124,9 +124,7 @@ struct BitsEvalParams {
   uint32_t Gs;               // words per lit_t row (lit_t_stride(q))
   const uint32_t* lists;     // per clause: positive-literal features (padded to 4 with o), then
                              // negated-literal features (padded to 4 with o + 1)
-  const int64_t* offs;       // [m*n_loc + 1] list offsets (multiples of 4)
-  const int32_t* npos;       // [m*n_loc] padded length of the positive part
-  const int32_t* inc_count;  // [m*n_loc]
+  const int4* meta;          // [m*n_loc] {list offset / 4, list length, positive-part length, 0}
   uint32_t* prev;            // refresh mode: [m*n_loc][Wq]
   int32_t n_loc, j_begin, m, Wq;
   int32_t cta_clauses, chunks;  // clauses per CTA (<= 2040), CTAs per class
@@ -149,7 +147,7 @@ bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out
 int64_t build_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int32_t* inc_count,
                            int32_t* lens, int32_t* npos, int64_t* offs, cudaStream_t s);
 void fill_lists_launch(const uint32_t* state, int clauses, int B, int Wp, int Wx, int o, const int64_t* offs,
-                       const int32_t* npos, uint32_t* lists, cudaStream_t s);
+                       const int32_t* npos, uint32_t* lists, int4* meta, cudaStream_t s);
 int64_t lit_t_stride(int64_t q);
 void transpose_literals_launch(const uint32_t* xplane, int64_t row_stride, int64_t q, int o, uint32_t* lit_t,
                                cudaStream_t s);
