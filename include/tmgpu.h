@@ -230,15 +230,17 @@ int tmg_train_epoch_sequential(tmg_machine* tm, tmg_pool* pool, int32_t epoch, d
  * tmg_refresh_tallies, class sums and predictions cover the whole machine;
  * calls that replay the reference's serial streams (sequential trainer,
  * update_clause, feedback, the W = 1 replay, regression) need one device and
- * fail with TMG_EINVAL. An epoch runs every shard's kernel on its own device
- * and exchanges tally deltas every window (tmg_machine_set_windows, default
- * 16) on side streams, overlapped with the next window: NCCL all-reduce when
- * the devices are distinct and libnccl.so.2 loads (TSETLIN_EXCHANGE=peer
- * forces the other path), else a peer-memory reduction kernel. Pools are
- * replicated to the shards' devices on first use. ndev == 1 creates a plain
- * machine. */
+ * fail with TMG_EINVAL. An epoch is one kernel launch per shard on its own
+ * device; while they run, the shards' cumulative tally deltas are exchanged
+ * about `windows` times per epoch (tmg_machine_set_windows, default 16) on
+ * high-priority side streams: NCCL all-reduce when the devices are distinct
+ * and libnccl.so.2 loads (TSETLIN_EXCHANGE=peer forces the other path), else
+ * a peer-memory reduction kernel. Pools are replicated to the shards' devices
+ * on first use. ndev == 1 creates a plain machine. */
 int tmg_machine_create_devices(const tmg_config* cfg, int32_t o, int32_t m, const int32_t* devices, int32_t ndev,
                                tmg_machine** out);
+/* Tally exchanges per epoch of a sharded machine (the interval adapts to the
+ * previous epoch's length). */
 int tmg_machine_set_windows(tmg_machine* tm, int32_t windows);
 /* Tallies of the pool's replica for shard k of the last sharded machine that
  * used it (q x m int32; test hook: every replica holds the same tallies). */
@@ -251,7 +253,7 @@ int tmg_nccl_available(char* why, int32_t len);
  * to every rank, each rank creates its communicator on its device and
  * attaches it to its shard (tmg_machine_create_shard with the even-aligned
  * slice of its rank). tmg_train_epoch then trains this rank's clauses with
- * the windowed exchange over NCCL and reports every rank's feedback events;
+ * the streaming tally exchange over NCCL and reports every rank's feedback events;
  * tmg_class_sums / tmg_predict / tmg_refresh_tallies return whole-machine
  * results on every rank. These calls are collective: every rank makes them
  * in the same order with the same arguments. Attach NULL to detach. */

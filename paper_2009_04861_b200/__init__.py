@@ -9,7 +9,22 @@ RegressionHead, tmmodel v1 I/O) over the C ABI of libtmgpu.so
 Importing the package loads libtmgpu.so and raises ImportError if it has not
 been built: there is no CPU fallback.
 """
-from . import _capi as _capi_mod
+import importlib.util as _ilu
+import os as _os
+
+# Sharded machines load NCCL at run time (csrc/group.cu). Point the engine at
+# the NCCL wheel torch links against, so that a process which uses the
+# engine's NCCL before importing torch does not leave an older system
+# libnccl.so.2 in place for libtorch_cuda.so to bind to.
+if "TMG_NCCL_LIB" not in _os.environ:
+    _spec = _ilu.find_spec("nvidia.nccl") if _ilu.find_spec("nvidia") else None
+    for _root in (_spec.submodule_search_locations or []) if _spec else []:
+        _cand = _os.path.join(_root, "lib", "libnccl.so.2")
+        if _os.path.exists(_cand):
+            _os.environ["TMG_NCCL_LIB"] = _cand
+            break
+
+from . import _capi as _capi_mod  # noqa: E402
 
 _capi_mod.lib()  # fail loudly at import when the CUDA engine is missing
 

@@ -302,6 +302,8 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
   p.n_loc = tm->n_loc;
   p.j_begin = tm->j_begin;
   p.m = tm->m;
+  p.w_begin = 0;
+  p.w_end = tm->m * tm->n_loc;
   p.o = tm->o;
   p.Wp = tm->Wp;
   p.Wq = tm->Wq;
@@ -486,10 +488,15 @@ void epoch_keys(tmg_machine* tm, int32_t epoch) {
   tm->cur_epoch = epoch;
 }
 
-void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, bool with_delta) {
+void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, bool with_delta, int w_begin,
+                      int w_end) {
   tmg::TrainParams p = make_params(tm, pool);
   p.t_begin = t0;
   p.t_end = t1;
+  if (w_end >= 0) {  // one wave of the clause order
+    p.w_begin = w_begin;
+    p.w_end = w_end;
+  }
   if (with_delta && !pool->peers.empty())
     fail(TMG_EINVAL, "pool has peer tally replicas attached: the windowed exchange would count every change twice "
                      "(detach with tmg_pool_set_peers(pool, NULL, 0))");
@@ -505,6 +512,12 @@ void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, b
   if (!ok) fail(TMG_ERUNTIME, "no async kernel instantiation for this shape");
   CK(cudaGetLastError());
   tm->entries_dirty = true;
+}
+
+int resident_clause_warps(tmg_machine* tm, tmg_pool* pool, int* warps_per_cta) {
+  const tmg::TrainParams p = make_params(tm, pool);
+  DeviceGuard dg(tm->device);
+  return tmg::train_async_resident_warps(p, tm->B, tm->NW, warps_per_cta);
 }
 
 // Class sums of q literal rows (x-plane words at xplane, row stride 2*Wp)

@@ -204,7 +204,12 @@ void reset_state(tmg_machine* tm);
 tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int jb, int je, int all_positive = 0);
 void upload_order(tmg_machine* tm, tmg_pool* pool, int32_t epoch);
 void epoch_keys(tmg_machine* tm, int32_t epoch);
-void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, bool with_delta);
+// Steps [t0, t1) of every clause's pass — of the clause-order warps
+// [w_begin, w_end) only when w_end >= 0 (one wave of a sharded epoch).
+void run_async_window(tmg_machine* tm, tmg_pool* pool, int64_t t0, int64_t t1, bool with_delta, int w_begin = 0,
+                      int w_end = -1);
+// Clause warps one launch keeps resident on tm's device, and the CTA width.
+int resident_clause_warps(tmg_machine* tm, tmg_pool* pool, int* warps_per_cta);
 void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool train_mode, int32_t* d_out,
                        uint32_t* prev, const uint32_t* lit_t = nullptr);
 const uint32_t* pool_lit_t(tmg_machine* tm, const tmg_pool* pool);

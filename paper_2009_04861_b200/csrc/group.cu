@@ -4,13 +4,12 @@
 // train_epoch_parallel(tm, pool, workers, epoch) (trainer.cpp:181-242): W
 // threads update disjoint clauses and share the q x m tallies through
 // relaxed atomics (pool.hpp:57-59, pool.cpp:93-106). Here the clause pairs of
-// every class are split over GPUs; each shard's kernel updates its own tally
-// replica, and the replicas exchange their changes every window of the
-// clause passes: the window's deltas are snapshotted on the shard's stream,
-// summed over all shards on a side stream while the next window runs, and the
-// other shards' share (sum - own) is added before the window after next — the
-// same relaxed, lock-free tally semantics as the reference's threads, with at
-// most two windows of extra staleness.
+// every class are split over GPUs; each shard's epoch is one kernel launch
+// over its clauses that updates its own tally replica and a cumulative delta
+// buffer, and while the kernels run, a host loop on high-priority side streams
+// exchanges the deltas (sharded_epoch): every other shard's changes reach a
+// replica one exchange interval (~1/16 of an epoch) after they happen — the
+// same relaxed, lock-free tally semantics as the reference's threads.
 //
 // Two ways to hold the shards:
 //   * one process, several devices (tmg_machine_create_devices; the C++
@@ -29,9 +28,11 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <thread>
 
 #include "engine.h"
 
@@ -62,7 +63,15 @@ Nccl& nccl() {
   std::lock_guard<std::mutex> lock(mu);
   if (n.tried) return n;
   n.tried = true;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  // The copy the process already has (torch's, when torch is imported) —
+  // loading a second, older libnccl.so.2 first would make the later
+  // libtorch_cuda.so bind to it by SONAME and fail on newer symbols. Else
+  // $TMG_NCCL_LIB (the Python package points it at the NCCL wheel torch
+  // uses), else the system's.
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  const char* env = std::getenv("TMG_NCCL_LIB");
+  if (!h && env && *env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) {
     const char* e = dlerror();
     n.why = e ? e : "dlopen(libnccl.so.2) failed";
@@ -104,6 +113,19 @@ __global__ void peer_sum_kernel(int32_t* __restrict__ out, PeerSrc s, int64_t co
   }
 }
 
+// tallies += (other shards' deltas since the last exchange) =
+// (sum_new - sum_prev) - (own_new - own_prev), atomically: the epoch kernel
+// is adding to the same tallies meanwhile.
+__global__ void stream_apply_kernel(int32_t* __restrict__ tallies, const int32_t* __restrict__ red_new,
+                                    const int32_t* __restrict__ red_prev, const int32_t* __restrict__ own_new,
+                                    const int32_t* __restrict__ own_prev, int64_t count) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t v = (red_new[i] - red_prev[i]) - (own_new[i] - own_prev[i]);
+    if (v) atomicAdd(tallies + i, v);
+  }
+}
+
 struct Exchange {
   bool use_nccl = false;
   int nranks = 1, rank = 0;           // processes (tmg_comm); 1 for a one-process group
@@ -111,11 +133,17 @@ struct Exchange {
   std::vector<ncclComm_t> comms;      // use_nccl: one per local shard
   std::vector<cudaStream_t> cstreams;  // side stream per local shard
   struct Slot {
+    // snap[b]: the shard's cumulative tally deltas of this epoch as copied at
+    // exchange b, plus one trailing element: 1 once the shard's kernel has
+    // finished; red[b]: its sum over every shard
     DevBuf<int32_t> snap[2], red[2];
     cudaEvent_t snap_ev[2] = {nullptr, nullptr}, red_ev[2] = {nullptr, nullptr};
+    cudaEvent_t done = nullptr;  // the shard's epoch kernel finished
+    int32_t* flag = nullptr;     // pinned host: [0] done flag to send, [1] reduced done count
   };
   std::vector<std::unique_ptr<Slot>> slots;
   int64_t count = 0;
+  double interval_s = 0.002;  // time between exchanges (adapted to the epoch length)
   DevBuf<unsigned long long> scratch64;  // cross-rank event / sum reductions
   DevBuf<int32_t> scratch32;
 
@@ -124,11 +152,23 @@ struct Exchange {
     cstreams.resize(devices.size());
     for (size_t k = 0; k < devices.size(); ++k) {
       DeviceGuard dg(devices[k]);
-      CK(cudaStreamCreateWithFlags(&cstreams[k], cudaStreamNonBlocking));
+      // the exchange's copies, sums and applies run beside the epoch kernel,
+      // which fills every SM: the highest priority puts them on the next free slot
+      int lo = 0, hi = 0;
+      CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      CK(cudaStreamCreateWithPriority(&cstreams[k], cudaStreamNonBlocking, hi));
       for (int b = 0; b < 2; ++b) {
         CK(cudaEventCreateWithFlags(&slots[k]->snap_ev[b], cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&slots[k]->red_ev[b], cudaEventDisableTiming));
       }
+      CK(cudaEventCreateWithFlags(&slots[k]->done, cudaEventDisableTiming));
+      CK(cudaMallocHost(reinterpret_cast<void**>(&slots[k]->flag), 2 * sizeof(int32_t)));
+      // Load the exchange's kernels now: with lazy module loading a first
+      // launch beside a running epoch kernel would wait for the device to
+      // drain, i.e. the first epoch's exchanges would all happen at its end.
+      cudaFuncAttributes attr;
+      CK(cudaFuncGetAttributes(&attr, peer_sum_kernel));
+      CK(cudaFuncGetAttributes(&attr, stream_apply_kernel));
     }
   }
 
@@ -155,6 +195,8 @@ struct Exchange {
           if (slots[k]->snap_ev[b]) cudaEventDestroy(slots[k]->snap_ev[b]);
           if (slots[k]->red_ev[b]) cudaEventDestroy(slots[k]->red_ev[b]);
         }
+      if (k < slots.size() && slots[k]->done) cudaEventDestroy(slots[k]->done);
+      if (k < slots.size() && slots[k]->flag) cudaFreeHost(slots[k]->flag);
       if (k < comms.size() && comms[k] && nccl().CommDestroy) nccl().CommDestroy(comms[k]);
       if (k < cstreams.size() && cstreams[k]) cudaStreamDestroy(cstreams[k]);
     }
@@ -300,12 +342,27 @@ std::vector<tmg_pool*> replicas_for(tmg_machine* g, tmg_pool* pool) {
 }
 
 // ----------------------------------------------------------- the epoch ---
+// One asynchronous epoch of every shard, with the tally replicas exchanged
+// while the epochs run. Each shard's epoch is ONE launch over all its clauses
+// — the schedule of a single-GPU epoch (clause warps retire and the next take
+// their place), which learns measurably better than cutting every clause's
+// pass into lock-step windows. The kernels add every tally
+// change to their own replica and to a cumulative delta buffer that is never
+// reset during the epoch; a host loop on high-priority side streams copies the
+// cumulative deltas (copy engine), sums them over all shards (NCCL or the
+// peer-memory kernel) and adds to each replica the others' growth since the
+// previous exchange. A 32-bit copy of a word that kernels are RED-adding to
+// reads some prefix of those adds, so every change is counted exactly once
+// over the epoch; the loop ends with an exchange taken after every shard's
+// kernel has finished (a done flag rides in the sums).
 void sharded_epoch(Exchange& X, const std::vector<tmg_machine*>& shards, const std::vector<tmg_pool*>& pools,
                    int32_t epoch, int windows, std::vector<uint64_t>& events) {
   const size_t n = shards.size();
   const int64_t q = pools[0]->q;
   const int m = shards[0]->m;
-  X.ensure(q * m);
+  const int64_t cnt = q * m;
+  X.ensure(cnt + 1);
+  const auto t_begin = std::chrono::steady_clock::now();
   for (size_t k = 0; k < n; ++k) {
     tmg_machine* tm = shards[k];
     DeviceGuard dg(tm->device);
@@ -314,33 +371,65 @@ void sharded_epoch(Exchange& X, const std::vector<tmg_machine*>& shards, const s
     epoch_keys(tm, epoch);
     CK(cudaMemsetAsync(tm->events.ptr, 0, tm->events.bytes(), tm->stream));
     CK(cudaMemsetAsync(pools[k]->delta.ptr, 0, pools[k]->delta.bytes(), tm->stream));
-  }
-  const int64_t W = std::max<int64_t>(1, std::min<int64_t>(windows, q));
-  const size_t bytes = static_cast<size_t>(q) * m * sizeof(int32_t);
-  auto apply = [&](int b) {  // tallies += (sum over shards) - own, for window b's snapshot
-    for (size_t k = 0; k < n; ++k) {
-      DeviceGuard dg(shards[k]->device);
-      X.wait_reduced(k, b, shards[k]->stream);
-      tmg::apply_snapshot_launch(pools[k]->tallies.ptr, X.slots[k]->red[b].ptr, X.slots[k]->snap[b].ptr, q * m,
-                                 shards[k]->stream);
-      CK(cudaGetLastError());
+    for (int b = 0; b < 2; ++b) {  // the "previous" snapshot and sum of exchange 0 are zero
+      CK(cudaMemsetAsync(X.slots[k]->snap[b].ptr, 0, X.slots[k]->snap[b].bytes(), tm->stream));
+      CK(cudaMemsetAsync(X.slots[k]->red[b].ptr, 0, X.slots[k]->red[b].bytes(), tm->stream));
     }
-  };
-  for (int64_t w = 0; w < W; ++w) {
-    const int b = static_cast<int>(w & 1);
-    const int64_t t0 = q * w / W, t1 = q * (w + 1) / W;
-    for (size_t k = 0; k < n; ++k) {
-      tmg_machine* tm = shards[k];
-      DeviceGuard dg(tm->device);
-      run_async_window(tm, pools[k], t0, t1, true);
-      CK(cudaMemcpyAsync(X.slots[k]->snap[b].ptr, pools[k]->delta.ptr, bytes, cudaMemcpyDeviceToDevice, tm->stream));
-      CK(cudaMemsetAsync(pools[k]->delta.ptr, 0, bytes, tm->stream));
-      CK(cudaEventRecord(X.slots[k]->snap_ev[b], tm->stream));
+    CK(cudaStreamSynchronize(tm->stream));
+  }
+  for (size_t k = 0; k < n; ++k) {  // the epochs: one launch per shard
+    tmg_machine* tm = shards[k];
+    DeviceGuard dg(tm->device);
+    run_async_window(tm, pools[k], 0, q, true);
+    CK(cudaEventRecord(X.slots[k]->done, tm->stream));
+  }
+  const int total = static_cast<int>(n) * X.nranks;
+  const auto interval = std::chrono::duration<double>(X.interval_s);
+  for (int64_t it = 0;; ++it) {
+    const int b = static_cast<int>(it & 1), p = b ^ 1;
+    // wait for the interval or for every local shard to finish
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      bool all = true;
+      for (size_t k = 0; k < n && all; ++k) all = cudaEventQuery(X.slots[k]->done) == cudaSuccess;
+      if (all || std::chrono::steady_clock::now() - t0 >= interval) break;
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    for (size_t k = 0; k < n; ++k) {  // snapshot the cumulative deltas (+ done flag)
+      DeviceGuard dg(shards[k]->device);
+      Exchange::Slot& sl = *X.slots[k];
+      sl.flag[0] = cudaEventQuery(sl.done) == cudaSuccess ? 1 : 0;  // before the copy: a done shard's copy is final
+      X.wait_reduced(k, b, X.cstreams[k]);  // slot b's last readers (two exchanges ago) are done
+      CK(cudaMemcpyAsync(sl.snap[b].ptr, pools[k]->delta.ptr, static_cast<size_t>(cnt) * 4, cudaMemcpyDeviceToDevice,
+                         X.cstreams[k]));
+      CK(cudaMemcpyAsync(sl.snap[b].ptr + cnt, sl.flag, 4, cudaMemcpyHostToDevice, X.cstreams[k]));
+      CK(cudaEventRecord(sl.snap_ev[b], X.cstreams[k]));
     }
     X.reduce(b);
-    if (w >= 1) apply(static_cast<int>((w - 1) & 1));
+    for (size_t k = 0; k < n; ++k) {  // replica += the other shards' growth since the last exchange
+      DeviceGuard dg(shards[k]->device);
+      Exchange::Slot& sl = *X.slots[k];
+      X.wait_reduced(k, b, X.cstreams[k]);
+      tmg::count_launch();
+      stream_apply_kernel<<<148, 256, 0, X.cstreams[k]>>>(pools[k]->tallies.ptr, sl.red[b].ptr, sl.red[p].ptr,
+                                                          sl.snap[b].ptr, sl.snap[p].ptr, cnt);
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(sl.flag + 1, sl.red[b].ptr + cnt, 4, cudaMemcpyDeviceToHost, X.cstreams[k]));
+    }
+    for (size_t k = 0; k < n; ++k) {  // (also frees the pinned flags for the next exchange)
+      DeviceGuard dg(shards[k]->device);
+      CK(cudaStreamSynchronize(X.cstreams[k]));
+    }
+    if (X.slots[0]->flag[1] >= total) break;  // every shard's final deltas are in this exchange
   }
-  apply(static_cast<int>((W - 1) & 1));
+  for (size_t k = 0; k < n; ++k) {
+    DeviceGuard dg(shards[k]->device);
+    CK(cudaStreamSynchronize(X.cstreams[k]));
+    CK(cudaStreamSynchronize(shards[k]->stream));
+  }
+  // aim at `windows` exchanges in the next epoch of similar length
+  const double took = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count();
+  X.interval_s = std::max(2e-4, took / std::max(1, windows));
   events.assign(static_cast<size_t>(2 * m), 0);
   std::vector<unsigned long long> ev(static_cast<size_t>(2 * m));
   for (size_t k = 0; k < n; ++k) {

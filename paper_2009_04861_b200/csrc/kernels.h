@@ -54,6 +54,9 @@ struct TrainParams {
   // 1 = interleaved (warp w -> class w % m, clause w / m), so each resident
   // wave holds a slice of every class instead of all clauses of a few.
   int32_t interleave;
+  // Launch over clause-order warps [w_begin, w_end) only (a wave of a
+  // sharded epoch); the whole machine is [0, m * n_loc).
+  int32_t w_begin, w_end;
   int32_t all_positive;
   uint32_t thr_high, thr_low;  // async: P(u < p) thresholds as 32-bit fixed point
   BernThresholds bern;         // the same, split for the sampler
@@ -136,6 +139,10 @@ struct BitsEvalParams {
 // B (plane count) and NW (words per lane per part) instantiations.
 bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks);
 bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks);
+// Clause warps the async kernel for this shape keeps resident on the device
+// at once (one wave), and the warps per CTA (waves are cut at CTA multiples).
+int train_async_resident_warps(const TrainParams& p, int B, int NW, int* warps_per_cta);
+int train_async_smem_resident_warps(const TrainParams& p, int B, int NW, int* warps_per_cta);
 bool train_mirror_launch(const TrainParams& p, const MirrorParams& mp, int B, int NW, cudaStream_t s);
 bool type_i_async_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, uint32_t i, int out, int B, int NW,
                               cudaStream_t s);

@@ -42,8 +42,8 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   load_alias(P, atab);
   const int lane = static_cast<int>(lane_id());
   const AliasRef aref = lane_alias(atab, lane);
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= P.m * P.n_loc) return;
+  const int w = P.w_begin + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= P.w_end) return;
   const int lc = clause_of_warp(P, w, blockDim.x >> 5);
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(32) type_i_async_once_kernel(TrainParams P, ui
 
 template <int NW, int B>
 void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
-  const int clauses = p.m * p.n_loc;
+  const int clauses = p.w_end - p.w_begin;
   const int warps_per_block = 4;
   const int grid = (clauses + warps_per_block - 1) / warps_per_block;
   if (blocks) *blocks = grid;
@@ -646,6 +646,26 @@ void launch_mirror(const TrainParams& p, const MirrorParams& mp, cudaStream_t s)
                          static_cast<int>(shm));
   count_launch();
   train_mirror_kernel<NW, B><<<1, 32, shm, s>>>(p, mp);
+}
+
+template <int NW, int B>
+int resident_async() {
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, train_async_kernel<NW, B, true>, 128, 0);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms * 4;
+}
+
+template <int B>
+int resident_async_nw(int NW) {
+  switch (NW) {
+    case 1: return resident_async<1, B>();
+    case 2: return resident_async<2, B>();
+    case 3: return resident_async<3, B>();
+    case 4: return resident_async<4, B>();
+    default: return 0;
+  }
 }
 
 template <int B>
@@ -717,6 +737,17 @@ bool type_i_async_once_launch(const TrainParams& p, uint32_t* state, uint32_t g,
   TMG_ONCE(3, 4) TMG_ONCE(3, 8) TMG_ONCE(3, 15) TMG_ONCE(4, 4) TMG_ONCE(4, 8) TMG_ONCE(4, 15)
 #undef TMG_ONCE
   return false;
+}
+
+int train_async_resident_warps(const TrainParams& p, int B, int NW, int* warps_per_cta) {
+  if (NW > 4) return train_async_smem_resident_warps(p, B, NW, warps_per_cta);
+  *warps_per_cta = 4;
+  switch (B) {
+    case 4: return resident_async_nw<4>(NW);
+    case 8: return resident_async_nw<8>(NW);
+    case 15: return resident_async_nw<15>(NW);
+    default: return 0;
+  }
 }
 
 bool train_async_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {

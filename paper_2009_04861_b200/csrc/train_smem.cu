@@ -165,8 +165,8 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   const int lane = threadIdx.x & 31;
   const AliasRef aref = lane_alias(atab, lane);
   const int wib = threadIdx.x >> 5;
-  const int w = blockIdx.x * cpb + wib;
-  if (w >= P.m * P.n_loc) return;
+  const int w = P.w_begin + blockIdx.x * cpb + wib;
+  if (w >= P.w_end) return;
   const int lc = clause_of_warp(P, w, cpb);
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
@@ -260,6 +260,29 @@ size_t smem_bytes(int B, int Wp, int cpb) {
   return sizeof(uint32_t) * (static_cast<size_t>(cpb) * B * 2 * Wp + kAliasWordsPacked);
 }
 
+// Clauses per CTA: the count (<= kSmemMaxCpb) with the most resident warps
+// per SM (every CTA carries its own alias table); returns those warps per SM
+// (0: no count fits in shared memory — planes in place).
+template <int NW, int B, bool P2>
+int smem_plan(const TrainParams& p, int* cpb_out) {
+  int cpb = 1, best = 0;
+  for (int c = 1; c <= kSmemMaxCpb; ++c) {
+    const size_t b = smem_bytes(B, p.Wp, c);
+    if (b > kSmemMax) break;
+    if (b > 48 * 1024)
+      cudaFuncSetAttribute(train_async_smem_kernel<NW, B, P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(b));
+    int ctas = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, train_async_smem_kernel<NW, B, P2>, 32 * c, b);
+    if (ctas * c > best) {
+      best = ctas * c;
+      cpb = c;
+    }
+  }
+  *cpb_out = cpb;
+  return best;
+}
+
 template <int NW, int B, bool P2>
 bool launch_smem_p2(const TrainParams& p, cudaStream_t s, int* blocks) {
   // Clauses per CTA: the count (<= kSmemMaxCpb) with the most resident warps
@@ -279,7 +302,7 @@ bool launch_smem_p2(const TrainParams& p, cudaStream_t s, int* blocks) {
     }
   }
   const size_t shm = smem_bytes(B, p.Wp, cpb);
-  const int clauses = p.m * p.n_loc;
+  const int clauses = p.w_end - p.w_begin;
   if (shm > kSmemMax) {
     if constexpr (NW != 0) {
       return false;
@@ -356,6 +379,23 @@ bool type_i_smem_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, 
     if (B == 15) return p2 ? go(type_i_smem_once_kernel<0, 15, true>) : go(type_i_smem_once_kernel<0, 15, false>);
   }
   return false;
+}
+
+int train_async_smem_resident_warps(const TrainParams& p, int B, int NW, int* warps_per_cta) {
+  const int nw = compiled_width(NW) ? NW : 0;
+  const bool p2 = p.lo == 0 && p.hi == (1u << B) - 1u;
+  int cpb = 1, per_sm = 0, dev = 0, sms = 0;
+#define TMG_PLAN(nw_, b_)                                                                          \
+  if (nw == nw_ && B == b_) per_sm = p2 ? smem_plan<nw_, b_, true>(p, &cpb) : smem_plan<nw_, b_, false>(p, &cpb);
+#define TMG_PLAN_B(nw_) TMG_PLAN(nw_, 4) TMG_PLAN(nw_, 8) TMG_PLAN(nw_, 15)
+  TMG_PLAN_B(6) TMG_PLAN_B(8) TMG_PLAN_B(10) TMG_PLAN_B(12) TMG_PLAN_B(16) TMG_PLAN_B(0)
+#undef TMG_PLAN_B
+#undef TMG_PLAN
+  if (per_sm == 0) per_sm = 8, cpb = 1;  // in place: one clause per CTA
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  *warps_per_cta = cpb;
+  return per_sm * sms;
 }
 
 bool train_async_smem_launch(const TrainParams& p, int B, int NW, cudaStream_t s, int* blocks) {
