@@ -553,13 +553,20 @@ void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool 
   const int64_t blocks = (q + 1023) / 1024;
   const int64_t resident = int64_t(148) * 5;
   const int64_t steps = blocks * tm->lists_total;  // warp-level literal loads
-  const int64_t waves = std::min<int64_t>(6, std::max<int64_t>(2, steps / (resident * 8 * 1024)));
+  const char* wv = std::getenv("TMG_EVAL_MINWAVES");
+  const int64_t min_waves = wv ? std::atoi(wv) : 3;
+  const int64_t waves = std::min<int64_t>(6, std::max<int64_t>(min_waves, steps / (resident * 8 * 1024)));
   int64_t chunks = (resident * waves + blocks * tm->m - 1) / (blocks * tm->m);
   chunks = std::max<int64_t>(chunks, (tm->n_loc + 2039) / 2040);
   chunks = std::min<int64_t>(chunks, std::max(1, tm->n_loc / 32));
   chunks = std::max<int64_t>(chunks, (tm->n_loc + 2039) / 2040);
   chunks = std::min<int64_t>(chunks, 65535 / tm->m);
   e.cta_clauses = static_cast<int32_t>((tm->n_loc + chunks - 1) / chunks);
+  {
+    const char* dyn = std::getenv("TMG_EVAL_DYNAMIC");
+    const int64_t avg = tm->lists_total / std::max(1, tm->clauses());
+    e.dynamic = dyn ? (dyn[0] == '1') : (avg > 16 ? 1 : 0);
+  }
   e.chunks = static_cast<int32_t>((tm->n_loc + e.cta_clauses - 1) / e.cta_clauses);
   CK(cudaMemsetAsync(d_out, 0, static_cast<size_t>(q) * tm->m * 4, tm->stream));
   tmg::eval_bits_launch(e, train_mode, tm->stream);

@@ -208,6 +208,37 @@ __device__ __forceinline__ uint32_t fold_columns(const uint32_t* __restrict__ ls
   return acc;
 }
 
+// Short lists (a few literals, e.g. MNIST-shaped machines): the positive and
+// negated parts in one loop of 8 loads — each aligned group of 4 entries is
+// all positive or all negated (np is a multiple of 4), so the group's AND
+// feeds `pos` and its OR feeds `neg` under a warp-uniform test.
+__device__ __forceinline__ uint32_t fold_short(const uint32_t* __restrict__ lst, int len, int np,
+                                               const char* __restrict__ col, uint32_t row_bytes, uint32_t pos) {
+  const uint4* p = reinterpret_cast<const uint4*>(lst);
+  uint32_t neg = 0u;
+  int k = 0;
+  for (; k + 8 <= len; k += 8, p += 2) {
+    const uint4 a = __ldg(p), b = __ldg(p + 1);
+    const uint32_t v0 = column(col, a.x, row_bytes), v1 = column(col, a.y, row_bytes);
+    const uint32_t v2 = column(col, a.z, row_bytes), v3 = column(col, a.w, row_bytes);
+    const uint32_t v4 = column(col, b.x, row_bytes), v5 = column(col, b.y, row_bytes);
+    const uint32_t v6 = column(col, b.z, row_bytes), v7 = column(col, b.w, row_bytes);
+    if (k < np) pos &= v0 & v1 & v2 & v3;
+    else neg |= v0 | v1 | v2 | v3;
+    if (k + 4 < np) pos &= v4 & v5 & v6 & v7;
+    else neg |= v4 | v5 | v6 | v7;
+    if (!__any_sync(kFull, (pos & ~neg) != 0u)) return 0u;  // every example falsified
+  }
+  if (k < len) {
+    const uint4 a = __ldg(p);
+    const uint32_t v0 = column(col, a.x, row_bytes), v1 = column(col, a.y, row_bytes);
+    const uint32_t v2 = column(col, a.z, row_bytes), v3 = column(col, a.w, row_bytes);
+    if (k < np) pos &= v0 & v1 & v2 & v3;
+    else neg |= v0 | v1 | v2 | v3;
+  }
+  return pos & ~neg;
+}
+
 template <bool TRAIN>
 __global__ void __launch_bounds__(kEvalWarps * 32, 5) eval_bits_kernel(BitsEvalParams P) {
   __shared__ uint32_t red[kEvalWarps][kSumPlanes][32];
@@ -237,17 +268,26 @@ __global__ void __launch_bounds__(kEvalWarps * 32, 5) eval_bits_kernel(BitsEvalP
     uint32_t acc = valid;  // empty clause: Train 1
     if (TRAIN || len != 0) {  // empty clause: Predict 0 (core.hpp:211-213)
       const uint32_t* lst = P.lists + (static_cast<size_t>(static_cast<uint32_t>(mt.x)) << 2);
-      acc = fold_columns<true>(lst, np, col, row_bytes, acc, 0u);
-      if (__any_sync(kFull, acc != 0u) && len > np) acc &= ~fold_columns<false>(lst + np, len - np, col, row_bytes, 0u, acc);
+      if (!P.dynamic) {
+        acc = fold_short(lst, len, np, col, row_bytes, acc);
+      } else {
+        acc = fold_columns<true>(lst, np, col, row_bytes, acc, 0u);
+        if (__any_sync(kFull, acc != 0u) && len > np)
+          acc &= ~fold_columns<false>(lst + np, len - np, col, row_bytes, 0u, acc);
+      }
       if (TRAIN && P.prev != nullptr && gw < P.Wq)
         P.prev[(static_cast<size_t>(c) * P.n_loc + jl) * P.Wq + gw] = acc;
       const int j = P.j_begin + jl;
       if (P.all_positive || !(j & 1)) count_word<true>(cnt, acc);
       else count_word<false>(cnt, acc);
     }
-    int nj = 0;
-    if (lane == 0) nj = atomicAdd(&next_clause, 1);
-    jl = __shfl_sync(kFull, nj, 0);
+    if (P.dynamic) {
+      int nj = 0;
+      if (lane == 0) nj = atomicAdd(&next_clause, 1);
+      jl = __shfl_sync(kFull, nj, 0);
+    } else {
+      jl += kEvalWarps;  // short lists: a fixed stride, no claim on the critical path
+    }
   }
   // CTA reduction of the warps' counters: bit-sliced ripple adds in shared memory.
 #pragma unroll

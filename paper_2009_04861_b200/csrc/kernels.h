@@ -131,6 +131,8 @@ struct BitsEvalParams {
   uint32_t* prev;            // refresh mode: [m*n_loc][Wq]
   int32_t n_loc, j_begin, m, Wq;
   int32_t cta_clauses, chunks;  // clauses per CTA (<= 2040), CTAs per class
+  int32_t dynamic;              // long lists: clauses handed out through a shared counter, two
+                                // folds of 16 loads; short lists: by stride, one fold of 8 loads
   int32_t all_positive;         // regression head: every clause votes +1
   int64_t q;
   int32_t* sums;  // [q][m], accumulated with atomics
