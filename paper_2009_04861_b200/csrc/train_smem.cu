@@ -33,19 +33,59 @@ constexpr int kSmemUnroll = TMG_SMEM_UNROLL;
 constexpr int kSmemMaxCpb = TMG_SMEM_MAXCPB;
 constexpr size_t kSmemMax = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 
-template <int B>
+// One clause's automaton planes in shared memory (or, INPLACE, in HBM with
+// the global [plane][part][Wp] layout). The shared-memory copy (QUAD) keeps,
+// per part, the planes below the top one in 16-byte quads
+// ([quad][Wp] of uint4: one LDS.128 / STS.128 reads or writes 4 planes of a
+// word; lanes hold consecutive words, so a warp's access is 512 contiguous
+// bytes, conflict-free), the 1-3 planes left over as single-plane arrays, and
+// the top plane (the include mask, read by every evaluation) as its own
+// conflict-free array: B = 8 takes 5 accesses per word instead of 8, B = 15
+// takes 6 instead of 15, with no padding.
+template <int B, bool QUAD = false>
 struct SmemPlanes {
-  uint32_t* s;  // [B][2][Wp] of this warp
+  static constexpr int KQ = QUAD ? (B - 1) / 4 : 0;  // full quads below the top plane
+  uint32_t* s;  // this warp's planes
   int Wp;
+  __host__ __device__ static size_t index(int b, int part, int w, int Wp) {
+    if (!QUAD) return (static_cast<size_t>(b) * 2 + part) * Wp + w;
+    const size_t base = static_cast<size_t>(part) * B * Wp;
+    if (b < 4 * KQ) return base + (static_cast<size_t>(b / 4) * Wp + w) * 4 + b % 4;
+    return base + static_cast<size_t>(b) * Wp + w;  // leftover planes, then the top plane at b = B - 1
+  }
   __device__ __forceinline__ void get(int part, int w, Planes<B>& out) const {
+    if constexpr (QUAD) {
+      const uint32_t* base = s + static_cast<size_t>(part) * B * Wp;
 #pragma unroll
-    for (int b = 0; b < B; ++b) out.p[b] = s[(b * 2 + part) * Wp + w];
+      for (int q = 0; q < KQ; ++q) {
+        const uint4 v = reinterpret_cast<const uint4*>(base)[static_cast<size_t>(q) * Wp + w];
+        out.p[4 * q] = v.x;
+        out.p[4 * q + 1] = v.y;
+        out.p[4 * q + 2] = v.z;
+        out.p[4 * q + 3] = v.w;
+      }
+#pragma unroll
+      for (int b = 4 * KQ; b < B; ++b) out.p[b] = base[static_cast<size_t>(b) * Wp + w];
+    } else {
+#pragma unroll
+      for (int b = 0; b < B; ++b) out.p[b] = s[(b * 2 + part) * Wp + w];
+    }
   }
   __device__ __forceinline__ void put(int part, int w, const Planes<B>& in) {
+    if constexpr (QUAD) {
+      uint32_t* base = s + static_cast<size_t>(part) * B * Wp;
 #pragma unroll
-    for (int b = 0; b < B; ++b) s[(b * 2 + part) * Wp + w] = in.p[b];
+      for (int q = 0; q < KQ; ++q)
+        reinterpret_cast<uint4*>(base)[static_cast<size_t>(q) * Wp + w] =
+            make_uint4(in.p[4 * q], in.p[4 * q + 1], in.p[4 * q + 2], in.p[4 * q + 3]);
+#pragma unroll
+      for (int b = 4 * KQ; b < B; ++b) base[static_cast<size_t>(b) * Wp + w] = in.p[b];
+    } else {
+#pragma unroll
+      for (int b = 0; b < B; ++b) s[(b * 2 + part) * Wp + w] = in.p[b];
+    }
   }
-  __device__ __forceinline__ uint32_t top(int part, int w) const { return s[((B - 1) * 2 + part) * Wp + w]; }
+  __device__ __forceinline__ uint32_t top(int part, int w) const { return s[index(B - 1, part, w, Wp)]; }
 };
 
 // A step's literal row as seen by one lane: words p*32 + lane of the x- and
@@ -79,8 +119,8 @@ struct LitRow<0> {
   __device__ __forceinline__ int words() const { return Wp >> 5; }
 };
 
-template <int NW, int B>
-__device__ __forceinline__ int eval_train_smem(const SmemPlanes<B>& S, const LitRow<NW>& r, int lane) {
+template <int NW, typename SP>
+__device__ __forceinline__ int eval_train_smem(const SP& S, const LitRow<NW>& r, int lane) {
   uint32_t viol = 0, any = 0;
 #pragma unroll
   for (int p = 0; p < r.words(); ++p) {
@@ -102,8 +142,8 @@ __device__ __forceinline__ uint32_t valid_of(int w, int o) {
 // lane at a time, with the register kernel's draws (clause.cuh type_i_async):
 // alias patterns from Philox counters (clause, example, 2*word + part, 0),
 // or the bit-serial sampler when p_high != 1 - p_low.
-template <int NW, int B, bool P2, int OUT>
-__device__ __forceinline__ void type_i_smem_out(SmemPlanes<B>& S, const LitRow<NW>& r, const TrainParams& P,
+template <int NW, int B, bool P2, int OUT, typename SP>
+__device__ __forceinline__ void type_i_smem_out(SP& S, const LitRow<NW>& r, const TrainParams& P,
                                                 uint32_t g, uint32_t i32, int lane, AliasRef aref) {
   constexpr int before = OUT;
 #pragma unroll kSmemUnroll
@@ -139,8 +179,8 @@ __device__ __forceinline__ void type_i_smem_out(SmemPlanes<B>& S, const LitRow<N
 }
 
 // The clause output is warp-uniform: one branch, each arm with a constant one.
-template <int NW, int B, bool P2>
-__device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& r, int before, const TrainParams& P,
+template <int NW, int B, bool P2, typename SP>
+__device__ __forceinline__ void type_i_smem(SP& S, const LitRow<NW>& r, int before, const TrainParams& P,
                                             uint32_t g, uint32_t i32, int lane, AliasRef aref) {
   if (before)
     type_i_smem_out<NW, B, P2, 1>(S, r, P, g, i32, lane, aref);
@@ -155,10 +195,11 @@ __device__ __forceinline__ void type_i_smem(SmemPlanes<B>& S, const LitRow<NW>& 
 // place (every word is lane-owned), shared memory holds the alias table only.
 template <int NW, int B, bool P2, bool INPLACE = false>
 __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(TrainParams P) {
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem[];
+  using SP = SmemPlanes<B, !INPLACE>;  // shared-memory copies use the quad layout
   const int Wp = P.Wp;
   const int cpb = blockDim.x >> 5;
-  const size_t words = static_cast<size_t>(B) * 2 * Wp;
+  const size_t words = static_cast<size_t>(B) * 2 * Wp;  // per clause, either layout
   uint32_t* atab = INPLACE ? smem : smem + cpb * words;
   fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
   __syncthreads();
@@ -173,9 +214,12 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
   const bool positive = P.all_positive || (j & 1) == 0;
   uint32_t* st = P.state + static_cast<size_t>(lc) * words;
-  SmemPlanes<B> S{INPLACE ? st : smem + wib * words, Wp};
+  SP S{INPLACE ? st : smem + wib * words, Wp};
   if (!INPLACE)
-    for (size_t k = lane; k < words; k += 32) S.s[k] = st[k];
+    for (size_t k = lane; k < words; k += 32) {
+      const int b = static_cast<int>(k / (2 * Wp)), part = static_cast<int>((k / Wp) & 1), w = static_cast<int>(k % Wp);
+      S.s[SP::index(b, part, w, Wp)] = st[k];
+    }
   __syncwarp();
   uint32_t* prev_row = P.prev + static_cast<size_t>(lc) * P.Wq;
   const int64_t offset = clause_offset_dev(g, P.q);
@@ -202,7 +246,7 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
       const int64_t is = cd < 0 ? ~cd : cd;
       LitRow<NW> r;
       r.load(P.xplane + is * 2 * Wp + lane, Wp);
-      const int before = eval_train_smem<NW, B>(S, r, lane);
+      const int before = eval_train_smem<NW>(S, r, lane);
       int after = before;
       if (cd >= 0) {  // Type II (feedback.cpp:72-83)
         if (before) {
@@ -224,11 +268,11 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
             }
           }
           __syncwarp();
-          if (__any_sync(kFull, moved != 0)) after = eval_train_smem<NW, B>(S, r, lane);
+          if (__any_sync(kFull, moved != 0)) after = eval_train_smem<NW>(S, r, lane);
         }
       } else {  // Type I (feedback.cpp:32-70), one word pair at a time
         type_i_smem<NW, B, P2>(S, r, before, P, g, static_cast<uint32_t>(is), lane, aref);
-        after = eval_train_smem<NW, B>(S, r, lane);
+        after = eval_train_smem<NW>(S, r, lane);
       }
       outs |= static_cast<unsigned>(after) << sl;
     }
@@ -243,8 +287,10 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   __syncwarp();
   int cnt = 0;
   for (size_t k = lane; k < words; k += 32) {
-    if (!INPLACE) st[k] = S.s[k];
-    if (k >= static_cast<size_t>(B - 1) * 2 * Wp) cnt += __popc(S.s[k]);
+    const int b = static_cast<int>(k / (2 * Wp)), part = static_cast<int>((k / Wp) & 1), w = static_cast<int>(k % Wp);
+    const uint32_t v = S.s[SP::index(b, part, w, Wp)];
+    if (!INPLACE) st[k] = v;
+    if (b == B - 1) cnt += __popc(v);
   }
 #pragma unroll
   for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
@@ -336,18 +382,24 @@ bool launch_smem(const TrainParams& p, cudaStream_t s, int* blocks) {
 template <int NW, int B, bool P2>
 __global__ void __launch_bounds__(32) type_i_smem_once_kernel(TrainParams P, uint32_t* state, uint32_t g,
                                                               uint32_t i, int out) {
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem[];
+  using SP = SmemPlanes<B, true>;
   const int lane = threadIdx.x;
-  const size_t words = static_cast<size_t>(B) * 2 * P.Wp;
+  const int Wp = P.Wp;
+  const size_t words = static_cast<size_t>(B) * 2 * Wp;
   uint32_t* atab = smem + words;
   fill_alias_packed(atab, P.alias8, lane, 32);
-  for (size_t k = lane; k < words; k += 32) smem[k] = state[k];
+  auto at = [&](size_t k) {
+    return SP::index(static_cast<int>(k / (2 * Wp)), static_cast<int>((k / Wp) & 1), static_cast<int>(k % Wp), Wp);
+  };
+  for (size_t k = lane; k < words; k += 32) smem[at(k)] = state[k];
   __syncwarp();
-  SmemPlanes<B> S{smem, P.Wp};
+  SP S{smem, Wp};
   LitRow<NW> r;
-  r.load(P.xplane + lane, P.Wp);
+  r.load(P.xplane + lane, Wp);
   type_i_smem<NW, B, P2>(S, r, out, P, g, i, lane, lane_alias(atab, lane));
-  for (size_t k = lane; k < words; k += 32) state[k] = smem[k];
+  __syncwarp();
+  for (size_t k = lane; k < words; k += 32) state[k] = smem[at(k)];
 }
 
 // Row widths (words per lane) with a register-held literal row.
