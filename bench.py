@@ -243,6 +243,43 @@ def other_configs(local):
     return out
 
 
+def sharded_line(d, local) -> dict:
+    """The N > 1 machinery on this one GPU: the bench epoch
+    through a one-rank NCCL communicator (the code path of every rank of the
+    N-GPU run: streaming tally exchange, event all-reduce) against the plain
+    machine, and a two-shard machine on this GPU (peer-memory sums) against
+    one machine of the same clause count. Fresh epoch 0, best of 3."""
+    import paper_2009_04861_b200 as T
+    pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M_CLS, device=local)
+
+    def best(tm):
+        out = []
+        for _ in range(4):
+            tm.reset()
+            pool.reset_tallies()
+            out.append(T.train_epoch_parallel(tm, pool, 1, 0).seconds * 1e3)
+        return min(out[1:])
+
+    cfg = T.TMConfig(clauses=N_CLAUSES, margin=MARGIN, specificity=SPEC, state_depth=STATE_N, seed=TM_SEED)
+    out = {"plain_ms": best(T.MultiClassTM(cfg, O_FEAT, M_CLS, device=local))}
+    ok, why = T.nccl_available()
+    if ok:
+        comm = T.Comm(T.Comm.unique_id(), 1, 0, local)
+        tm = T.MultiClassTM(cfg, O_FEAT, M_CLS, device=local, clause_range=(0, N_CLAUSES))
+        tm.attach_comm(comm)
+        out["one_rank_comm_ms"] = best(tm)
+        out["one_rank_comm_overhead"] = out["one_rank_comm_ms"] / out["plain_ms"]
+        tm.attach_comm(None)
+        del tm, comm
+    else:
+        out["nccl"] = why
+    cfg2 = T.TMConfig(clauses=2 * N_CLAUSES, margin=MARGIN, specificity=SPEC, state_depth=STATE_N, seed=TM_SEED)
+    out["plain_2x_clauses_ms"] = best(T.MultiClassTM(cfg2, O_FEAT, M_CLS, device=local))
+    out["two_shards_one_gpu_ms"] = best(T.MultiClassTM(cfg2, O_FEAT, M_CLS, devices=[local, local]))
+    out["two_shards_overhead"] = out["two_shards_one_gpu_ms"] / out["plain_2x_clauses_ms"]
+    return out
+
+
 def sequential_line(local, with_ref: bool) -> dict:
     """train_epoch_sequential, the reference's classic
     trainer replayed bit-exactly on the GPU (gate scan with xoshiro jump-ahead,
@@ -583,6 +620,7 @@ def run_ours(args):
         if not args.no_other_configs:
             line["other_configs"] = other_configs(local)
             line["sequential_trainer"] = sequential_line(local, not args.no_cpu)
+            line["sharded_path"] = sharded_line(d, local)
     # ---- CPU reference beside it (rank 0, N=1 only)
     if world == 1 and not args.no_cpu and os.path.exists(REF_DRIVER):
         cores = os.cpu_count() or 1
