@@ -37,6 +37,11 @@ CASES = {
                          noise=0.0, data_seed=2352),
     "imdb_q12000": dict(data="imdb", q=12000, qtest=4000, clauses=10000, T=100, s=15.0, epochs=2,
                         noise=0.0, data_seed=10000),
+    # the reference's own one-worker schedule at the IMDb shape (the band)
+    "imdb_q4000_w1": dict(data="imdb", q=4000, qtest=2000, clauses=10000, T=100, s=15.0, epochs=2,
+                          noise=0.0, data_seed=10000, workers=1, seeds=3),
+    "imdb_q12000_w1": dict(data="imdb", q=12000, qtest=4000, clauses=10000, T=100, s=15.0, epochs=2,
+                           noise=0.0, data_seed=10000, workers=1, seeds=1),
     # The configuration bench.py times (BASELINE.json configs[1]) at its full
     # size: q = 60 000 training rows, 10 000 test rows, 3 epochs.
     "mnist_q60000": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
