@@ -224,9 +224,13 @@ def other_configs(local):
     parity tests cover their accuracy."""
     import paper_2009_04861_b200 as T
     from paper_2009_04861_b200 import synth
+    import torch
+    from paper_2009_04861_b200 import _capi
+    from paper_2009_04861_b200.tsetlin import machine_stream
     out = []
-    for kind, q, n, T_, s_, seed in (("fmnist", 60000, 8000, 100, 15.0, 2352), ("imdb", 25000, 10000, 100, 15.0, 10000)):
-        d = synth.make(kind, q, 0, seed)
+    for kind, q, qt, n, T_, s_, seed in (("fmnist", 60000, 10000, 8000, 100, 15.0, 2352),
+                                         ("imdb", 25000, 25000, 10000, 100, 15.0, 10000)):
+        d = synth.make(kind, q, qt, seed)
         tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=T_, specificity=s_, seed=TM_SEED), d.features, d.classes,
                             device=local)
         pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes, device=local)
@@ -235,11 +239,26 @@ def other_configs(local):
             pool.reset_tallies()
             rep = T.train_epoch_parallel(tm, pool, 1, 0)
         t = rep.device_seconds
+        # predict: class sums of the test rows on the trained state (device time)
+        test = T.ExamplePool(d.features, d.test_x, d.test_y, d.classes, device=local)
+        sums = torch.zeros(qt * d.classes, dtype=torch.int32, device=f"cuda:{local}")
+        stream = torch.cuda.ExternalStream(machine_stream(tm), device=f"cuda:{local}")
+        pms = []
+        for r in range(4):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _capi.check(_capi.lib().tmg_class_sums_device(tm.handle, test.handle, T.PREDICT, sums.data_ptr()))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            if r:
+                pms.append(e0.elapsed_time(e1))
         out.append({"workload": f"{kind} {d.features}b x {d.classes}c x {n} clauses, q={q}, fresh epoch 0",
                     "ms_per_epoch": t * 1e3, "examples_per_s": q / t,
                     "clause_literal_evals_per_s": d.classes * n * q * 2.0 * d.features / t,
-                    "feedback_events": rep.total_feedback_events()})
-        del tm, pool
+                    "feedback_events": rep.total_feedback_events(),
+                    "predict_test_rows": qt, "predict_ms": min(pms),
+                    "test_accuracy_after_epoch0": T.evaluate_accuracy(tm, test)})
+        del tm, pool, test
     return out
 
 
