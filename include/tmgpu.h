@@ -99,6 +99,9 @@ const char* tmg_last_error(void);
 int tmg_device_count(int32_t* count);
 /* Kernels launched by this library so far (process-wide counter). */
 unsigned long long tmg_kernel_launches(void);
+/* Device time of the last class-sum kernel of this machine (CUDA events
+ * around the eval_bits_kernel launch alone: bench.py's inference roofline). */
+int tmg_last_eval_kernel_ms(tmg_machine* tm, float* ms);
 /* The CUDA stream (cudaStream_t) a machine's work runs on. */
 int tmg_machine_stream(tmg_machine* tm, void** stream);
 /* Statistical probe of the asynchronous Type I path (criterion

@@ -75,6 +75,7 @@ SIGNATURES = {
     "tmg_bind_bank": (C.c_int, [P, I32, I64]),
     "tmg_machine_create_devices": (C.c_int, [P, I32, I32, P, I32, P]),
     "tmg_machine_set_windows": (C.c_int, [P, I32]),
+    "tmg_last_eval_kernel_ms": (C.c_int, [P, P]),
     "tmg_pool_replica_tallies": (C.c_int, [P, I32, P]),
     "tmg_machine_exchange_info": (C.c_int, [P, P, P]),
     "tmg_nccl_available": (C.c_int, [P, I32]),

@@ -569,7 +569,13 @@ void class_sums_device(tmg_machine* tm, const uint32_t* xplane, int64_t q, bool 
   }
   e.chunks = static_cast<int32_t>((tm->n_loc + e.cta_clauses - 1) / e.cta_clauses);
   CK(cudaMemsetAsync(d_out, 0, static_cast<size_t>(q) * tm->m * 4, tm->stream));
+  if (!tm->eval0) {
+    CK(cudaEventCreate(&tm->eval0));
+    CK(cudaEventCreate(&tm->eval1));
+  }
+  CK(cudaEventRecord(tm->eval0, tm->stream));
   tmg::eval_bits_launch(e, train_mode, tm->stream);
+  CK(cudaEventRecord(tm->eval1, tm->stream));
   CK(cudaGetLastError());
 }
 
@@ -711,6 +717,8 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   tm->dbg.release();
   tm->alias8.release();
   tm->scratch16.release();
+  if (tm->eval0) cudaEventDestroy(tm->eval0);
+  if (tm->eval1) cudaEventDestroy(tm->eval1);
   if (tm->ev0) cudaEventDestroy(tm->ev0);
   if (tm->ev1) cudaEventDestroy(tm->ev1);
   if (tm->stream) cudaStreamDestroy(tm->stream);
@@ -1459,6 +1467,17 @@ TMG_API int tmg_alias8_table(uint32_t threshold, uint32_t* out) {
 
 TMG_API unsigned long long tmg_kernel_launches(void) {
   return __atomic_load_n(&tmg::g_launches, __ATOMIC_RELAXED);
+}
+
+TMG_API int tmg_last_eval_kernel_ms(tmg_machine* tm, float* ms) {
+  return guarded([&] {
+    M(tm);
+    need_single(tm, "tmg_last_eval_kernel_ms");
+    if (!tm->eval0) fail(TMG_EINVAL, "no class-sum kernel has run on this machine");
+    DeviceGuard dg(tm->device);
+    CK(cudaEventSynchronize(tm->eval1));
+    CK(cudaEventElapsedTime(ms, tm->eval0, tm->eval1));
+  });
 }
 
 TMG_API int tmg_machine_stream(tmg_machine* tm, void** stream) {

@@ -160,6 +160,7 @@ struct tmg_machine {
   std::vector<int64_t> bank_q;  // per bank (ClassBank::bound_examples); prev stride Wq covers the largest
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t eval0 = nullptr, eval1 = nullptr;  // around the last class-sum kernel
   tmgx::DevBuf<uint32_t> state, prev;
   tmgx::DevBuf<int32_t> inc_count, lens, npos, sums;
   tmgx::DevBuf<int64_t> offs;      // [clauses + 1] literal-list offsets
