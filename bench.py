@@ -16,11 +16,12 @@ q examples — the most expensive epoch, and identical work every step.
           reset, the epoch runs, the per-class feedback-event report is read
           back.
 Multi-GPU (torchrun): weak scaling in clauses — every rank owns 2000 clauses
-per class (global n = 2000 * world). Default exchange "comm": the engine's own
-NCCL communicator (tmg_comm_create, id broadcast once through
-torch.distributed) attached to the rank's shard, and tmg_train_epoch runs the
-windowed tally exchange inside the library, overlapped on a side stream
-(paper_2009_04861_b200/csrc/group.cu). Alternatives: "peer" (every tally
+per class (global n = 2000 * world). Default exchange "ipc": the engine's own
+communicator (tmg_comm_create_ipc, handles all-gathered once through
+torch.distributed) attached to the rank's shard; tmg_train_epoch runs the
+rank's epoch as one launch and exchanges the tally deltas beside it, each rank
+pulling the others' snapshots over CUDA IPC / NVLink with the copy engines
+(paper_2009_04861_b200/csrc/group.cu). "comm" does the same sums with NCCL. Alternatives: "peer" (every tally
 change also RED-added into the other ranks' replicas over CUDA IPC / NVLink
 by the training kernels), "overlapped"/"sync" (the same windows driven from
 Python with torch.distributed, paper_2009_04861_b200/distributed.py).
@@ -274,9 +275,9 @@ def other_configs(local):
 
 def sharded_line(d, local) -> dict:
     """The N > 1 machinery on this one GPU: the bench epoch
-    through a one-rank NCCL communicator (the code path of every rank of the
-    N-GPU run: streaming tally exchange, event all-reduce) against the plain
-    machine, and a two-shard machine on this GPU (peer-memory sums) against
+    through one-rank communicators — CUDA IPC (the N-GPU default) and NCCL —
+    (the code path of every rank of the N-GPU run: streaming tally exchange,
+    event all-reduce) against the plain machine, and a two-shard machine on this GPU (peer-memory sums) against
     one machine of the same clause count. Fresh epoch 0, best of 3."""
     import paper_2009_04861_b200 as T
     pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M_CLS, device=local)
@@ -302,6 +303,13 @@ def sharded_line(d, local) -> dict:
         del tm, comm
     else:
         out["nccl"] = why
+    ipc = T.Comm.ipc(1, 0, local, Q_TRAIN * M_CLS, lambda b: [b])  # the N-GPU default's code path
+    tm = T.MultiClassTM(cfg, O_FEAT, M_CLS, device=local, clause_range=(0, N_CLAUSES))
+    tm.attach_comm(ipc)
+    out["one_rank_ipc_ms"] = best(tm)
+    out["one_rank_ipc_overhead"] = out["one_rank_ipc_ms"] / out["plain_ms"]
+    tm.attach_comm(None)
+    del tm, ipc
     cfg2 = T.TMConfig(clauses=2 * N_CLAUSES, margin=MARGIN, specificity=SPEC, state_depth=STATE_N, seed=TM_SEED)
     out["plain_2x_clauses_ms"] = best(T.MultiClassTM(cfg2, O_FEAT, M_CLS, device=local))
     out["two_shards_one_gpu_ms"] = best(T.MultiClassTM(cfg2, O_FEAT, M_CLS, devices=[local, local]))
@@ -499,11 +507,21 @@ def run_ours(args):
     exchange, exchange_note = (args.exchange if world > 1 else "none"), None
     comm = None
     if exchange == "comm" and (args.share_device or args.dist_backend != "nccl"):
-        exchange, exchange_note = "overlapped", "NCCL needs one GPU per rank; one-device protocol test"
-    if exchange == "comm":  # the library's own NCCL communicator, windows inside tmg_train_epoch
+        exchange, exchange_note = "ipc", "NCCL needs one GPU per rank; one-device protocol test over CUDA IPC"
+    if exchange == "comm":  # the library's NCCL communicator, streaming exchange inside tmg_train_epoch
         uid = [T.Comm.unique_id() if rank == 0 else None]
         torch.distributed.broadcast_object_list(uid, src=0)
         comm = T.Comm(uid[0], world, rank, local)
+        tm.attach_comm(comm)
+        tm.set_windows(windows)
+    elif exchange == "ipc":  # the same exchange, snapshots pulled over CUDA IPC by the copy engines
+
+        def allgather(b):
+            out = [None] * world
+            torch.distributed.all_gather_object(out, b)
+            return out
+
+        comm = T.Comm.ipc(world, rank, local, Q_TRAIN * M_CLS, allgather)
         tm.attach_comm(comm)
         tm.set_windows(windows)
     if exchange == "peer":  # tally replicas over peer memory; NCCL windows if P2P is unavailable
@@ -520,7 +538,7 @@ def run_ours(args):
     def one_epoch(p):
         tm.reset()
         p.reset_tallies()
-        if world == 1 or exchange == "comm":
+        if world == 1 or exchange in ("comm", "ipc"):
             rep = T.train_epoch_parallel(tm, p, 1, 0)
             return rep.feedback_events, rep.type_i_events, (rep.device_seconds if world == 1 else None)
         if exchange == "peer":
@@ -681,11 +699,11 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-other-configs", action="store_true", help="skip the FMNIST/IMDb side measurements")
     ap.add_argument("--dist-backend", default="nccl", help="torch.distributed backend for N>1 (tests: gloo)")
-    ap.add_argument("--exchange", choices=["comm", "peer", "overlapped", "sync"], default="comm",
-                    help="N>1 tally exchange: the engine's NCCL communicator with the windowed exchange "
-                         "inside tmg_train_epoch (default); replicas updated by the training kernels over "
-                         "peer memory (NVLink); windowed all-reduce driven from Python, overlapped or "
-                         "host-synchronous")
+    ap.add_argument("--exchange", choices=["ipc", "comm", "peer", "overlapped", "sync"], default="ipc",
+                    help="N>1 tally exchange: the engine's streaming exchange inside tmg_train_epoch with the "
+                         "ranks' snapshots pulled over CUDA IPC by the copy engines (default) or summed by an "
+                         "NCCL communicator; replicas updated by the training kernels over peer memory "
+                         "(NVLink); windowed all-reduce driven from Python, overlapped or host-synchronous")
     ap.add_argument("--share-device", action="store_true",
                     help="run every rank on cuda:0 (one-GPU test of the N>1 protocol; not a measurement)")
     args = ap.parse_args()

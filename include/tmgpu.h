@@ -264,6 +264,15 @@ typedef struct tmg_comm tmg_comm;
 int tmg_comm_unique_id(unsigned char* id128);
 int tmg_comm_create(const unsigned char* id128, int32_t nranks, int32_t rank, int32_t device, tmg_comm** out);
 int tmg_comm_destroy(tmg_comm* comm);
+/* The same without NCCL, over CUDA IPC (one node): every rank maps the
+ * others' snapshot slots and pulls them with the copy engine (NVLink), so no
+ * exchange kernel needs to be co-scheduled across ranks. Create with the
+ * largest q x m any pool of the machine will have, export the 192-byte
+ * handle, gather every rank's handles (rank order, nranks x 192 bytes) over
+ * your transport, connect, attach. */
+int tmg_comm_create_ipc(int32_t nranks, int32_t rank, int32_t device, int64_t capacity, tmg_comm** out);
+int tmg_comm_ipc_handle(tmg_comm* comm, unsigned char* handle192);
+int tmg_comm_ipc_connect(tmg_comm* comm, const unsigned char* handles);
 int tmg_machine_attach_comm(tmg_machine* tm, tmg_comm* comm);
 
 /* Multi-GPU building blocks: one asynchronous window [t_begin, t_end) of every

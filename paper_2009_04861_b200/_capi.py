@@ -82,6 +82,9 @@ SIGNATURES = {
     "tmg_comm_unique_id": (C.c_int, [P]),
     "tmg_comm_create": (C.c_int, [P, I32, I32, I32, P]),
     "tmg_comm_destroy": (C.c_int, [P]),
+    "tmg_comm_create_ipc": (C.c_int, [I32, I32, I32, I64, P]),
+    "tmg_comm_ipc_handle": (C.c_int, [P, P]),
+    "tmg_comm_ipc_connect": (C.c_int, [P, P]),
     "tmg_machine_attach_comm": (C.c_int, [P, P]),
     "tmg_bank_bound_examples": (C.c_int, [P, I32, P]),
     "tmg_get_prev_outputs": (C.c_int, [P, I32, P]),

@@ -144,6 +144,20 @@ struct Exchange {
   std::vector<std::unique_ptr<Slot>> slots;
   int64_t count = 0;
   double interval_s = 0.002;  // time between exchanges (adapted to the epoch length)
+  // IPC mode (one process per GPU, no NCCL): every rank's snapshot slots and
+  // control words are mapped into every other rank (CUDA IPC over NVLink);
+  // each rank PULLS the others' snapshots with the copy engine and sums
+  // locally, so no exchange kernel has to be co-scheduled across ranks.
+  // ctl = [ready seq of slot 0, 1][consumed seq: slot 0 by rank 0..N-1][slot 1 by 0..N-1]
+  bool use_ipc = false;
+  int64_t seq = 0;                         // exchange sequence number, identical on every rank
+  int64_t ipc_count = 0;                   // capacity of the exported snapshot slots
+  DevBuf<int64_t> ctl;
+  std::vector<int32_t*> peer_snap[2];      // [slot][rank] (own rank: null)
+  std::vector<int64_t*> peer_ctl;          // [rank]
+  std::vector<std::unique_ptr<DevBuf<int32_t>>> recv;  // [rank] pulled snapshots
+  cudaStream_t pstream = nullptr;          // polling copies
+  int64_t* hpoll = nullptr;                // pinned host words for polling / flag writes
   DevBuf<unsigned long long> scratch64;  // cross-rank event / sum reductions
   DevBuf<int32_t> scratch32;
 
@@ -174,6 +188,11 @@ struct Exchange {
 
   void ensure(int64_t n) {
     if (n == count) return;
+    if (use_ipc) {  // slots were exported with their capacity; only the count used changes
+      if (n > ipc_count) fail(TMG_EINVAL, "pool larger than the IPC communicator's exported capacity");
+      count = n;
+      return;
+    }
     for (size_t k = 0; k < devices.size(); ++k) {
       DeviceGuard dg(devices[k]);
       for (int b = 0; b < 2; ++b) {  // plain cudaMalloc: peer-accessible (stream-ordered pools are not)
@@ -185,6 +204,16 @@ struct Exchange {
   }
 
   ~Exchange() {
+    if (use_ipc && !devices.empty()) {
+      cudaSetDevice(devices[0]);
+      for (int b = 0; b < 2; ++b)
+        for (int32_t* p : peer_snap[b])
+          if (p) cudaIpcCloseMemHandle(p);
+      for (int64_t* p : peer_ctl)
+        if (p) cudaIpcCloseMemHandle(p);
+      if (pstream) cudaStreamDestroy(pstream);
+      if (hpoll) cudaFreeHost(hpoll);
+    }
     for (size_t k = 0; k < devices.size(); ++k) {
       cudaSetDevice(devices[k]);
       if (k < cstreams.size() && cstreams[k]) cudaStreamSynchronize(cstreams[k]);
@@ -204,6 +233,52 @@ struct Exchange {
 
   // Sum of the shards' snapshot b (all local shards and, with NCCL, all
   // ranks) into every local shard's red[b]; red_ev[b] marks completion.
+  // Host-side poll of a device word (own or peer-mapped) until pred holds.
+  template <typename Pred>
+  void poll(const int64_t* dptr, Pred&& pred) {
+    for (;;) {
+      CK(cudaMemcpyAsync(hpoll, dptr, sizeof(int64_t), cudaMemcpyDeviceToHost, pstream));
+      CK(cudaStreamSynchronize(pstream));
+      if (pred(hpoll[0])) return;
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+  }
+
+  // IPC exchange of slot b with sequence number sq (the snapshot is already
+  // enqueued on cstreams[0]): publish ready, pull every other rank's
+  // snapshot once it is ready, tell it so, sum locally.
+  void reduce_ipc(int b, int64_t sq) {
+    DeviceGuard dg(devices[0]);
+    cudaStream_t cs = cstreams[0];
+    int64_t* words = hpoll + 1;  // [1] = sq for the flag writes
+    words[0] = sq;
+    CK(cudaMemcpyAsync(ctl.ptr + b, words, sizeof(int64_t), cudaMemcpyHostToDevice, cs));  // ready[b] = sq
+    PeerSrc src{};
+    src.n = 0;
+    src.p[src.n++] = slots[0]->snap[b].ptr;
+    for (int j = 0; j < nranks; ++j) {
+      if (j == rank) continue;
+      poll(peer_ctl[j] + b, [&](int64_t v) { return v == sq; });
+      CK(cudaMemcpyAsync(recv[j]->ptr, peer_snap[b][j], static_cast<size_t>(count) * 4, cudaMemcpyDeviceToDevice,
+                         cs));
+      CK(cudaMemcpyAsync(peer_ctl[j] + 2 + b * nranks + rank, words, sizeof(int64_t), cudaMemcpyHostToDevice, cs));
+      src.p[src.n++] = recv[j]->ptr;
+    }
+    tmg::count_launch();
+    peer_sum_kernel<<<64, 256, 0, cs>>>(slots[0]->red[b].ptr, src, count);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(slots[0]->red_ev[b], cs));
+    CK(cudaStreamSynchronize(cs));  // the flag words in hpoll are reused by the next exchange
+  }
+
+  // IPC: before overwriting own slot b, every other rank has pulled the
+  // snapshot it held (sequence number >= sq).
+  void wait_consumed(int b, int64_t sq) {
+    DeviceGuard dg(devices[0]);
+    for (int j = 0; j < nranks; ++j)
+      if (j != rank) poll(ctl.ptr + 2 + b * nranks + j, [&](int64_t v) { return v >= sq; });
+  }
+
   void reduce(int b) {
     const size_t n = devices.size();
     if (use_nccl) {
@@ -236,6 +311,42 @@ struct Exchange {
     }
   }
 
+  // Host-side sum over ranks through the IPC slots (events, class sums):
+  // each value split into int32 words in own slot 0, one exchange round.
+  template <typename T>
+  void allreduce_host_ipc(T* v, size_t n) {
+    const size_t words = n * sizeof(T) / 4;
+    if (static_cast<int64_t>(words) > ipc_count) fail(TMG_EINVAL, "host all-reduce larger than the IPC slots");
+    DeviceGuard dg(devices[0]);
+    const int64_t sq = seq++;
+    const int b = static_cast<int>(sq & 1);
+    wait_consumed(b, sq - 2);
+    std::vector<uint32_t> lo(words);
+    std::memcpy(lo.data(), v, words * 4);
+    const int64_t keep = count;
+    count = static_cast<int64_t>(words);
+    CK(cudaMemcpyAsync(slots[0]->snap[b].ptr, lo.data(), words * 4, cudaMemcpyHostToDevice, cstreams[0]));
+    // pull the raw words of every rank and add on the host (exact for uint64 too)
+    DeviceGuard dg2(devices[0]);
+    int64_t* w = hpoll + 1;
+    w[0] = sq;
+    CK(cudaMemcpyAsync(ctl.ptr + b, w, sizeof(int64_t), cudaMemcpyHostToDevice, cstreams[0]));
+    CK(cudaStreamSynchronize(cstreams[0]));
+    std::vector<T> acc(v, v + n), part(n);
+    for (int j = 0; j < nranks; ++j) {
+      if (j == rank) continue;
+      poll(peer_ctl[j] + b, [&](int64_t x) { return x == sq; });
+      CK(cudaMemcpyAsync(part.data(), peer_snap[b][j], words * 4, cudaMemcpyDeviceToHost, cstreams[0]));
+      CK(cudaMemcpyAsync(peer_ctl[j] + 2 + b * nranks + rank, w, sizeof(int64_t), cudaMemcpyHostToDevice,
+                         cstreams[0]));
+      CK(cudaStreamSynchronize(cstreams[0]));
+      for (size_t i = 0; i < n; ++i) acc[i] += part[i];
+    }
+    std::memcpy(v, acc.data(), n * sizeof(T));
+    count = keep;
+    wait_consumed(b, sq);
+  }
+
   // Before shard k touches snapshot b again: its own sum is done and (peer
   // mode) so is every other shard's read of its snapshot.
   void wait_reduced(size_t k, int b, cudaStream_t s) {
@@ -250,6 +361,7 @@ struct Exchange {
   template <typename T>
   void allreduce_host(T* v, size_t n) {
     if (nranks == 1) return;
+    if (use_ipc) return allreduce_host_ipc(v, n);
     static_assert(sizeof(T) == 4 || sizeof(T) == 8, "int32 / uint64 only");
     DeviceGuard dg(devices[0]);
     void* d = nullptr;
@@ -385,8 +497,11 @@ void sharded_epoch(Exchange& X, const std::vector<tmg_machine*>& shards, const s
   }
   const int total = static_cast<int>(n) * X.nranks;
   const auto interval = std::chrono::duration<double>(X.interval_s);
+  int64_t last_sq = -1;
   for (int64_t it = 0;; ++it) {
-    const int b = static_cast<int>(it & 1), p = b ^ 1;
+    const int64_t sq = X.seq++;  // the same on every rank: all ranks run the same exchanges
+    const int b = static_cast<int>(sq & 1), p = b ^ 1;
+    last_sq = sq;
     // wait for the interval or for every local shard to finish
     const auto t0 = std::chrono::steady_clock::now();
     for (;;) {
@@ -399,13 +514,15 @@ void sharded_epoch(Exchange& X, const std::vector<tmg_machine*>& shards, const s
       DeviceGuard dg(shards[k]->device);
       Exchange::Slot& sl = *X.slots[k];
       sl.flag[0] = cudaEventQuery(sl.done) == cudaSuccess ? 1 : 0;  // before the copy: a done shard's copy is final
-      X.wait_reduced(k, b, X.cstreams[k]);  // slot b's last readers (two exchanges ago) are done
+      if (X.use_ipc) X.wait_consumed(b, sq - 2);  // the other ranks pulled what slot b held
+      else X.wait_reduced(k, b, X.cstreams[k]);   // slot b's last readers (two exchanges ago) are done
       CK(cudaMemcpyAsync(sl.snap[b].ptr, pools[k]->delta.ptr, static_cast<size_t>(cnt) * 4, cudaMemcpyDeviceToDevice,
                          X.cstreams[k]));
       CK(cudaMemcpyAsync(sl.snap[b].ptr + cnt, sl.flag, 4, cudaMemcpyHostToDevice, X.cstreams[k]));
       CK(cudaEventRecord(sl.snap_ev[b], X.cstreams[k]));
     }
-    X.reduce(b);
+    if (X.use_ipc) X.reduce_ipc(b, sq);
+    else X.reduce(b);
     for (size_t k = 0; k < n; ++k) {  // replica += the other shards' growth since the last exchange
       DeviceGuard dg(shards[k]->device);
       Exchange::Slot& sl = *X.slots[k];
@@ -426,6 +543,10 @@ void sharded_epoch(Exchange& X, const std::vector<tmg_machine*>& shards, const s
     DeviceGuard dg(shards[k]->device);
     CK(cudaStreamSynchronize(X.cstreams[k]));
     CK(cudaStreamSynchronize(shards[k]->stream));
+  }
+  if (X.use_ipc) {  // no rank may zero its slots for the next epoch while another still pulls
+    X.wait_consumed(static_cast<int>(last_sq & 1), last_sq);
+    X.wait_consumed(static_cast<int>((last_sq - 1) & 1), last_sq - 1);
   }
   // aim at `windows` exchanges in the next epoch of similar length
   const double took = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count();
@@ -772,6 +893,81 @@ TMG_API int tmg_comm_create(const unsigned char* id, int32_t nranks, int32_t ran
       throw;
     }
     *out = c;
+  });
+}
+
+TMG_API int tmg_comm_create_ipc(int32_t nranks, int32_t rank, int32_t device, int64_t capacity, tmg_comm** out) {
+  return guarded([&] {
+    if (nranks < 1 || nranks > 16 || rank < 0 || rank >= nranks) fail(TMG_EINVAL, "bad rank / rank count (1-16)");
+    if (capacity < 1) fail(TMG_EINVAL, "capacity (q x m) must be >= 1");
+    auto c = new tmg_comm();
+    c->x = new Exchange();
+    try {
+      Exchange& x = *c->x;
+      x.use_ipc = true;
+      x.nranks = nranks;
+      x.rank = rank;
+      x.devices = {device};
+      x.init_streams();
+      DeviceGuard dg(device);
+      x.ipc_count = capacity + 1;  // + the done flag
+      for (int b = 0; b < 2; ++b) {
+        x.slots[0]->snap[b].alloc_plain(static_cast<size_t>(x.ipc_count));
+        x.slots[0]->red[b].alloc_plain(static_cast<size_t>(x.ipc_count));
+      }
+      x.ctl.alloc_plain(2 + 2 * static_cast<size_t>(nranks));
+      CK(cudaMemset(x.ctl.ptr, 0xFF, x.ctl.bytes()));  // every sequence word -1: nothing ready, nothing pulled
+      x.recv.resize(static_cast<size_t>(nranks));
+      for (int j = 0; j < nranks; ++j) {
+        if (j == rank) continue;
+        x.recv[static_cast<size_t>(j)] = std::make_unique<DevBuf<int32_t>>();
+        x.recv[static_cast<size_t>(j)]->alloc_plain(static_cast<size_t>(x.ipc_count));
+      }
+      CK(cudaStreamCreateWithFlags(&x.pstream, cudaStreamNonBlocking));
+      CK(cudaMallocHost(reinterpret_cast<void**>(&x.hpoll), 4 * sizeof(int64_t)));
+    } catch (...) {
+      delete c->x;
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+TMG_API int tmg_comm_ipc_handle(tmg_comm* comm, unsigned char* out) {
+  return guarded([&] {
+    if (!comm || !comm->x->use_ipc) fail(TMG_EINVAL, "not an IPC communicator");
+    Exchange& x = *comm->x;
+    DeviceGuard dg(x.devices[0]);
+    cudaIpcMemHandle_t h[3];
+    CK(cudaIpcGetMemHandle(&h[0], x.slots[0]->snap[0].ptr));
+    CK(cudaIpcGetMemHandle(&h[1], x.slots[0]->snap[1].ptr));
+    CK(cudaIpcGetMemHandle(&h[2], x.ctl.ptr));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "64-byte IPC handles");
+    std::memcpy(out, h, sizeof h);
+  });
+}
+
+TMG_API int tmg_comm_ipc_connect(tmg_comm* comm, const unsigned char* all) {
+  return guarded([&] {
+    if (!comm || !comm->x->use_ipc) fail(TMG_EINVAL, "not an IPC communicator");
+    Exchange& x = *comm->x;
+    DeviceGuard dg(x.devices[0]);
+    x.peer_snap[0].assign(static_cast<size_t>(x.nranks), nullptr);
+    x.peer_snap[1].assign(static_cast<size_t>(x.nranks), nullptr);
+    x.peer_ctl.assign(static_cast<size_t>(x.nranks), nullptr);
+    for (int j = 0; j < x.nranks; ++j) {
+      if (j == x.rank) continue;
+      cudaIpcMemHandle_t h[3];
+      std::memcpy(h, all + static_cast<size_t>(j) * sizeof h, sizeof h);
+      void* p = nullptr;
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaIpcOpenMemHandle(&p, h[b], cudaIpcMemLazyEnablePeerAccess));
+        x.peer_snap[b][static_cast<size_t>(j)] = static_cast<int32_t*>(p);
+      }
+      CK(cudaIpcOpenMemHandle(&p, h[2], cudaIpcMemLazyEnablePeerAccess));
+      x.peer_ctl[static_cast<size_t>(j)] = static_cast<int64_t*>(p);
+    }
   });
 }
 

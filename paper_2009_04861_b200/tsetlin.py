@@ -348,6 +348,21 @@ class Comm:
         self._h = C.c_void_p()
         check(lib().tmg_comm_create(buf, nranks, rank, device, C.byref(self._h)))
 
+    @classmethod
+    def ipc(cls, nranks: int, rank: int, device: int, capacity: int, allgather) -> "Comm":
+        """The NCCL-free communicator over CUDA IPC (one node): `capacity` =
+        the largest q x m of the machine's pools; `allgather(bytes) -> list of
+        bytes` in rank order (e.g. torch.distributed.all_gather_object)."""
+        self = cls.__new__(cls)
+        self._h = C.c_void_p()
+        check(lib().tmg_comm_create_ipc(nranks, rank, device, capacity, C.byref(self._h)))
+        h = (C.c_ubyte * 192)()
+        check(lib().tmg_comm_ipc_handle(self._h, h))
+        handles = allgather(bytes(h))
+        buf = (C.c_ubyte * (192 * nranks)).from_buffer_copy(b"".join(handles))
+        check(lib().tmg_comm_ipc_connect(self._h, buf))
+        return self
+
     @property
     def handle(self):
         return self._h

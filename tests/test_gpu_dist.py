@@ -45,6 +45,14 @@ def _worker(rank, world, port, out_dir, overlapped=False):
     tm = T.MultiClassTM(T.TMConfig(clauses=N, margin=20, specificity=10.0, seed=3), O_FEAT, M, clause_range=(jb, je))
     pool = T.ExamplePool(O_FEAT, d.train_x, d.train_y, M)
     eng = D.GpuShardEngine(tm, pool)
+    comm = None
+    if overlapped == "ipc":  # the engine's own streaming exchange over CUDA IPC (no NCCL)
+        def allgather(b):
+            out = [None] * world
+            dist.all_gather_object(out, b)
+            return out
+        comm = T.Comm.ipc(world, rank, 0, Q * M, allgather)
+        tm.attach_comm(comm)
     if overlapped == "peer":
         assert D.attach_peer_tallies(pool) == world - 1
         try:  # mixing the exchanges would count every tally change twice: refused
@@ -53,7 +61,10 @@ def _worker(rank, world, port, out_dir, overlapped=False):
         except ValueError as e:  # std::invalid_argument
             assert "peer tally replicas" in str(e)
     for e in range(2):
-        if overlapped == "peer":
+        if overlapped == "ipc":
+            rep = T.train_epoch_parallel(tm, pool, 8, e)
+            assert rep.total_feedback_events() > 0
+        elif overlapped == "peer":
             D.train_epoch_peer(tm, pool, e)
         elif overlapped:
             D.train_epoch_overlapped(tm, pool, e, windows=5)
@@ -64,8 +75,13 @@ def _worker(rank, world, port, out_dir, overlapped=False):
     np.save(os.path.join(out_dir, f"counters{rank}.npy"), np.stack([tm.banks[c].counters() for c in range(M)]))
     test = T.ExamplePool(O_FEAT, d.test_x, d.test_y, M)
     part = torch.from_numpy(T.class_sums(tm, test).astype(np.int64))
-    dist.all_reduce(part)
+    if comm is None:
+        dist.all_reduce(part)
+    # (an attached communicator returns the whole machine's sums already)
     np.save(os.path.join(out_dir, f"sums{rank}.npy"), part.numpy())
+    if comm is not None:
+        tm.attach_comm(None)
+        del comm
     dist.barrier()
     dist.destroy_process_group()
 
@@ -75,7 +91,8 @@ def _bits(prev, q):
     return b[..., :q].astype(np.int64)
 
 
-@pytest.mark.parametrize("overlapped,world", [(False, 2), (True, 2), ("peer", 2), ("peer", 3)])
+@pytest.mark.parametrize("overlapped,world", [(False, 2), (True, 2), ("peer", 2), ("peer", 3), ("ipc", 2),
+                                              ("ipc", 3)])
 def test_gpu_shards_two_processes(tmp_path, overlapped, world):
     """Synchronous windows (train_epoch_windows), the double-buffered,
     overlapped exchange (train_epoch_overlapped) and the peer-memory replicas
@@ -166,12 +183,13 @@ def test_two_rank_accuracy_parity(tmp_path, exchange):
     assert ok, msg
 
 
-@pytest.mark.parametrize("exchange,expect", [("comm", "overlapped"), ("peer", "peer")])
+@pytest.mark.parametrize("exchange,expect", [("ipc", "ipc"), ("comm", "ipc"), ("peer", "peer")])
 def test_bench_two_ranks_protocol(exchange, expect):
     """bench.py under torchrun with 2 ranks (gloo, shared device): one JSON
     line from rank 0 with n_gpus = 2 and a positive value. The default
-    exchange (the engine's NCCL communicator) needs one GPU per rank, so on
-    a shared device it falls back to the overlapped windows and says so."""
+    exchange (the engine's communicator over CUDA IPC) runs as it would on
+    two GPUs; the NCCL one needs one GPU per rank, so on a shared device it
+    falls back to IPC and says so."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.join(REPO, "bench.py"),
            "--gpus", "2", "--steps", "1", "--warmup", "1", "--no-cpu", "--dist-backend", "gloo", "--share-device",
@@ -184,3 +202,5 @@ def test_bench_two_ranks_protocol(exchange, expect):
     assert lines[0]["config"]["exchange"] == expect
     if exchange == "comm":
         assert "NCCL" in lines[0]["config"]["exchange_note"]
+    if expect == "ipc":  # the engine's exchange reported every rank's events
+        assert lines[0]["feedback_events_per_step"] > 0
