@@ -30,6 +30,14 @@ namespace tmg {
 namespace {
 
 constexpr int kEvalWarps = 8;   // warps per eval CTA (same example block, disjoint clause ranges)
+// Resident eval CTAs per SM the register budget is cut for (48 registers at 5).
+// Measured (tools/build_variants.sh, r2 eval sweep): 4 -> MNIST +6%, FMNIST -5%;
+// 6 -> MNIST +5%, FMNIST -4%. A software-pipelined short-list path (descriptor
+// two clauses ahead, first 8 entries one ahead) spilled at 5 and at 4 ran
+// MNIST 0.094 ms vs 0.078 ms, FMNIST +8%, IMDb +14%: removed.
+#ifndef TMG_EVAL_MINB
+#define TMG_EVAL_MINB 5
+#endif
 constexpr int kSumPlanes = 12;  // bit-sliced two's-complement counters: |sum| <= 2040 per CTA
 
 // One warp per clause: count the included literals (top plane) -> inc_count,
@@ -240,7 +248,7 @@ __device__ __forceinline__ uint32_t fold_short(const uint32_t* __restrict__ lst,
 }
 
 template <bool TRAIN>
-__global__ void __launch_bounds__(kEvalWarps * 32, 5) eval_bits_kernel(BitsEvalParams P) {
+__global__ void __launch_bounds__(kEvalWarps * 32, TMG_EVAL_MINB) eval_bits_kernel(BitsEvalParams P) {
   __shared__ uint32_t red[kEvalWarps][kSumPlanes][32];
   __shared__ int next_clause;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
