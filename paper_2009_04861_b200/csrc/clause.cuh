@@ -17,6 +17,12 @@
 #ifndef TMG_STEP_SAT_REG
 #define TMG_STEP_SAT_REG 0  // register kernels: clause-output-1 Type I as two passes (tm_device.cuh type_i_planes)
 #endif
+#ifndef TMG_ROW_X_ONLY
+#define TMG_ROW_X_ONLY 1  // async kernels read the x half of a literal row only (!x = ~x)
+#endif
+#ifndef TMG_ROW_X_MIN_NW
+#define TMG_ROW_X_MIN_NW 2  // register kernel: from this row width (words per lane)
+#endif
 #ifndef TMG_ALIAS
 #define TMG_ALIAS 1  // alias-table sampler for clause-output-0 Type I draws
 #endif

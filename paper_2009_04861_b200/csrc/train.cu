@@ -94,7 +94,12 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
 #pragma unroll
       for (int p = 0; p < NW; ++p) {
         xs[p] = __ldg(rp + p * 32);
-        ns[p] = __ldg(rp + 32 * NW + p * 32);
+        // !x words as ~x (TMG_ROW_X_ONLY, rows of >= TMG_ROW_X_MIN_NW words
+        // per lane): the bits past o differ from the stored !x plane (0
+        // there) but every use is masked by the valid bits or meets an
+        // include bit, which is never set past o.
+        if constexpr (TMG_ROW_X_ONLY && NW >= TMG_ROW_X_MIN_NW) ns[p] = ~xs[p];
+        else ns[p] = __ldg(rp + 32 * NW + p * 32);
       }
     };
     auto run = [&](const uint32_t (&xs)[NW], const uint32_t (&ns)[NW], int cd, uint32_t sl) {

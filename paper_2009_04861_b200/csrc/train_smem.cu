@@ -90,8 +90,18 @@ struct SmemPlanes {
 
 // A step's literal row as seen by one lane: words p*32 + lane of the x- and
 // !x-planes, p < words(). Held in registers for a compile-time width.
+// With TMG_ROW_X_ONLY the !x words are taken as ~x (train.cu fetch: bits
+// past o differ from the stored plane, and every use masks them out).
 template <int NW>
 struct LitRow {
+#if TMG_ROW_X_ONLY
+  uint32_t xw[NW];
+  __device__ __forceinline__ void load(const uint32_t* rp, int) {
+#pragma unroll
+    for (int p = 0; p < NW; ++p) xw[p] = __ldg(rp + p * 32);
+  }
+  __device__ __forceinline__ uint32_t n(int p) const { return ~xw[p]; }
+#else
   uint32_t xw[NW], nw_[NW];
   __device__ __forceinline__ void load(const uint32_t* rp, int Wp) {
 #pragma unroll
@@ -100,8 +110,9 @@ struct LitRow {
       nw_[p] = __ldg(rp + Wp + p * 32);
     }
   }
-  __device__ __forceinline__ uint32_t x(int p) const { return xw[p]; }
   __device__ __forceinline__ uint32_t n(int p) const { return nw_[p]; }
+#endif
+  __device__ __forceinline__ uint32_t x(int p) const { return xw[p]; }
   __device__ __forceinline__ int words() const { return NW; }
 };
 
@@ -115,7 +126,11 @@ struct LitRow<0> {
     Wp = w;
   }
   __device__ __forceinline__ uint32_t x(int p) const { return __ldg(rp + p * 32); }
+#if TMG_ROW_X_ONLY
+  __device__ __forceinline__ uint32_t n(int p) const { return ~__ldg(rp + p * 32); }
+#else
   __device__ __forceinline__ uint32_t n(int p) const { return __ldg(rp + Wp + p * 32); }
+#endif
   __device__ __forceinline__ int words() const { return Wp >> 5; }
 };
 
