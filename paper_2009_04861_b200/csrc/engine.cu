@@ -406,14 +406,21 @@ Gf2 gf2_pow(uint64_t k) {
   return result;
 }
 
-// Device layout of sequential.cu gf2_apply: [r][w][L] = 32-bit word w of row 8L + r.
+// Device layout of tm_device.cuh gf2_apply: nibble tables, entry (pos, v) =
+// the 8 words of m * (v << 4 pos) = XOR of the columns of m for v's bits.
 void gf2_layout(const Gf2& m, uint32_t* out) {
-  for (int r = 0; r < 8; ++r)
-    for (int w = 0; w < 8; ++w)
-      for (int l = 0; l < 32; ++l) {
-        const uint64_t v = m.r[8 * l + r][w >> 1];
-        out[(r * 8 + w) * 32 + l] = static_cast<uint32_t>((w & 1) ? v >> 32 : v);
-      }
+  uint32_t col[256][8] = {};
+  for (int i = 0; i < 256; ++i)
+    for (int b = 0; b < 256; ++b)
+      if ((m.r[i][b >> 6] >> (b & 63)) & 1) col[b][i >> 5] |= 1u << (i & 31);
+  for (int pos = 0; pos < 64; ++pos)
+    for (int v = 0; v < 16; ++v) {
+      uint32_t* e = out + (pos * 16 + v) * 8;
+      for (int w = 0; w < 8; ++w) e[w] = 0;
+      for (int bit = 0; bit < 4; ++bit)
+        if ((v >> bit) & 1)
+          for (int w = 0; w < 8; ++w) e[w] ^= col[4 * pos + bit][w];
+    }
 }
 
 // The parallel replay pays off once a bank has enough clauses to spread over
@@ -438,12 +445,13 @@ bool seq_grid_enabled() {
 void ensure_jumps(tmg_machine* tm) {
   const int L = 2 * tm->o;
   const int chunk = (L + 31) / 32;
-  if (tm->seq_jump.count != 4096) {
-    std::vector<uint32_t> host(4096);
+  constexpr size_t kTab = tmg::kGf2TabWords;
+  if (tm->seq_jump.count != 2 * kTab) {
+    std::vector<uint32_t> host(2 * kTab);
     gf2_layout(gf2_pow(static_cast<uint64_t>(chunk)), host.data());
-    gf2_layout(gf2_pow(static_cast<uint64_t>(L)), host.data() + 2048);
-    tm->seq_jump.alloc(4096);
-    CK(cudaMemcpy(tm->seq_jump.ptr, host.data(), 4096 * 4, cudaMemcpyHostToDevice));
+    gf2_layout(gf2_pow(static_cast<uint64_t>(L)), host.data() + kTab);
+    tm->seq_jump.alloc(2 * kTab);
+    CK(cudaMemcpy(tm->seq_jump.ptr, host.data(), host.size() * 4, cudaMemcpyHostToDevice));
   }
 }
 
@@ -455,7 +463,7 @@ void mirror_jumps(tmg_machine* tm, tmg::MirrorParams& mp) {
   if ((e && e[0] == '1') || 2 * tm->o < 256) return;
   ensure_jumps(tm);
   mp.jump_chunk = tm->seq_jump.ptr;
-  mp.jump_lits = tm->seq_jump.ptr + 2048;
+  mp.jump_lits = tm->seq_jump.ptr + tmg::kGf2TabWords;
   mp.chunk = (2 * tm->o + 31) / 32;
 }
 
@@ -466,7 +474,7 @@ void seq_jumps(tmg_machine* tm, tmg::SeqParams& sp) {
   ensure_jumps(tm);
   if (tm->seq_tstate.count != static_cast<size_t>(tm->n) * 4) tm->seq_tstate.alloc(static_cast<size_t>(tm->n) * 4);
   sp.jump_chunk = tm->seq_jump.ptr;
-  sp.jump_lits = tm->seq_jump.ptr + 2048;
+  sp.jump_lits = tm->seq_jump.ptr + tmg::kGf2TabWords;
   sp.chunk = chunk;
   sp.tstate = tm->seq_tstate.ptr;
   if (seq_grid_enabled()) {

@@ -7,6 +7,9 @@
 
 namespace tmg {
 
+// One 256 x 256 GF(2) jump matrix as nibble tables (tm_device.cuh gf2_apply).
+constexpr int kGf2TabWords = 64 * 16 * 8;
+
 // Number of kernels this library has launched (evidence for bench.py's gpu_launches).
 extern unsigned long long g_launches;
 inline void count_launch() { __atomic_fetch_add(&g_launches, 1ULL, __ATOMIC_RELAXED); }
@@ -104,8 +107,8 @@ struct SeqParams {  // classic sequential trainer mirror (trainer.cpp:138-179)
   unsigned long long* events;  // [m]
   // Parallel replay of the Type I draws (null: the serial replay). The
   // xoshiro256 state transition is linear over GF(2); jump_chunk = M^chunk
-  // and jump_lits = M^(2o) as 256 x 256 bit matrices in the lane-interleaved
-  // layout [row % 8][word][row / 8] (see sequential.cu gf2_apply).
+  // and jump_lits = M^(2o) as 256 x 256 bit matrices, each as kGf2TabWords
+  // words of nibble tables (see tm_device.cuh gf2_apply).
   const uint32_t* jump_chunk;
   const uint32_t* jump_lits;
   int32_t chunk;          // draws per lane: ceil(2o / 32)

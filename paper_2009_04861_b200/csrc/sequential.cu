@@ -22,6 +22,17 @@ namespace {
 
 constexpr int kSeqThreads = 1024;
 
+// TMG_STATS builds: phase cycle counts of the grid replay's lead warp in
+// P.dbg[200..204] (vote+barrier, scan, barrier, apply+barrier, jumps in scan).
+#ifdef TMG_STATS
+#define TMG_SEQ_CLOCK(var) const long long var = clock64()
+#define TMG_SEQ_ADD(k, v) \
+  if (P.dbg && lane == 0) P.dbg[k] += static_cast<unsigned long long>(v)
+#else
+#define TMG_SEQ_CLOCK(var)
+#define TMG_SEQ_ADD(k, v)
+#endif
+
 __device__ __forceinline__ uint32_t below_dev(Xoshiro& r, uint32_t bound) {  // rng.hpp:68-79
   uint64_t m = static_cast<uint64_t>(static_cast<uint32_t>(r.next())) * bound;
   uint32_t low = static_cast<uint32_t>(m);
@@ -73,40 +84,55 @@ __device__ __forceinline__ bool is_type2(const TrainParams& P, int j, int target
   return P.regress ? !regress_type1 : (target == 1) != positive;
 }
 
-// Parallel replay, phase 1 (one warp, lane 0 owns the stream): gate draws in
-// clause order; a gated Type I clause's state is recorded in S.tstate and its
-// 2o draws skipped with one jump (jl = M^(2o)). Gated bits go to gbits.
-// Returns the number of gated clauses.
+// Parallel replay, phase 1 (one warp): gate draws in clause order; a gated
+// Type I clause's state is recorded in S.tstate and its 2o draws skipped with
+// one jump (jl = M^(2o)). Gated bits go to gbits. Every lane steps its own
+// copy of the stream (identical in all lanes after the broadcast below), so
+// the loop is warp-uniform without shuffles; the gate is the integer test
+// next() < tp << 11 (tm_device.cuh u53_below), the Type I candidates a
+// per-feed bit pattern over j mod 32. Returns the number of gated clauses.
 __device__ unsigned long long scan_bank(const TrainParams& P, const SeqParams& S, Xoshiro& rng, double p, int target,
                                         bool regress_type1, const uint32_t* jl, uint32_t* gbits, int lane) {
-  unsigned long long gated_n = 0;
-  for (int j0 = 0; j0 < P.n; j0 += 32) {
-    uint32_t gw = 0;
-    for (int j = j0; j < min(P.n, j0 + 32); ++j) {
-      int gated = 0;
-      if (lane == 0) gated = rng.uniform() < p ? 1 : 0;
-      gated = __shfl_sync(kFull, gated, 0);
-      if (!gated) continue;
-      gw |= 1u << (j - j0);
-      ++gated_n;
-      if (!is_type2(P, j, target, regress_type1)) {
-        uint64_t* ts = S.tstate + static_cast<size_t>(j) * 4;
-        if (lane == 0) {
-          ts[0] = rng.s0;
-          ts[1] = rng.s1;
-          ts[2] = rng.s2;
-          ts[3] = rng.s3;
-        }
-        uint32_t sw[8];
-        state_to_words(rng, sw);
+  {
+    uint64_t q[4] = {rng.s0, rng.s1, rng.s2, rng.s3};
 #pragma unroll
-        for (int w = 0; w < 8; ++w) sw[w] = __shfl_sync(kFull, sw[w], 0);
-        gf2_apply(jl, sw, lane);
-        rng = words_to_state(sw);
+    for (int k = 0; k < 4; ++k) q[k] = __shfl_sync(kFull, q[k], 0);
+    rng = Xoshiro{q[0], q[1], q[2], q[3]};
+  }
+  const uint64_t tp = u53_below(p);
+  const bool every = (tp >> 53) != 0;  // p >= 1
+  const uint64_t th = tp << 11;        // (next >> 11) < tp  <=>  next < tp * 2^11
+  // is_type2 == false, as bits of j - j0 (j0 even)
+  const uint32_t cand = P.regress ? (regress_type1 ? kFull : 0u)
+                                  : (P.all_positive ? (target ? kFull : 0u) : (target ? 0x55555555u : 0xAAAAAAAAu));
+  unsigned long long gated_n = 0;
+  Xoshiro r = rng;
+  for (int j0 = 0; j0 < P.n; j0 += 32) {
+    const int nb = min(32, P.n - j0);
+    uint32_t gw = 0;
+    for (int b = 0; b < nb; ++b) {
+      if (!every && r.next() >= th) continue;  // skip iff u >= p (trainer.cpp:121)
+      if (every) r.next();
+      gw |= 1u << b;
+      if (!((cand >> b) & 1u)) continue;
+      TMG_SEQ_CLOCK(j0c);
+      if (lane == 0) {
+        uint64_t* ts = S.tstate + static_cast<size_t>(j0 + b) * 4;
+        ts[0] = r.s0;
+        ts[1] = r.s1;
+        ts[2] = r.s2;
+        ts[3] = r.s3;
       }
+      uint32_t sw[8];
+      state_to_words(r, sw);
+      gf2_apply(jl, sw, lane);
+      r = words_to_state(sw);
+      TMG_SEQ_ADD(204, clock64() - j0c);
     }
+    gated_n += __popc(gw);
     if (lane == 0) gbits[j0 >> 5] = gw;
   }
+  rng = r;
   return gated_n;
 }
 
@@ -155,6 +181,7 @@ __device__ void apply_gated(const TrainParams& P, const SeqParams& S, int c, int
   __syncwarp();
   Xoshiro rl = words_to_state(mine);
   const int k0 = lane * S.chunk, k1 = min(L, k0 + S.chunk);
+  const uint64_t th = u53_below(S.p_high), tl = u53_below(S.p_low);
   uint32_t hw = 0, lw = 0;
   int cw = k0 >> 5;
   for (int k = k0; k < k1; ++k) {
@@ -164,9 +191,9 @@ __device__ void apply_gated(const TrainParams& P, const SeqParams& S, int c, int
       hw = lw = 0;
       cw = k >> 5;
     }
-    const double u = rl.uniform();
-    hw |= (u < S.p_high ? 1u : 0u) << (k & 31);
-    lw |= (u < S.p_low ? 1u : 0u) << (k & 31);
+    const uint64_t u = next53(rl);
+    hw |= (u < th ? 1u : 0u) << (k & 31);
+    lw |= (u < tl ? 1u : 0u) << (k & 31);
   }
   if (k1 > k0) {
     if (hw) atomicOr(&hb[cw], hw);
@@ -201,18 +228,21 @@ __device__ void apply_gated(const TrainParams& P, const SeqParams& S, int c, int
 
 template <int B>
 __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainParams P, SeqParams S) {
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem[];
   const int L = 2 * P.o;
   const int refw = (L + 31) / 32 + 2;
-  uint32_t* hbits = smem;                 // u < p_high, reference literal order
-  uint32_t* lbits = smem + refw;          // u < p_low
-  uint32_t* outs = smem + 2 * refw;       // clause outputs of the fed bank (bit per clause)
-  // parallel replay (S.jump_chunk != null): jump matrices, gated bits, and
-  // per-warp draw buffers (hbits / lbits of the clause a warp is applying)
+  // parallel replay (S.jump_chunk != null): jump tables first (16-byte
+  // aligned), then the serial replay's draw bits and the clause outputs, then
+  // the gated bits and per-warp draw buffers (hbits / lbits of the clause a
+  // warp is applying)
+  const int tabw = S.jump_chunk ? 2 * kGf2TabWords : 0;
+  uint32_t* jc = smem;
+  uint32_t* jl = jc + kGf2TabWords;
+  uint32_t* hbits = smem + tabw;          // u < p_high, reference literal order
+  uint32_t* lbits = hbits + refw;         // u < p_low
+  uint32_t* outs = lbits + refw;          // clause outputs of the fed bank (bit per clause)
   const int nwords = (P.n + 31) / 32;
-  uint32_t* jc = outs + nwords;
-  uint32_t* jl = jc + 2048;
-  uint32_t* gbits = jl + 2048;
+  uint32_t* gbits = outs + nwords;
   uint32_t* wbuf = gbits + nwords;
   __shared__ int vote;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
@@ -220,10 +250,10 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
   const size_t cstride = static_cast<size_t>(B) * 2 * Wp;
   Xoshiro rng{S.rng[0], S.rng[1], S.rng[2], S.rng[3]};
   unsigned long long ev_local = 0;
-  for (int k = tid; k < 2 * refw; k += blockDim.x) smem[k] = 0;
+  for (int k = tid; k < 2 * refw; k += blockDim.x) hbits[k] = 0;
   const bool par = S.jump_chunk != nullptr;
   if (par) {
-    for (int k = tid; k < 2048; k += blockDim.x) {
+    for (int k = tid; k < kGf2TabWords; k += blockDim.x) {
       jc[k] = S.jump_chunk[k];
       jl[k] = S.jump_lits[k];
     }
@@ -309,9 +339,10 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
           const int e = target ? T - vc : T + vc;
           p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
         }
+        const uint64_t tp = u53_below(p);
         for (int j = 0; j < n; ++j) {
           int gated = 0;
-          if (lane == 0) gated = rng.uniform() < p ? 1 : 0;
+          if (lane == 0) gated = next53(rng) < tp ? 1 : 0;
           gated = __shfl_sync(kFull, gated, 0);
           if (!gated) continue;
           ++ev_local;
@@ -337,11 +368,12 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_kernel(TrainPara
             }
           } else {  // Type I: 2o draws in literal order (feedback.cpp:45,63)
             if (lane == 0) {
+              const uint64_t th = u53_below(S.p_high), tl = u53_below(S.p_low);
               uint32_t hw = 0, lw = 0;
               for (int k = 0; k < L; ++k) {
-                const double u = rng.uniform();
-                hw |= (u < S.p_high ? 1u : 0u) << (k & 31);
-                lw |= (u < S.p_low ? 1u : 0u) << (k & 31);
+                const uint64_t u = next53(rng);
+                hw |= (u < th ? 1u : 0u) << (k & 31);
+                lw |= (u < tl ? 1u : 0u) << (k & 31);
                 if ((k & 31) == 31 || k == L - 1) {
                   hbits[k >> 5] = hw;
                   lbits[k >> 5] = lw;
@@ -401,19 +433,19 @@ template <int B>
 __global__ void __launch_bounds__(kSeqThreads) train_sequential_grid_kernel(TrainParams P, SeqParams S) {
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem[];
   const int L = 2 * P.o;
   const int refw = (L + 31) / 32 + 2;
   uint32_t* jc = smem;
-  uint32_t* jl = jc + 2048;
-  uint32_t* wbuf = jl + 2048;
+  uint32_t* jl = jc + kGf2TabWords;
+  uint32_t* wbuf = jl + kGf2TabWords;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int n = P.n, Wp = P.Wp, nwords = (n + 31) / 32;
   const int gwarp = blockIdx.x * nwarps + warp, gwarps = gridDim.x * nwarps;
   const bool lead = blockIdx.x == 0 && warp == 0;  // owns the reference stream
   const size_t cstride = static_cast<size_t>(B) * 2 * Wp;
   Xoshiro rng{S.rng[0], S.rng[1], S.rng[2], S.rng[3]};
-  for (int k = tid; k < 2048; k += blockDim.x) {
+  for (int k = tid; k < kGf2TabWords; k += blockDim.x) {
     jc[k] = S.jump_chunk[k];
     jl[k] = S.jump_lits[k];
   }
@@ -430,6 +462,7 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_grid_kernel(Trai
       const int target = feed == 0 ? 1 : 0;
       uint32_t* outs = S.g_outs + static_cast<size_t>(slot) * nwords;
       int32_t* vote = S.g_misc + slot;
+      TMG_SEQ_CLOCK(c0);
       // (a) vote pass (trainer.cpp:62-68)
       for (int j = gwarp; j < n; j += gwarps) {
         const uint32_t* top = P.state + (static_cast<size_t>(c) * n + j) * cstride + static_cast<size_t>(B - 1) * 2 * Wp;
@@ -448,6 +481,7 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_grid_kernel(Trai
         }
       }
       grid.sync();
+      TMG_SEQ_CLOCK(c1);
       // (b) gate scan
       if (lead) {
         if (feed == 0 && !P.regress && lane == 0) {
@@ -468,7 +502,9 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_grid_kernel(Trai
         for (int k = lane; k < nwords; k += 32) other[k] = 0;
         if (lane == 0) S.g_misc[slot ^ 1] = 0;
       }
+      TMG_SEQ_CLOCK(c2);
       grid.sync();
+      TMG_SEQ_CLOCK(c3);
       // (c) apply the gated clauses
       if (warp < S.par_warps) {
         bool rt1;
@@ -481,6 +517,14 @@ __global__ void __launch_bounds__(kSeqThreads) train_sequential_grid_kernel(Trai
         }
       }
       grid.sync();
+#ifdef TMG_STATS
+      if (lead) {
+        TMG_SEQ_ADD(200, c1 - c0);
+        TMG_SEQ_ADD(201, c2 - c1);
+        TMG_SEQ_ADD(202, c3 - c2);
+        TMG_SEQ_ADD(203, clock64() - c3);
+      }
+#endif
     }
   }
   if (lead && lane == 0) {
@@ -499,8 +543,8 @@ bool train_sequential_launch(const TrainParams& p, const SeqParams& sp_in, int B
   SeqParams sp = sp_in;
   size_t words = 2 * refw + nwords;
   if (sp.jump_chunk) {  // parallel replay: as many applying warps as shared memory holds draw buffers for
-    const size_t fixed = words + 4096 + nwords;
-    const size_t budget = 200 * 1024 / sizeof(uint32_t);
+    const size_t fixed = words + 2 * kGf2TabWords + nwords;
+    const size_t budget = 220 * 1024 / sizeof(uint32_t);  // of the 227 KB a CTA may opt into
     const long pw = fixed < budget ? static_cast<long>((budget - fixed) / (2 * refw)) : 0;
     sp.par_warps = static_cast<int32_t>(std::min<long>(kSeqThreads / 32, pw));
     if (sp.par_warps < 1) {
@@ -511,7 +555,7 @@ bool train_sequential_launch(const TrainParams& p, const SeqParams& sp_in, int B
   }
   const size_t shm = sizeof(uint32_t) * words;
   if (sp.jump_chunk && sp.g_outs) {  // grid-wide replay: one CTA per SM, as many as there are clauses for
-    const size_t gshm = sizeof(uint32_t) * (4096 + static_cast<size_t>(sp.par_warps) * 2 * refw);
+    const size_t gshm = sizeof(uint32_t) * (2 * kGf2TabWords + static_cast<size_t>(sp.par_warps) * 2 * refw);
     auto grid_go = [&](auto kern) {
       if (gshm > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(gshm));

@@ -95,25 +95,55 @@ struct Xoshiro {
   }
 };
 
+// The comparison u < p of a reference draw u = m * 2^-53 (m = next() >> 11 <
+// 2^53) as an integer test m < u53_below(p): p * 2^53 is exact in double, so
+// m * 2^-53 < p  <=>  m < p * 2^53  <=>  m < ceil(p * 2^53). NaN: never true.
+__device__ __forceinline__ uint64_t u53_below(double p) {
+  if (!(p > 0.0)) return 0;
+  if (p >= 1.0) return uint64_t(1) << 53;
+  return static_cast<uint64_t>(ceil(p * 0x1.0p53));
+}
+__device__ __forceinline__ uint64_t next53(Xoshiro& r) { return r.next() >> 11; }
+
 // ---- xoshiro256 jump-ahead on the GPU: the state update of rng.hpp next()
-// is linear over GF(2), so k steps are one 256 x 256 bit matrix (built on the
-// host, engine.cu seq_jump_rows). A warp applies it cooperatively: lane L
-// computes output bits 8L .. 8L+7 (row r of that byte: parity(row & s)),
-// the 32 bytes are gathered with one OR-reduction per 32-bit word. The
-// matrix lives in shared memory as [r][w][L] (row 8L + r, word w), so for a
-// fixed (r, w) the 32 lanes read 32 consecutive words (no bank conflicts).
-__device__ __forceinline__ void gf2_apply(const uint32_t* mt, uint32_t (&s)[8], int lane) {
-  uint32_t byte = 0;
+// is linear over GF(2), so k steps are one 256 x 256 bit matrix M (built on
+// the host, engine.cu gf2_pow). It is stored as nibble tables: entry (pos, v)
+// = the 8 words of M * (v << 4 pos), i.e. the XOR of the columns of M for the
+// set bits of nibble value v at nibble position pos (64 x 16 entries, 32 KB).
+// A warp applies it cooperatively: lane L looks up the two nibbles of state
+// byte L and the 32 partial products are XOR-reduced (redux.sync) per word.
+#ifndef TMG_GF2_REDUX
+#define TMG_GF2_REDUX 1  // one redux.sync per word (0: shuffle reduce-scatter, measured slower)
+#endif
+__device__ __forceinline__ void gf2_apply(const uint32_t* tab, uint32_t (&s)[8], int lane) {
+  const int ws = lane >> 2;
+  uint32_t v = s[0];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
-    uint32_t acc = 0;
+  for (int k = 1; k < 8; ++k) v = ws == k ? s[k] : v;
+  const uint32_t byte = (v >> (8 * (lane & 3))) & 0xFFu;
+  const uint4* e0 = reinterpret_cast<const uint4*>(tab + ((2 * lane) * 16 + (byte & 15u)) * 8);
+  const uint4* e1 = reinterpret_cast<const uint4*>(tab + ((2 * lane + 1) * 16 + (byte >> 4)) * 8);
+  const uint4 a0 = e0[0], a1 = e0[1], b0 = e1[0], b1 = e1[1];
+  const uint32_t x[8] = {a0.x ^ b0.x, a0.y ^ b0.y, a0.z ^ b0.z, a0.w ^ b0.w,
+                         a1.x ^ b1.x, a1.y ^ b1.y, a1.z ^ b1.z, a1.w ^ b1.w};
+#if TMG_GF2_REDUX
 #pragma unroll
-    for (int w = 0; w < 8; ++w) acc ^= mt[(r * 8 + w) * 32 + lane] & s[w];
-    byte |= (static_cast<uint32_t>(__popc(acc)) & 1u) << r;
-  }
-  const uint32_t mine = byte << (8 * (lane & 3));
+  for (int w = 0; w < 8; ++w) s[w] = __reduce_xor_sync(kFull, x[w]);
+#else
+  // Reduce-scatter by halving (lane bits 4, 3, 2 pick the half kept), then
+  // the last two lane bits, so lane L ends with word L >> 2; then gather.
+  const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+  uint32_t y[4], z[2];
 #pragma unroll
-  for (int w = 0; w < 8; ++w) s[w] = __reduce_or_sync(kFull, (lane >> 2) == w ? mine : 0u);
+  for (int k = 0; k < 4; ++k) y[k] = (h4 ? x[k + 4] : x[k]) ^ __shfl_xor_sync(kFull, h4 ? x[k] : x[k + 4], 16);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) z[k] = (h3 ? y[k + 2] : y[k]) ^ __shfl_xor_sync(kFull, h3 ? y[k] : y[k + 2], 8);
+  uint32_t v1 = (h2 ? z[1] : z[0]) ^ __shfl_xor_sync(kFull, h2 ? z[0] : z[1], 4);
+  v1 ^= __shfl_xor_sync(kFull, v1, 2);
+  v1 ^= __shfl_xor_sync(kFull, v1, 1);
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s[w] = __shfl_sync(kFull, v1, 4 * w);
+#endif
 }
 
 __device__ __forceinline__ void state_to_words(const Xoshiro& r, uint32_t (&s)[8]) {
@@ -161,6 +191,7 @@ __device__ __forceinline__ void draw_type_i_bits(Xoshiro& rng, int L, int chunk,
   __syncwarp();
   Xoshiro rl = words_to_state(mine);
   const int k0 = lane * chunk, k1 = min(L, k0 + chunk);
+  const uint64_t th = u53_below(p_high), tl = u53_below(p_low);
   uint32_t hw = 0, lw = 0;
   int cw = k0 >> 5;
   for (int k = k0; k < k1; ++k) {
@@ -170,9 +201,9 @@ __device__ __forceinline__ void draw_type_i_bits(Xoshiro& rng, int L, int chunk,
       hw = lw = 0;
       cw = k >> 5;
     }
-    const double u = rl.uniform();
-    hw |= (u < p_high ? 1u : 0u) << (k & 31);
-    lw |= (u < p_low ? 1u : 0u) << (k & 31);
+    const uint64_t u = next53(rl);
+    hw |= (u < th ? 1u : 0u) << (k & 31);
+    lw |= (u < tl ? 1u : 0u) << (k & 31);
   }
   if (k1 > k0) {
     if (hw) atomicOr(&hbits[cw], hw);

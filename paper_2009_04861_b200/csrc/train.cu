@@ -161,19 +161,20 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
 // draws in literal order k = 0..2o-1 (feedback.cpp:45,63).
 template <int NW, int B>
 __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorParams M) {
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x;
   const int L = 2 * P.o;
   const int refw = (L + 31) / 32 + 2;  // + padding for funnel shifts
-  uint32_t* hbits = smem;              // u < p_high, reference literal order
-  uint32_t* lbits = smem + refw;       // u < p_low
-  uint32_t* jc = smem + 2 * refw;      // jump matrices (M.jump_chunk != null)
-  uint32_t* jl = jc + 2048;
+  const int tabw = M.jump_chunk ? 2 * kGf2TabWords : 0;
+  uint32_t* jc = smem;                 // jump tables (M.jump_chunk != null)
+  uint32_t* jl = jc + kGf2TabWords;
+  uint32_t* hbits = smem + tabw;       // u < p_high, reference literal order
+  uint32_t* lbits = hbits + refw;      // u < p_low
   const int64_t q = P.q;
   const int T = P.margin;
-  for (int k = lane; k < 2 * refw; k += 32) smem[k] = 0;
+  for (int k = lane; k < 2 * refw; k += 32) hbits[k] = 0;
   if (M.jump_chunk)
-    for (int k = lane; k < 2048; k += 32) {
+    for (int k = lane; k < kGf2TabWords; k += 32) {
       jc[k] = M.jump_chunk[k];
       jl[k] = M.jump_lits[k];
     }
@@ -204,11 +205,12 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
         draw_type_i_bits(rng, L, M.chunk, M.p_high, M.p_low, jc, jl, hbits, lbits, refw, lane);
       } else {
         if (lane == 0) {
+          const uint64_t th = u53_below(M.p_high), tl = u53_below(M.p_low);
           uint32_t hw = 0, lw = 0;
           for (int k = 0; k < L; ++k) {
-            const double u = rng.uniform();
-            hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
-            lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
+            const uint64_t u = next53(rng);
+            hw |= (u < th ? 1u : 0u) << (k & 31);
+            lw |= (u < tl ? 1u : 0u) << (k & 31);
             if ((k & 31) == 31 || k == L - 1) {
               hbits[k >> 5] = hw;
               lbits[k >> 5] = lw;
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
         for (int sidx = 0; sidx < steps; ++sidx) {
           const double ps = __shfl_sync(kFull, p, sidx);
           int gated = 0;
-          if (lane == 0) gated = rng.uniform() < ps ? 1 : 0;  // skip iff u >= p (trainer.cpp:121)
+          if (lane == 0) gated = next53(rng) < u53_below(ps) ? 1 : 0;  // skip iff u >= p (trainer.cpp:121)
           gated = __shfl_sync(kFull, gated, 0);
           if (!gated) continue;
           ++events;
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
           p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
           target = (y == 1) == positive ? 1 : 0;
         }
-        gated = rng.uniform() < p ? 1 : 0;  // skip iff u >= p (trainer.cpp:121)
+        gated = next53(rng) < u53_below(p) ? 1 : 0;  // skip iff u >= p (trainer.cpp:121)
       }
       gated = __shfl_sync(kFull, gated, 0);
       if (!gated) continue;
@@ -385,20 +387,21 @@ __global__ void __launch_bounds__(32) train_mirror_kernel(TrainParams P, MirrorP
 // place in HBM (lane-owned words, as in sequential.cu), the row is read on use.
 template <int B>
 __global__ void __launch_bounds__(32) train_mirror_wide_kernel(TrainParams P, MirrorParams M) {
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x;
   const int L = 2 * P.o;
   const int refw = (L + 31) / 32 + 2;
-  uint32_t* hbits = smem;
-  uint32_t* lbits = smem + refw;
-  uint32_t* jc = smem + 2 * refw;
-  uint32_t* jl = jc + 2048;
+  const int tabw = M.jump_chunk ? 2 * kGf2TabWords : 0;
+  uint32_t* jc = smem;  // jump tables (M.jump_chunk != null)
+  uint32_t* jl = jc + kGf2TabWords;
+  uint32_t* hbits = smem + tabw;
+  uint32_t* lbits = hbits + refw;
   const int64_t q = P.q;
   const int T = P.margin;
   const int Wp = P.Wp, words = P.Wp >> 5;
-  for (int k = lane; k < 2 * refw; k += 32) smem[k] = 0;
+  for (int k = lane; k < 2 * refw; k += 32) hbits[k] = 0;
   if (M.jump_chunk)
-    for (int k = lane; k < 2048; k += 32) {
+    for (int k = lane; k < kGf2TabWords; k += 32) {
       jc[k] = M.jump_chunk[k];
       jl[k] = M.jump_lits[k];
     }
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(32) train_mirror_wide_kernel(TrainParams P, Mi
           p = static_cast<double>(e) / (2.0 * static_cast<double>(T));
           target = (y == 1) == positive ? 1 : 0;
         }
-        gated = rng.uniform() < p ? 1 : 0;
+        gated = next53(rng) < u53_below(p) ? 1 : 0;
       }
       gated = __shfl_sync(kFull, gated, 0);
       if (!gated) continue;
@@ -503,11 +506,12 @@ __global__ void __launch_bounds__(32) train_mirror_wide_kernel(TrainParams P, Mi
           draw_type_i_bits(rng, L, M.chunk, M.p_high, M.p_low, jc, jl, hbits, lbits, refw, lane);
         } else {
           if (lane == 0) {
+            const uint64_t th = u53_below(M.p_high), tl = u53_below(M.p_low);
             uint32_t hw = 0, lw = 0;
             for (int k = 0; k < L; ++k) {
-              const double u = rng.uniform();
-              hw |= (u < M.p_high ? 1u : 0u) << (k & 31);
-              lw |= (u < M.p_low ? 1u : 0u) << (k & 31);
+              const uint64_t u = next53(rng);
+              hw |= (u < th ? 1u : 0u) << (k & 31);
+              lw |= (u < tl ? 1u : 0u) << (k & 31);
               if ((k & 31) == 31 || k == L - 1) {
                 hbits[k >> 5] = hw;
                 lbits[k >> 5] = lw;
@@ -645,7 +649,7 @@ void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
 template <int NW, int B>
 void launch_mirror(const TrainParams& p, const MirrorParams& mp, cudaStream_t s) {
   const int refw = (2 * p.o + 31) / 32 + 2;
-  const size_t shm = sizeof(uint32_t) * (2 * refw + (mp.jump_chunk ? 4096 : 0));
+  const size_t shm = sizeof(uint32_t) * (2 * refw + (mp.jump_chunk ? 2 * kGf2TabWords : 0));
   if (shm > 48 * 1024)
     cudaFuncSetAttribute(train_mirror_kernel<NW, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(shm));
@@ -698,7 +702,7 @@ bool dispatch_mirror(const TrainParams& p, const MirrorParams& mp, int NW, cudaS
     case 16: launch_mirror<16, B>(p, mp, s); return true;
     default: {  // rows wider than 16 words per lane: planes in place
       const int refw = (2 * p.o + 31) / 32 + 2;
-      const size_t shm = sizeof(uint32_t) * (2 * refw + (mp.jump_chunk ? 4096 : 0));
+      const size_t shm = sizeof(uint32_t) * (2 * refw + (mp.jump_chunk ? 2 * kGf2TabWords : 0));
       if (shm > 227 * 1024) return false;
       if (shm > 48 * 1024)
         cudaFuncSetAttribute(train_mirror_wide_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
