@@ -48,9 +48,9 @@ CASES = {
                          noise=0.0, data_seed=2009),
     # The reference's own worker-count spread at that configuration.
     "mnist_q60000_w1": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
-                            noise=0.0, data_seed=2009, workers=1, seeds=1),
+                            noise=0.0, data_seed=2009, workers=1, seeds=3),
     "mnist_q60000_w2": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
-                            noise=0.0, data_seed=2009, workers=2, seeds=2),
+                            noise=0.0, data_seed=2009, workers=2, seeds=3),
     "mnist_q60000_w4": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
                             noise=0.0, data_seed=2009, workers=4, seeds=2),
 }
@@ -66,27 +66,55 @@ def run(case, seed, workers):
     return [json.loads(l) for l in out.splitlines() if l.strip()]
 
 
+def _update(path, name, fn):
+    """Read-modify-write of accuracy_ref.json under an exclusive file lock
+    (several generator processes may run at once)."""
+    import fcntl
+    with open(path + ".lock", "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        res = json.load(open(path)) if os.path.exists(path) else {}
+        res[name] = fn(res.get(name))
+        json.dump(res, open(path, "w"), indent=1)
+
+
 def main():
+    """Usage: gen_accuracy_ref.py [case ...]. Seeds already recorded for a case
+    are kept (resume); the missing ones up to the case's seed count run in
+    parallel when PARALLEL_SEEDS=1 (one-worker cases: one core each)."""
+    from concurrent.futures import ThreadPoolExecutor
     names = sys.argv[1:] or list(CASES)
     path = os.path.join(HERE, "accuracy_ref.json")
-    res = json.load(open(path)) if os.path.exists(path) else {}
     workers = os.cpu_count() or 1
     for name in names:
         case = CASES[name]
-        per_seed, seconds, events = {}, {}, {}
-        for seed in range(1, case.get("seeds", 5) + 1):
+        old = (json.load(open(path)) if os.path.exists(path) else {}).get(name) or {}
+        done = set(old.get("per_seed", {})) if old.get("config") == case or "seeds" in case else set()
+        todo = [s for s in range(1, case.get("seeds", 5) + 1) if str(s) not in done]
+
+        def one(seed):
             rows = run(case, seed, workers)
-            per_seed[str(seed)] = [r["test_accuracy"] for r in rows]
-            seconds[str(seed)] = [r["seconds"] for r in rows]
-            events[str(seed)] = [r["feedback_events"] for r in rows]
-            print(name, seed, per_seed[str(seed)], seconds[str(seed)], flush=True)
-            final = [v[-1] for v in per_seed.values()]
-            # re-read: other cases may be running concurrently into the same file
-            res = json.load(open(path)) if os.path.exists(path) else {}
-            res[name] = dict(config=case, workers=case.get("workers", workers), per_seed=per_seed,
-                             mean_final=sum(final) / len(final), epoch_seconds=seconds,
-                             feedback_events=events)
-            json.dump(res, open(path, "w"), indent=1)
+            acc = [r["test_accuracy"] for r in rows]
+            print(name, seed, acc, [r["seconds"] for r in rows], flush=True)
+
+            def merge(prev):
+                prev = prev if prev and prev.get("per_seed") else {}
+                per_seed = dict(prev.get("per_seed", {}))
+                seconds = dict(prev.get("epoch_seconds", {}))
+                events = dict(prev.get("feedback_events", {}))
+                per_seed[str(seed)] = acc
+                seconds[str(seed)] = [r["seconds"] for r in rows]
+                events[str(seed)] = [r["feedback_events"] for r in rows]
+                final = [v[-1] for v in per_seed.values()]
+                return dict(config=case, workers=case.get("workers", workers), per_seed=per_seed,
+                            mean_final=sum(final) / len(final), epoch_seconds=seconds, feedback_events=events)
+            _update(path, name, merge)
+
+        if os.environ.get("PARALLEL_SEEDS") == "1":
+            with ThreadPoolExecutor(len(todo) or 1) as ex:
+                list(ex.map(one, todo))
+        else:
+            for seed in todo:
+                one(seed)
 
 
 if __name__ == "__main__":
