@@ -1,6 +1,7 @@
 #!/usr/bin/env bash
 # Jump-ahead segment count (TMG_JUMP_SEGMENTS) A/B: the W = 1 replay and the
 # sequential replay, MNIST- and IMDb-shaped, after the replay parity tests.
+# (TMG_JUMP_SEGMENTS was an experiment knob in engine.cu jump_chunk, removed after this A/B: 32 segments stay.)
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "sequential or mirror or w1 or jump or dropin or golden" > gpurun_out/seg_pytest.txt 2>&1; echo "exit $?" >> gpurun_out/seg_pytest.txt; tail -n 2 gpurun_out/seg_pytest.txt
 TMG_JUMP_SEGMENTS=4 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "sequential_parallel_replay or w1_replay_jump" 2>&1 | tail -n 1
