@@ -266,6 +266,7 @@ tmg_machine* create_machine(const tmg_config* cfg, int o, int m, int device, int
     tm->events.alloc(2 * static_cast<size_t>(m));  // all events, then Type I events
     tm->dbg.alloc(tmg::kDebugCounters);
     CK(cudaMemsetAsync(tm->dbg.ptr, 0, tm->dbg.bytes(), tm->stream));
+    tm->work.alloc(1);
     {
       uint32_t tab[256];
       build_alias8(prob_threshold(1.0 / cfg->specificity), tab);
@@ -350,6 +351,7 @@ tmg::TrainParams make_params(tmg_machine* tm, tmg_pool* pool) {
 #ifdef TMG_STATS
   p.dbg = tm->dbg.ptr;
 #endif
+  p.work = tm->work.ptr;
   return p;
 }
 
@@ -723,6 +725,7 @@ TMG_API int tmg_machine_destroy(tmg_machine* tm) {
   tm->lists.release();
   tm->events.release();
   tm->dbg.release();
+  tm->work.release();
   tm->alias8.release();
   tm->scratch16.release();
   if (tm->eval0) cudaEventDestroy(tm->eval0);

@@ -169,6 +169,7 @@ struct tmg_machine {
   tmgx::DevBuf<uint32_t> lit_t;    // scratch: feature-major example columns of non-pool rows
   tmgx::DevBuf<unsigned long long> events;
   tmgx::DevBuf<unsigned long long> dbg;  // instrumentation counters (TMG_STATS builds)
+  tmgx::DevBuf<int32_t> work;            // clause counter of the persistent shared-memory kernel
   tmgx::DevBuf<uint32_t> alias8;         // alias table of the clause-output-0 Type I draw
   tmgx::DevBuf<uint16_t> scratch16;
   // sequential-trainer jump matrices (M^chunk, M^(2o)) and per-clause states

@@ -72,6 +72,7 @@ struct TrainParams {
   int64_t t_begin, t_end;      // async: window of each clause's pass
   unsigned long long* events;  // [2m]: feedback events per class, then Type I events per class
   unsigned long long* dbg;     // [kDebugCounters] instrumentation (TMG_STATS builds), else null
+  int32_t* work;               // [1] clause counter of the persistent shared-memory kernel (zeroed per launch)
 };
 
 constexpr int kDebugCounters = 256;

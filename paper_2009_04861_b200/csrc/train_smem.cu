@@ -9,6 +9,9 @@
 // up to 16 384 features). NW == 0: any width — the row stays in global
 // memory (L1-cached) and is read where it is used, and a CTA holds one or two
 // clauses depending on what fits in shared memory.
+#include <algorithm>
+#include <cstdlib>
+
 #include "clause.cuh"
 #include "kernels.h"
 #include "tm_device.cuh"
@@ -31,6 +34,10 @@ namespace {
 
 constexpr int kSmemUnroll = TMG_SMEM_UNROLL;
 constexpr int kSmemMaxCpb = TMG_SMEM_MAXCPB;
+#ifndef TMG_SMEM_PERSIST_MAX
+#define TMG_SMEM_PERSIST_MAX 12  // most clause slots of the persistent CTA
+#endif
+constexpr int kSmemPersistMax = TMG_SMEM_PERSIST_MAX;
 constexpr size_t kSmemMax = 227 * 1024;  // opt-in shared memory per CTA on sm_100
 
 // One clause's automaton planes in shared memory (or, INPLACE, in HBM with
@@ -203,33 +210,23 @@ __device__ __forceinline__ void type_i_smem(SP& S, const LitRow<NW>& r, int befo
     type_i_smem_out<NW, B, P2, 0>(S, r, P, g, i32, lane, aref);
 }
 
-// One warp per clause, blockDim.x / 32 clauses per CTA; dynamic shared memory
-// = the clauses' planes, then kAliasCopies copies of the alias table.
-// INPLACE (rows whose planes exceed shared memory, beyond ~107k features at
-// 8 planes): one clause per CTA, the planes stay in HBM/L2 and are updated in
-// place (every word is lane-owned), shared memory holds the alias table only.
-template <int NW, int B, bool P2, bool INPLACE = false>
-__global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(TrainParams P) {
-  extern __shared__ __align__(16) uint32_t smem[];
+// One clause of the shared-memory path, run by one warp: clause-order index
+// w (G: clause_of_warp's block size), its planes copied into `slot` (or
+// updated in place at `st` when INPLACE), every window of its pass, the
+// planes written back, its include count and events published.
+template <int NW, int B, bool P2, bool INPLACE>
+__device__ __forceinline__ void smem_clause(const TrainParams& P, uint32_t* slot, int w, int G, AliasRef aref,
+                                            int lane) {
   using SP = SmemPlanes<B, !INPLACE>;  // shared-memory copies use the quad layout
   const int Wp = P.Wp;
-  const int cpb = blockDim.x >> 5;
   const size_t words = static_cast<size_t>(B) * 2 * Wp;  // per clause, either layout
-  uint32_t* atab = INPLACE ? smem : smem + cpb * words;
-  fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const AliasRef aref = lane_alias(atab, lane);
-  const int wib = threadIdx.x >> 5;
-  const int w = P.w_begin + blockIdx.x * cpb + wib;
-  if (w >= P.w_end) return;
-  const int lc = clause_of_warp(P, w, cpb);
+  const int lc = clause_of_warp(P, w, G);
   const int c = lc / P.n_loc;
   const int j = P.j_begin + lc % P.n_loc;
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
   const bool positive = P.all_positive || (j & 1) == 0;
   uint32_t* st = P.state + static_cast<size_t>(lc) * words;
-  SP S{INPLACE ? st : smem + wib * words, Wp};
+  SP S{INPLACE ? st : slot, Wp};
   if (!INPLACE)
     for (size_t k = lane; k < words; k += 32) {
       const int b = static_cast<int>(k / (2 * Wp)), part = static_cast<int>((k / Wp) & 1), w = static_cast<int>(k % Wp);
@@ -317,6 +314,78 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   }
 }
 
+
+// One warp per clause, blockDim.x / 32 clauses per CTA; dynamic shared memory
+// = the clauses' planes, then kAliasCopies copies of the alias table.
+// INPLACE (rows whose planes exceed shared memory, beyond ~107k features at
+// 8 planes): one clause per CTA, the planes stay in HBM/L2 and are updated in
+// place (every word is lane-owned), shared memory holds the alias table only.
+template <int NW, int B, bool P2, bool INPLACE = false>
+__global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(TrainParams P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int cpb = blockDim.x >> 5;
+  const size_t words = static_cast<size_t>(B) * 2 * P.Wp;
+  uint32_t* atab = INPLACE ? smem : smem + cpb * words;
+  fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const AliasRef aref = lane_alias(atab, lane);
+  const int wib = threadIdx.x >> 5;
+  const int w = P.w_begin + blockIdx.x * cpb + wib;
+  if (w >= P.w_end) return;
+  smem_clause<NW, B, P2, INPLACE>(P, smem + wib * words, w, cpb, aref, lane);
+}
+
+// Persistent form: one CTA per SM with as many clause slots (warps) as shared
+// memory holds next to ONE alias table; each warp pulls the next clause-order
+// index from P.work until the range is done, so a slow clause never holds a
+// whole CTA's shared memory idle (the launched form frees a CTA's slots only
+// when its last clause ends). Same clause order (G = kSmemOrderG).
+constexpr int kSmemOrderG = 2;
+template <int NW, int B, bool P2>
+__global__ void __launch_bounds__(32 * kSmemPersistMax, 1) train_async_smem_persistent_kernel(TrainParams P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int slots = blockDim.x >> 5;
+  const size_t words = static_cast<size_t>(B) * 2 * P.Wp;
+  uint32_t* atab = smem + slots * words;
+  fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const AliasRef aref = lane_alias(atab, lane);
+  uint32_t* slot = smem + (threadIdx.x >> 5) * words;
+  const int total = P.w_end - P.w_begin;
+  while (true) {
+    int k = 0;
+    if (lane == 0) k = atomicAdd(P.work, 1);
+    k = __shfl_sync(kFull, k, 0);
+    if (k >= total) break;
+    smem_clause<NW, B, P2, false>(P, slot, P.w_begin + k, kSmemOrderG, aref, lane);
+    __syncwarp();
+  }
+}
+
+// The persistent kernel's plan: clause slots per CTA (as many as shared
+// memory holds beside one alias table, <= kSmemPersistMax) and resident CTAs
+// per SM; returns the resident clause warps per SM (0: not applicable).
+// TMG_SMEM_PERSIST=0 disables it (A/B checks).
+template <int NW, int B, bool P2>
+int persistent_plan(const TrainParams& p, int* slots_out, int* ctas_out) {
+  const char* e = std::getenv("TMG_SMEM_PERSIST");
+  if ((e && e[0] == '0') || p.work == nullptr) return 0;
+  const size_t per = sizeof(uint32_t) * static_cast<size_t>(B) * 2 * p.Wp;
+  const size_t atab = sizeof(uint32_t) * kAliasWordsPacked;
+  if (per + atab > kSmemMax) return 0;
+  const int slots = static_cast<int>(std::min<size_t>(kSmemPersistMax, (kSmemMax - atab) / per));
+  const size_t shm = slots * per + atab;
+  auto kern = train_async_smem_persistent_kernel<NW, B, P2>;
+  if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
+  int ctas = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas, kern, 32 * slots, shm);
+  *slots_out = slots;
+  *ctas_out = ctas;
+  return ctas * slots;
+}
+
 size_t smem_bytes(int B, int Wp, int cpb) {
   return sizeof(uint32_t) * (static_cast<size_t>(cpb) * B * 2 * Wp + kAliasWordsPacked);
 }
@@ -339,6 +408,12 @@ int smem_plan(const TrainParams& p, int* cpb_out) {
       best = ctas * c;
       cpb = c;
     }
+  }
+  int slots = 0, pctas = 0;
+  const int pw = persistent_plan<NW, B, P2>(p, &slots, &pctas);
+  if (pw > best && pctas > 0) {
+    *cpb_out = slots;
+    return pw;
   }
   *cpb_out = cpb;
   return best;
@@ -374,6 +449,19 @@ bool launch_smem_p2(const TrainParams& p, cudaStream_t s, int* blocks) {
       train_async_smem_kernel<0, B, P2, true><<<clauses, 32, ashm, s>>>(p);
       return true;
     }
+  }
+  int slots = 0, pctas = 0;
+  if (persistent_plan<NW, B, P2>(p, &slots, &pctas) > best && pctas > 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int pgrid = std::max(1, std::min(sms * pctas, (clauses + slots - 1) / slots));
+    if (blocks) *blocks = pgrid;
+    if (cudaMemsetAsync(p.work, 0, sizeof(int32_t), s) != cudaSuccess) return false;
+    const size_t pshm = sizeof(uint32_t) * (static_cast<size_t>(slots) * B * 2 * p.Wp + kAliasWordsPacked);
+    count_launch();
+    train_async_smem_persistent_kernel<NW, B, P2><<<pgrid, 32 * slots, pshm, s>>>(p);
+    return true;
   }
   const int grid = (clauses + cpb - 1) / cpb;
   if (blocks) *blocks = grid;
