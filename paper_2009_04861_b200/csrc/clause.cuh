@@ -317,8 +317,9 @@ __device__ __forceinline__ int64_t clause_offset_dev(uint32_t g, int64_t q) {
 #ifndef TMG_ALIAS_HOIST
 #define TMG_ALIAS_HOIST 1
 #endif
+template <int C = kAliasCopies>
 __device__ __forceinline__ AliasRef lane_alias(const uint32_t* tab, int lane) {
-  AliasRef r = alias_ref(tab, static_cast<uint32_t>(lane) & (kAliasCopies - 1));
+  AliasRef r = alias_ref(tab, static_cast<uint32_t>(lane) & (C - 1));
 #if TMG_ALIAS_HOIST
   asm volatile("mov.u32 %0, %0;" : "+r"(r.base));
   asm volatile("mov.u32 %0, %0;" : "+r"(r.pbase));

@@ -404,18 +404,27 @@ __device__ __forceinline__ void type_i_planes(Planes<B>& w, uint32_t lit, int ou
 // to 2^-32 units, engine.cu build_alias8), each literal's within 2^-25 of p. One Philox block = the 32 literals of a word slot;
 // `tab` holds kAliasCopies interleaved copies of the 256 entries so the 32
 // lanes' random lookups hit at most two shared-memory wavefronts.
-constexpr int kAliasCopies = 16;
+#ifndef TMG_ALIAS_COPIES
+#define TMG_ALIAS_COPIES 16
+#endif
+constexpr int kAliasCopies = TMG_ALIAS_COPIES;
 // Shared-memory image of the table: thresholds (threshold << 8, low byte 0)
 // as 256 x kAliasCopies u32, then the alias patterns as 256 x kAliasCopies
 // bytes (20 KB). The threshold test is then a plain u < E (no masking), and
 // the second lookup goes to the lightly used LSU pipe instead of the ALU.
 constexpr int kAliasWords = 256 * kAliasCopies + 256 * kAliasCopies / 4;
 
-// The packed image (16 KB: entries threshold << 8 | alias as they are),
-// for kernels whose occupancy is bound by shared memory (train_smem.cu).
-constexpr int kAliasWordsPacked = 256 * kAliasCopies;
+// The packed image (entries threshold << 8 | alias as they are, C copies:
+// 4 KB at C = 4), for kernels whose occupancy is bound by shared memory
+// (train_smem.cu: fewer copies, one more resident clause per SM at IMDb shape).
+#ifndef TMG_SMEM_ALIAS_COPIES
+#define TMG_SMEM_ALIAS_COPIES 4
+#endif
+constexpr int kSmemAliasCopies = TMG_SMEM_ALIAS_COPIES;
+constexpr int kAliasWordsPacked = 256 * kSmemAliasCopies;
+template <int C = kSmemAliasCopies>
 __device__ __forceinline__ void fill_alias_packed(uint32_t* tab, const uint32_t* entries, int tid, int n) {
-  for (int k = tid; k < 256 * kAliasCopies; k += n) tab[k] = __ldg(entries + k / kAliasCopies);
+  for (int k = tid; k < 256 * C; k += n) tab[k] = __ldg(entries + k / C);
 }
 
 // Fills the split image from the machine's 256 packed entries
@@ -441,7 +450,7 @@ __device__ __forceinline__ AliasRef alias_ref(const uint32_t* tab, uint32_t lane
 }
 
 // The 32-literal pattern of one word slot from one Philox block (4 draws).
-template <bool SPLIT = true>
+template <bool SPLIT = true, int C = kAliasCopies>
 __device__ __forceinline__ uint32_t alias_word(const U4 r, AliasRef ar, uint32_t need) {
   uint32_t b[4];
 #pragma unroll
@@ -449,10 +458,10 @@ __device__ __forceinline__ uint32_t alias_word(const U4 r, AliasRef ar, uint32_t
     const uint32_t u = j == 0 ? r.x : (j == 1 ? r.y : (j == 2 ? r.z : r.w));
     const uint32_t col = u & 0xFFu;
     uint32_t e;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(mad_u32(col, 4u * kAliasCopies, ar.base)));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(e) : "r"(mad_u32(col, 4u * C, ar.base)));
     if (SPLIT) {
       uint32_t a;
-      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(a) : "r"(mad_u32(col, kAliasCopies, ar.pbase)));
+      asm volatile("ld.shared.u8 %0, [%1];" : "=r"(a) : "r"(mad_u32(col, C, ar.pbase)));
       b[j] = u < e ? u : a;  // (u >> 8) < threshold: the column's own pattern; low byte = the draw
     } else {
       b[j] = (u | 0xFFu) < e ? u : e;  // the same test on the packed entry
@@ -462,10 +471,10 @@ __device__ __forceinline__ uint32_t alias_word(const U4 r, AliasRef ar, uint32_t
   return __byte_perm(lo, hi, 0x5410) & need;
 }
 
-template <int K, bool SPLIT = true, typename Gen>
+template <int K, bool SPLIT = true, int C = kAliasCopies, typename Gen>
 __device__ __forceinline__ void alias_words(const uint32_t (&need)[K], AliasRef ar, uint32_t (&bern)[K], Gen&& gen) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) bern[k] = alias_word<SPLIT>(gen(k, 0), ar, need[k]);
+  for (int k = 0; k < K; ++k) bern[k] = alias_word<SPLIT, C>(gen(k, 0), ar, need[k]);
 }
 
 // Warp-cooperative exact Bernoulli masks for one Type I event: every lane

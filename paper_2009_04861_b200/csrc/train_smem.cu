@@ -183,7 +183,7 @@ __device__ __forceinline__ void type_i_smem_out(SP& S, const LitRow<NW>& r, cons
     if (before && !P.alias_sel) {
       bernoulli_words<2, true>(need, sel, P.bern, bern, gen);
     } else {
-      alias_words<2, false>(need, aref, bern, gen);
+      alias_words<2, false, kSmemAliasCopies>(need, aref, bern, gen);
       if (before) {
         bern[0] = (bern[0] ^ sel[0]) & need[0];
         bern[1] = (bern[1] ^ sel[1]) & need[1];
@@ -316,7 +316,7 @@ __device__ __forceinline__ void smem_clause(const TrainParams& P, uint32_t* slot
 
 
 // One warp per clause, blockDim.x / 32 clauses per CTA; dynamic shared memory
-// = the clauses' planes, then kAliasCopies copies of the alias table.
+// = the clauses' planes, then kSmemAliasCopies copies of the alias table.
 // INPLACE (rows whose planes exceed shared memory, beyond ~107k features at
 // 8 planes): one clause per CTA, the planes stay in HBM/L2 and are updated in
 // place (every word is lane-owned), shared memory holds the alias table only.
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(32 * kSmemMaxCpb) train_async_smem_kernel(Trai
   fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const AliasRef aref = lane_alias(atab, lane);
+  const AliasRef aref = lane_alias<kSmemAliasCopies>(atab, lane);
   const int wib = threadIdx.x >> 5;
   const int w = P.w_begin + blockIdx.x * cpb + wib;
   if (w >= P.w_end) return;
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(32 * kSmemPersistMax, 1) train_async_smem_pers
   fill_alias_packed(atab, P.alias8, threadIdx.x, blockDim.x);
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const AliasRef aref = lane_alias(atab, lane);
+  const AliasRef aref = lane_alias<kSmemAliasCopies>(atab, lane);
   uint32_t* slot = smem + (threadIdx.x >> 5) * words;
   const int total = P.w_end - P.w_begin;
   while (true) {
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(32) type_i_smem_once_kernel(TrainParams P, uin
   SP S{smem, Wp};
   LitRow<NW> r;
   r.load(P.xplane + lane, Wp);
-  type_i_smem<NW, B, P2>(S, r, out, P, g, i, lane, lane_alias(atab, lane));
+  type_i_smem<NW, B, P2>(S, r, out, P, g, i, lane, lane_alias<kSmemAliasCopies>(atab, lane));
   __syncwarp();
   for (size_t k = lane; k < words; k += 32) state[k] = smem[at(k)];
 }
