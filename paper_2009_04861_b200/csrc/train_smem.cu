@@ -17,7 +17,7 @@
 #include "tm_device.cuh"
 
 #ifndef TMG_SMEM_UNROLL
-#define TMG_SMEM_UNROLL 2  // word pairs of a Type I feedback processed together (ILP at low occupancy)
+#define TMG_SMEM_UNROLL 5  // word pairs of a Type I feedback processed together (ILP at low occupancy; IMDb: 1 / 2 / 4 / 5 / 10 -> 214 / 203 / 200 / 198.5 / 284 ms)
 #endif
 
 namespace tmg {
