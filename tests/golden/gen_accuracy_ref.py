@@ -52,7 +52,7 @@ CASES = {
     "mnist_q60000_w2": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
                             noise=0.0, data_seed=2009, workers=2, seeds=3),
     "mnist_q60000_w4": dict(data="mnist", q=60000, qtest=10000, clauses=2000, T=50, s=10.0, epochs=3,
-                            noise=0.0, data_seed=2009, workers=4, seeds=2),
+                            noise=0.0, data_seed=2009, workers=4, seeds=3),
 }
 
 
