@@ -61,6 +61,10 @@ struct Clause {
 
   bool nonempty = false;  // include count > 0, refreshed by every eval_train
 
+  // Row word of slot p held by this lane (x plane; !x is the same word of
+  // the second half).
+  __device__ __forceinline__ int word_of(int p, int lane) const { return p * 32 + lane; }
+
   // Train-mode evaluation (core.hpp:208-219): empty clause -> 1.
   __device__ __forceinline__ int eval_train(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) {
     uint32_t viol = 0, any = 0;
@@ -123,6 +127,116 @@ struct Clause {
   __device__ __forceinline__ void type_i_word(int part, int p, uint32_t lit, int out, int boost,
                                               uint32_t bern, uint32_t lo, uint32_t hi) {
     type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(s[part][p], lit, out, boost, bern, valid[p], lo, hi);
+  }
+};
+
+// The same clause with the last word slot PACKED (rows whose last slot has
+// R <= 16 valid words, e.g. FMNIST's 74 words = 2 full slots + 10): lanes
+// 0..R-1 hold that slot's x-part words, lanes R..2R-1 its !x-part words, the
+// rest a padding word of the x part (never valid). Type I then draws 2NW - 1
+// word slots per lane instead of 2NW, with the same Philox counters (keyed by
+// word and part, not by lane), so the automata move exactly as in Clause.
+// Rows are read x-only: n[p] = ~x[p] (TMG_ROW_X_ONLY).
+template <int NW, int B, bool P2 = false>
+struct ClausePk {
+  static_assert(NW >= 2, "packing needs a full slot before the last");
+  Planes<B> s[2][NW - 1];  // full slots [part][pass]
+  Planes<B> pk;            // the packed slot
+  uint32_t valid[NW - 1];
+  uint32_t vpk;
+  int pk_part, pk_w;  // part and row word of this lane's packed-slot word
+  bool nonempty = false;
+
+  __device__ __forceinline__ int word_of(int p, int lane) const { return p < NW - 1 ? p * 32 + lane : pk_w; }
+  __device__ __forceinline__ static uint32_t valid_bits_of(int wi, int o) {
+    const int first = wi * 32;
+    return first >= o ? 0u : (o - first >= 32 ? kFull : ((1u << (o - first)) - 1u));
+  }
+  // The literal value word of the packed slot: x for part 0, !x for part 1.
+  __device__ __forceinline__ uint32_t pk_lit(const uint32_t (&x)[NW]) const {
+    return pk_part ? ~x[NW - 1] : x[NW - 1];
+  }
+
+  __device__ __forceinline__ void load(const uint32_t* base, int Wp, int lane, int o) {
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) {
+      const int wi = p * 32 + lane;
+      valid[p] = valid_bits_of(wi, o);
+#pragma unroll
+      for (int part = 0; part < 2; ++part)
+#pragma unroll
+        for (int b = 0; b < B; ++b) s[part][p].p[b] = base[(b * 2 + part) * Wp + wi];
+    }
+    const int R = (o + 31) / 32 - 32 * (NW - 1);  // valid words of the last slot (<= 16)
+    const int last = 32 * (NW - 1);
+    pk_part = lane >= R && lane < 2 * R ? 1 : 0;
+    pk_w = last + (lane < R ? lane : (lane < 2 * R ? lane - R : lane - R));  // idle: padding words of part 0
+    vpk = lane < 2 * R ? valid_bits_of(pk_w, o) : 0u;
+#pragma unroll
+    for (int b = 0; b < B; ++b) pk.p[b] = base[(b * 2 + pk_part) * Wp + pk_w];
+  }
+
+  __device__ __forceinline__ void store(uint32_t* base, int Wp, int lane) const {
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p)
+#pragma unroll
+      for (int part = 0; part < 2; ++part)
+#pragma unroll
+        for (int b = 0; b < B; ++b) base[(b * 2 + part) * Wp + p * 32 + lane] = s[part][p].p[b];
+#pragma unroll
+    for (int b = 0; b < B; ++b) base[(b * 2 + pk_part) * Wp + pk_w] = pk.p[b];
+  }
+
+  __device__ __forceinline__ uint32_t violations(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) const {
+    uint32_t viol = pk.p[B - 1] & ~pk_lit(x);
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) viol |= (s[0][p].p[B - 1] & ~x[p]) | (s[1][p].p[B - 1] & ~n[p]);
+    return viol;
+  }
+  __device__ __forceinline__ int eval_train(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) {
+    const uint32_t viol = violations(x, n);
+    uint32_t any = pk.p[B - 1];
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) any |= s[0][p].p[B - 1] | s[1][p].p[B - 1];
+    const unsigned vb = __ballot_sync(kFull, viol != 0);
+    nonempty = __any_sync(kFull, any != 0);
+    return !nonempty ? 1 : (vb == 0 ? 1 : 0);
+  }
+  __device__ __forceinline__ int eval_cached(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) const {
+    const unsigned vb = __ballot_sync(kFull, violations(x, n) != 0);
+    return !nonempty ? 1 : (vb == 0 ? 1 : 0);
+  }
+  __device__ __forceinline__ void refresh_nonempty() {
+    uint32_t any = pk.p[B - 1];
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) any |= s[0][p].p[B - 1] | s[1][p].p[B - 1];
+    nonempty = __any_sync(kFull, any != 0);
+  }
+  __device__ __forceinline__ int include_count() const {
+    int cnt = __popc(pk.p[B - 1]);
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) cnt += __popc(s[0][p].p[B - 1]) + __popc(s[1][p].p[B - 1]);
+#pragma unroll
+    for (int off = 16; off; off >>= 1) cnt += __shfl_xor_sync(kFull, cnt, off);
+    return cnt;
+  }
+  // Type II (feedback.cpp:72-83), as Clause::type_ii.
+  __device__ __forceinline__ bool type_ii(const uint32_t (&x)[NW], const uint32_t (&n)[NW]) {
+    uint32_t moved = 0;
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) {
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const uint32_t lit = part ? n[p] : x[p];
+        const uint32_t inc = ~lit & ~s[part][p].p[B - 1] & valid[p];
+        add_one<B>(s[part][p], inc);
+        moved |= inc;
+      }
+    }
+    const uint32_t inc = ~pk_lit(x) & ~pk.p[B - 1] & vpk;
+    add_one<B>(pk, inc);
+    moved |= inc;
+    return __any_sync(kFull, moved != 0);
   }
 };
 
@@ -249,6 +363,50 @@ __device__ __forceinline__ void type_i_async(Clause<NW, B, P2>& cl, const uint32
       cl.type_i_word(0, p, x[p], 0, P.boost, bern[2 * p], P.lo, P.hi);
       cl.type_i_word(1, p, n[p], 0, P.boost, bern[2 * p + 1], P.lo, P.hi);
     }
+  }
+}
+
+// Type I on a packed clause: the full slots as in type_i_async, the packed
+// slot as one more word slot with its own (word, part) counter. Clause-output-1
+// draws take the alias table only (the launcher packs only when alias_sel).
+template <int NW, int B, bool P2>
+__device__ __forceinline__ void type_i_async(ClausePk<NW, B, P2>& cl, const uint32_t (&x)[NW],
+                                             const uint32_t (&n)[NW], int before, const TrainParams& P, uint32_t g,
+                                             uint32_t i, int lane, AliasRef atab) {
+  constexpr int K = 2 * NW - 1;
+  uint32_t need[K], sel[K], bern[K];
+#pragma unroll
+  for (int p = 0; p < NW - 1; ++p) {
+    need[2 * p] = need[2 * p + 1] = cl.valid[p];
+    sel[2 * p] = x[p];
+    sel[2 * p + 1] = n[p];
+  }
+  need[K - 1] = cl.vpk;
+  sel[K - 1] = cl.pk_lit(x);
+  const uint32_t wid_pk = static_cast<uint32_t>(cl.pk_w * 2 + cl.pk_part);
+  auto gen = [&](int slot, int blk) {
+    const uint32_t wid = slot < K - 1 ? static_cast<uint32_t>(((slot >> 1) * 32 + lane) * 2 + (slot & 1)) : wid_pk;
+    return philox4x32(U4{g, i, wid, static_cast<uint32_t>(blk)}, P.rkey);
+  };
+  alias_words<K>(need, atab, bern, gen);
+  if (before) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) bern[k] = (bern[k] ^ sel[k]) & need[k];
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) {
+      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[0][p], x[p], 1, P.boost, bern[2 * p], cl.valid[p], P.lo, P.hi);
+      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[1][p], n[p], 1, P.boost, bern[2 * p + 1], cl.valid[p], P.lo,
+                                                  P.hi);
+    }
+    type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.pk, sel[K - 1], 1, P.boost, bern[K - 1], cl.vpk, P.lo, P.hi);
+  } else {
+#pragma unroll
+    for (int p = 0; p < NW - 1; ++p) {
+      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[0][p], x[p], 0, P.boost, bern[2 * p], cl.valid[p], P.lo, P.hi);
+      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[1][p], n[p], 0, P.boost, bern[2 * p + 1], cl.valid[p], P.lo,
+                                                  P.hi);
+    }
+    type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.pk, sel[K - 1], 0, P.boost, bern[K - 1], cl.vpk, P.lo, P.hi);
   }
 }
 

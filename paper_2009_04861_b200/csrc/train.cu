@@ -14,6 +14,8 @@
 //   train_mirror : one warp replays the reference's W-worker schedule with the
 //                  reference xoshiro streams, bit-exact (sync mirror mode).
 #include <cstdio>
+#include <cstdlib>
+#include <type_traits>
 
 #include "clause.cuh"
 #include "kernels.h"
@@ -36,7 +38,7 @@ constexpr int async_min_blocks(int NW, int B) {
 #else
 #define TMG_ASYNC_BOUNDS __launch_bounds__(128, TMG_ASYNC_MINB)
 #endif
-template <int NW, int B, bool P2>
+template <int NW, int B, bool P2, bool PACK = false>
 __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   __shared__ uint32_t atab[TMG_ALIAS ? kAliasWords : 1];
   load_alias(P, atab);
@@ -50,7 +52,7 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
   const uint32_t g = static_cast<uint32_t>(c) * P.n + j;
   const bool positive = P.all_positive || (j & 1) == 0;
 
-  Clause<NW, B, P2> cl;
+  std::conditional_t<PACK, ClausePk<NW, B, P2>, Clause<NW, B, P2>> cl;
   uint32_t* st = P.state + static_cast<size_t>(lc) * B * 2 * P.Wp;
   cl.load(st, P.Wp, lane, P.o);
   cl.refresh_nonempty();
@@ -90,16 +92,16 @@ __global__ void TMG_ASYNC_BOUNDS train_async_kernel(TrainParams P) {
       cd = __shfl_sync(kFull, code, l);
       // Literal rows are [x words | !x words] (2 * Wp words, nplane = xplane
       // + Wp): one address, both planes at compile-time offsets.
-      const uint32_t* rp = P.xplane + static_cast<size_t>(cd < 0 ? ~cd : cd) * (64 * NW) + lane;
+      const uint32_t* rp = P.xplane + static_cast<size_t>(cd < 0 ? ~cd : cd) * (64 * NW);
 #pragma unroll
       for (int p = 0; p < NW; ++p) {
-        xs[p] = __ldg(rp + p * 32);
+        xs[p] = __ldg(rp + cl.word_of(p, lane));
         // !x words as ~x (TMG_ROW_X_ONLY, rows of >= TMG_ROW_X_MIN_NW words
         // per lane): the bits past o differ from the stored !x plane (0
         // there) but every use is masked by the valid bits or meets an
         // include bit, which is never set past o.
-        if constexpr (TMG_ROW_X_ONLY && NW >= TMG_ROW_X_MIN_NW) ns[p] = ~xs[p];
-        else ns[p] = __ldg(rp + 32 * NW + p * 32);
+        if constexpr (PACK || (TMG_ROW_X_ONLY && NW >= TMG_ROW_X_MIN_NW)) ns[p] = ~xs[p];
+        else ns[p] = __ldg(rp + 32 * NW + p * 32 + lane);
       }
     };
     auto run = [&](const uint32_t (&xs)[NW], const uint32_t (&ns)[NW], int cd, uint32_t sl) {
@@ -615,22 +617,31 @@ __global__ void __launch_bounds__(128) feedback_rates_kernel(TrainParams P, cons
 // applies it) on the clause planes at `state`, literal row 0 of P, Philox
 // counters (clause g, example i): the deterministic unit the async sampler's
 // bit-exact parity test checks against oracle/tm_oracle.c:tm_async_type_i.
-template <int NW, int B, bool P2>
+template <int NW, int B, bool P2, bool PACK = false>
 __global__ void __launch_bounds__(32) type_i_async_once_kernel(TrainParams P, uint32_t* state, uint32_t g,
                                                                uint32_t i, int out) {
   __shared__ uint32_t atab[TMG_ALIAS ? kAliasWords : 1];
   load_alias(P, atab);
   const int lane = threadIdx.x;
-  Clause<NW, B, P2> cl;
+  std::conditional_t<PACK, ClausePk<NW, B, P2>, Clause<NW, B, P2>> cl;
   cl.load(state, P.Wp, lane, P.o);
   uint32_t x[NW], n[NW];
 #pragma unroll
   for (int p = 0; p < NW; ++p) {
-    x[p] = P.xplane[p * 32 + lane];
-    n[p] = P.nplane[p * 32 + lane];
+    x[p] = P.xplane[cl.word_of(p, lane)];
+    n[p] = PACK ? ~x[p] : P.nplane[p * 32 + lane];
   }
   type_i_async<NW, B, P2>(cl, x, n, out, P, g, i, lane, lane_alias(atab, lane));
   cl.store(state, P.Wp, lane);
+}
+
+// Pack the last word slot (ClausePk) when it holds at most 16 valid words and
+// the clause-output-1 draws use the alias table; TMG_ASYNC_PACK=0 disables it
+// (A/B checks).
+bool pack_last_slot(const TrainParams& p, int NW) {
+  const char* e = std::getenv("TMG_ASYNC_PACK");
+  if ((e && e[0] == '0') || NW < 2 || !TMG_ALIAS || !TMG_ROW_X_ONLY || !p.alias_sel) return false;
+  return (p.o + 31) / 32 - 32 * (NW - 1) <= 16;
 }
 
 template <int NW, int B>
@@ -640,7 +651,15 @@ void launch_async(const TrainParams& p, cudaStream_t s, int* blocks) {
   const int grid = (clauses + warps_per_block - 1) / warps_per_block;
   if (blocks) *blocks = grid;
   count_launch();
-  if (TMG_ASYNC_P2 && p.lo == 0 && p.hi == (1u << B) - 1u)
+  const bool p2 = TMG_ASYNC_P2 && p.lo == 0 && p.hi == (1u << B) - 1u;
+  if constexpr (NW >= 2) {
+    if (pack_last_slot(p, NW)) {
+      if (p2) train_async_kernel<NW, B, true, true><<<grid, 32 * warps_per_block, 0, s>>>(p);
+      else train_async_kernel<NW, B, false, true><<<grid, 32 * warps_per_block, 0, s>>>(p);
+      return;
+    }
+  }
+  if (p2)
     train_async_kernel<NW, B, true><<<grid, 32 * warps_per_block, 0, s>>>(p);
   else
     train_async_kernel<NW, B, false><<<grid, 32 * warps_per_block, 0, s>>>(p);
@@ -731,6 +750,15 @@ bool feedback_rates_launch(const TrainParams& p, const uint32_t* state0, int out
   return false;
 }
 
+template <int NW, int B, typename Go>
+bool once_dispatch(const TrainParams& p, bool p2, Go&& go) {
+  if constexpr (NW >= 2) {
+    if (pack_last_slot(p, NW))
+      return p2 ? go(type_i_async_once_kernel<NW, B, true, true>) : go(type_i_async_once_kernel<NW, B, false, true>);
+  }
+  return p2 ? go(type_i_async_once_kernel<NW, B, true>) : go(type_i_async_once_kernel<NW, B, false>);
+}
+
 bool type_i_async_once_launch(const TrainParams& p, uint32_t* state, uint32_t g, uint32_t i, int out, int B, int NW,
                               cudaStream_t s) {
   const bool p2 = TMG_ASYNC_P2 && p.lo == 0 && p.hi == (1u << B) - 1u;
@@ -739,9 +767,8 @@ bool type_i_async_once_launch(const TrainParams& p, uint32_t* state, uint32_t g,
     kern<<<1, 32, 0, s>>>(p, state, g, i, out);
     return true;
   };
-#define TMG_ONCE(nw, b)                                                            \
-  if (NW == nw && B == b)                                                          \
-    return p2 ? go(type_i_async_once_kernel<nw, b, true>) : go(type_i_async_once_kernel<nw, b, false>);
+#define TMG_ONCE(nw, b) \
+  if (NW == nw && B == b) return once_dispatch<nw, b>(p, p2, go);
   TMG_ONCE(1, 4) TMG_ONCE(1, 8) TMG_ONCE(1, 15) TMG_ONCE(2, 4) TMG_ONCE(2, 8) TMG_ONCE(2, 15)
   TMG_ONCE(3, 4) TMG_ONCE(3, 8) TMG_ONCE(3, 15) TMG_ONCE(4, 4) TMG_ONCE(4, 8) TMG_ONCE(4, 15)
 #undef TMG_ONCE
