@@ -14,8 +14,12 @@
 #ifndef TMG_ASYNC_UNROLL_NW
 #define TMG_ASYNC_UNROLL_NW 1  // widest rows (words per lane) that get the 2x unrolled step loop
 #endif
-#ifndef TMG_STEP_SAT_REG
-#define TMG_STEP_SAT_REG 0  // register kernels: clause-output-1 Type I as two passes (tm_device.cuh type_i_planes)
+#ifndef TMG_STEP_SAT_REG_NW
+// Register kernels: clause-output-1 Type I as ONE up/down saturating pass
+// (tm_device.cuh type_i_planes FUSED) for rows of at least this many words per
+// lane, two passes below (MNIST 1-word rows: 67.6 vs 68.3 ms fused; FMNIST
+// 3-word rows: 524 vs 559 ms fused).
+#define TMG_STEP_SAT_REG_NW 2
 #endif
 #ifndef TMG_ROW_X_ONLY
 #define TMG_ROW_X_ONLY 1  // async kernels read the x half of a literal row only (!x = ~x)
@@ -126,7 +130,7 @@ struct Clause {
   // Type I on word slot p of part `part` (tm_device.cuh type_i_planes).
   __device__ __forceinline__ void type_i_word(int part, int p, uint32_t lit, int out, int boost,
                                               uint32_t bern, uint32_t lo, uint32_t hi) {
-    type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(s[part][p], lit, out, boost, bern, valid[p], lo, hi);
+    type_i_planes<B, P2, (NW >= TMG_STEP_SAT_REG_NW)>(s[part][p], lit, out, boost, bern, valid[p], lo, hi);
   }
 };
 
@@ -394,19 +398,19 @@ __device__ __forceinline__ void type_i_async(ClausePk<NW, B, P2>& cl, const uint
     for (int k = 0; k < K; ++k) bern[k] = (bern[k] ^ sel[k]) & need[k];
 #pragma unroll
     for (int p = 0; p < NW - 1; ++p) {
-      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[0][p], x[p], 1, P.boost, bern[2 * p], cl.valid[p], P.lo, P.hi);
-      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[1][p], n[p], 1, P.boost, bern[2 * p + 1], cl.valid[p], P.lo,
+      type_i_planes<B, P2, (NW >= TMG_STEP_SAT_REG_NW)>(cl.s[0][p], x[p], 1, P.boost, bern[2 * p], cl.valid[p], P.lo, P.hi);
+      type_i_planes<B, P2, (NW >= TMG_STEP_SAT_REG_NW)>(cl.s[1][p], n[p], 1, P.boost, bern[2 * p + 1], cl.valid[p], P.lo,
                                                   P.hi);
     }
-    type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.pk, sel[K - 1], 1, P.boost, bern[K - 1], cl.vpk, P.lo, P.hi);
+    type_i_planes<B, P2, (NW >= TMG_STEP_SAT_REG_NW)>(cl.pk, sel[K - 1], 1, P.boost, bern[K - 1], cl.vpk, P.lo, P.hi);
   } else {
 #pragma unroll
     for (int p = 0; p < NW - 1; ++p) {
-      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[0][p], x[p], 0, P.boost, bern[2 * p], cl.valid[p], P.lo, P.hi);
-      type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.s[1][p], n[p], 0, P.boost, bern[2 * p + 1], cl.valid[p], P.lo,
+      type_i_planes<B, P2, (NW >= TMG_STEP_SAT_REG_NW)>(cl.s[0][p], x[p], 0, P.boost, bern[2 * p], cl.valid[p], P.lo, P.hi);
+      type_i_planes<B, P2, (NW >= TMG_STEP_SAT_REG_NW)>(cl.s[1][p], n[p], 0, P.boost, bern[2 * p + 1], cl.valid[p], P.lo,
                                                   P.hi);
     }
-    type_i_planes<B, P2, TMG_STEP_SAT_REG != 0>(cl.pk, sel[K - 1], 0, P.boost, bern[K - 1], cl.vpk, P.lo, P.hi);
+    type_i_planes<B, P2, (NW >= TMG_STEP_SAT_REG_NW)>(cl.pk, sel[K - 1], 0, P.boost, bern[K - 1], cl.vpk, P.lo, P.hi);
   }
 }
 
