@@ -264,6 +264,9 @@ def test_type_i_table1_conformance(o, N, s, boost, out):
 @pytest.mark.parametrize("o,N,s,boost", [(784, 128, 10.0, False), (784, 128, 10.0, True), (784, 100, 10.0, False),
                                          (12, 128, 3.9, False), (40, 5, 2.0, True), (2352, 128, 15.0, False),
                                          (1500, 300, 7.5, False), (2000, 128, 1.0, False),
+                                         # the packed last word slot at its edge: 16 valid words
+                                         # (packed) and 17 (plain), ClausePk in csrc/clause.cuh
+                                         (1536, 128, 10.0, False), (1537, 128, 10.0, True),
                                          (5000, 128, 15.0, False), (10000, 128, 15.0, True),
                                          (9000, 100, 25.0, False), (15000, 128, 10.0, False),
                                          (20000, 128, 10.0, False), (40000, 5, 3.0, True)])
