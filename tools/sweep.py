@@ -67,6 +67,10 @@ def run(kind, clauses_list, q, qt, T_, s, epochs=2):
     pool = T.ExamplePool(d.features, d.train_x, d.train_y, d.classes)
     test = T.ExamplePool(d.features, d.test_x, d.test_y, d.classes) if qt else None
     m, o = d.classes, d.features
+    # the shape's own kernels (row width, packing, shared-memory plan) loaded
+    # and their launch attributes set before the first timed epoch
+    wpool = T.ExamplePool(o, d.train_x[:256], d.train_y[:256], m)
+    T.train_epoch_parallel(T.MultiClassTM(T.TMConfig(clauses=8, margin=T_, specificity=s, seed=1), o, m), wpool, 1, 0)
     for n in clauses_list:
         tm = T.MultiClassTM(T.TMConfig(clauses=n, margin=T_, specificity=s, seed=42), o, m)
         pool.reset_tallies()
