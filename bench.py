@@ -263,12 +263,22 @@ def other_configs(local):
             torch.cuda.synchronize()
             if r:
                 pms.append(e0.elapsed_time(e1))
-        out.append({"workload": f"{kind} {d.features}b x {d.classes}c x {n} clauses, q={q}, fresh epoch 0",
-                    "ms_per_epoch": t * 1e3, "examples_per_s": q / t,
-                    "clause_literal_evals_per_s": d.classes * n * q * 2.0 * d.features / t,
-                    "feedback_events": rep.total_feedback_events(),
-                    "predict_test_rows": qt, "predict_ms": min(pms),
-                    "test_accuracy_after_epoch0": T.evaluate_accuracy(tm, test)})
+        rec = {"workload": f"{kind} {d.features}b x {d.classes}c x {n} clauses, q={q}, fresh epoch 0",
+               "ms_per_epoch": t * 1e3, "examples_per_s": q / t,
+               "clause_literal_evals_per_s": d.classes * n * q * 2.0 * d.features / t,
+               "feedback_events": rep.total_feedback_events(),
+               "predict_test_rows": qt, "predict_ms": min(pms),
+               "test_accuracy_after_epoch0": T.evaluate_accuracy(tm, test)}
+        # the committed ncu capture of this shape's training kernel (same
+        # command shape, tools/gpu_final_r2.sh): pipe use and DRAM per launch
+        prof = os.path.join(REPO, "profiles", {"fmnist": "r2w_fmnist_async.json", "imdb": "r2w_imdb_smem.json"}[kind])
+        if os.path.exists(prof):
+            pj = json.load(open(prof))
+            rec["ncu"] = {k: pj.get(k) for k in ("kernel", "duration_ms", "pipe_alu_pct", "issue_active_pct",
+                                                  "dram_bytes_per_launch", "registers_per_thread",
+                                                  "occupancy_achieved_pct")}
+            rec["ncu"]["source"] = os.path.relpath(prof, REPO)
+        out.append(rec)
         del tm, pool, test
     return out
 
